@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for libwn (arXiv 2510.25159 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl wn|reference]
+
+Metric (BASELINE.json): winding-number queries/s (and query*segment pairs/s,
+% of the FP64 pipe roofline).  Workload: BASELINE configs[4] = C5, the largest
+single-GPU config (20,000 synthetic B-Rep faces, 64x64 uv grid per face =
+81.92M queries, degree 1-5 rational Bezier p-curves, 30% periodic in u),
+seeded synthetic data (wn_workloads.configs.gen_c5; the paper's datasets are not
+in the container).  One STEP = one pass of the whole hot path over the batch:
+wn_build_faces (segment prep K1, lifting K2a, planning, emission K2c) +
+wn_query (bucketing K4 + query kernel K3) + wn_free_faces, inputs resident in
+HBM.  Inputs (1.64 GB of queries) are larger than L2, so no flush is needed.
+
+N > 1 (torchrun): weak scaling, every rank runs its own independent C5 batch
+(seed 5 + rank); no data-path collective; the timed region is
+bracketed by barriers and the max over ranks is reported.
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed as it
+stands on the host cores, each step a bounded sample of the same workload.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "winding-number queries/sec and query·segment pairs/sec; % of FP64 pipe peak"
+UNIT = "queries/s"
+WORKLOAD = ("C5 synthetic B-Rep batch / tessellation: 20000 faces, loops 1-8 (geometric), "
+            "segments/loop 4-128 (log-uniform), degree 1-5 rational Bezier, 30% periodic in u, "
+            "64x64 uv grid per face (81,920,000 queries), fp64")
+
+# FP64 roofline: B200 = 148 SMs x 64 FP64 lanes/clk,
+# FMA = 2 flops, at the 1965 MHz max SM clock (MEASURED_PEAKS.json sm_max_mhz).
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# Algorithmic FP64 flops per unit of K3 work, this implementation (crossing
+# mode), counted from the SASS of k_query<double> (DESIGN.md "K3 work per
+# unit"; ncu cross-check in profiles/): per (query, segment) pair tested in
+# phase 1, per recursion node, per midpoint evaluation (degree-weighted mean).
+FLOPS_PER_PAIR = 14.0
+FLOPS_PER_NODE = 13.0
+FLOPS_PER_EVAL = 40.0
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def _clock_sampler(gpu_index):
+    cmd = ["nvidia-smi", "-i", str(gpu_index),
+           "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+           "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+           "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+           "--format=csv,noheader,nounits", "-lms", "50"]
+    try:
+        return subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except OSError:
+        return None
+
+
+def _clock_summary(proc, t0, t1):
+    if proc is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        proc.kill()
+        out = ""
+    rows = []
+    for line in out.strip().splitlines():
+        parts = [p.strip() for p in line.split(",")]
+        if len(parts) < 9:
+            continue
+        try:
+            ts = time.mktime(time.strptime(parts[0].split(".")[0], "%Y/%m/%d %H:%M:%S"))
+            rows.append((ts, float(parts[1]), float(parts[2]), parts[5:9]))
+        except Exception:
+            continue
+    inwin = [r for r in rows if t0 - 1.0 <= r[0] <= t1 + 1.0] or rows
+    if not inwin:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    reasons = sorted({names[i] for r in inwin for i, v in enumerate(r[3]) if v.lower() == "active"})
+    return {"sm_mhz": statistics.median(r[1] for r in inwin), "sm_max_mhz": max(r[2] for r in inwin),
+            "reasons": reasons, "samples": len(inwin)}
+
+
+def _cpu_baseline(wl, target_s, rank_seed=0):
+    """Oracle (as it stands) on a bounded random sample of the same workload."""
+    import oracle
+    cores = os.cpu_count() or 1
+    rng = np.random.default_rng(1234 + rank_seed)
+    nq = len(wl["face_id"])
+    pilot = rng.choice(nq, size=min(nq, 256), replace=False)
+    t = time.perf_counter()
+    oracle.query(wl, face_id=wl["face_id"][pilot], uv=wl["uv"][pilot], nthreads=cores)
+    tp = time.perf_counter() - t
+    rate = len(pilot) / max(tp, 1e-6)
+    m = int(min(nq, max(512, rate * target_s)))
+    idx = np.sort(rng.choice(nq, size=m, replace=False))
+    t = time.perf_counter()
+    oracle.query(wl, face_id=wl["face_id"][idx], uv=wl["uv"][idx], nthreads=cores)
+    dt = time.perf_counter() - t
+    return {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": "%d random queries of the C5 batch (all faces eligible), one oracle call incl. its "
+                      "own lifting/pairing of all faces, %.1f s wall" % (m, dt)}, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from wn_workloads import configs as G
+    wl = G.gen_c5(seed=5)
+    import oracle
+    cores = os.cpu_count() or 1
+    # size one step as a bounded sample (~ a few seconds per step)
+    rng = np.random.default_rng(99)
+    nq = len(wl["face_id"])
+    pilot = rng.choice(nq, size=256, replace=False)
+    t = time.perf_counter()
+    oracle.query(wl, face_id=wl["face_id"][pilot], uv=wl["uv"][pilot], nthreads=cores)
+    rate = 256 / max(time.perf_counter() - t, 1e-6)
+    per_step = int(max(512, min(nq, rate * args.ref_step_s)))
+    samples = [np.sort(rng.choice(nq, size=per_step, replace=False)) for _ in range(args.warmup + args.steps)]
+    for i in range(args.warmup):
+        oracle.query(wl, face_id=wl["face_id"][samples[i]], uv=wl["uv"][samples[i]], nthreads=cores)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        oracle.query(wl, face_id=wl["face_id"][samples[i]], uv=wl["uv"][samples[i]], nthreads=cores)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample_per_step": per_step},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "%d random C5 queries per step, %d steps" % (per_step, args.steps)},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wn", choices=["wn", "reference"])
+    ap.add_argument("--angle-mode", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=6.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "wn" and not os.environ.get("WN_BENCH_ALLOW_SHORT"):
+        args.warmup = 3
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2510_25159_b200 as wn
+    from wn_workloads import configs as G
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = G.gen_c5(seed=5 + rank)
+    nq = len(wl["face_id"])
+    pairs = G.n_input_pairs(wl)
+    st = torch.cuda.current_stream(dev)
+    T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    geo_np = [wl["ctrl_uv"], wl["ctrl_w"], wl["seg_degree"], wl["loop_seg_off"], wl["face_loop_off"],
+              wl["face_periodic"], wl["face_domain"]]
+    geo_dt = [torch.float64, torch.float64, torch.int32, torch.int32, torch.int32, torch.uint8, torch.float64]
+    geo = [T(a, d) for a, d in zip(geo_np, geo_dt)]
+    fid = T(wl["face_id"], torch.int32)
+    uv = T(wl["uv"], torch.float64)
+    wnd = torch.empty(nq, dtype=torch.float64, device=dev)
+    flg = torch.empty(nq, dtype=torch.uint8, device=dev)
+    kw = dict(angle_mode=args.angle_mode, device=dev)
+
+    launches = {"build": 0, "query": 0}
+
+    def step(timing=False):
+        faces = wn.Faces.build(*geo, **kw)
+        launches["build"] = wn.last_build_launches()
+        if timing:
+            faces.set_timing(True)
+        faces.query_raw(nq, fid.data_ptr(), uv.data_ptr(), wnd.data_ptr(), flg.data_ptr(), st.cuda_stream)
+        launches["query"] = wn.last_query_launches()
+        k3 = None
+        if timing:
+            k3 = faces
+        else:
+            faces.close()
+        return k3
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K full steps ----
+    clk = _clock_sampler(local) if rank == 0 else None
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    tw0 = time.time()
+    e0.record(st)
+    k3_ms, k3_n = 0.0, 0
+    for _ in range(args.steps):
+        h = step(timing=True)
+        ms, n = h.timing()        # waits on the K3 events of this step (build already synced)
+        k3_ms += ms
+        k3_n += n
+        h.close()
+    e1.record(st)
+    torch.cuda.synchronize()
+    tw1 = time.time()
+    if dist:
+        dist.barrier()
+    elapsed = e0.elapsed_time(e1)
+    clocks = _clock_summary(clk, tw0, tw1) if rank == 0 else None
+    t_max = elapsed
+    if dist:
+        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    ms_step = t_max / args.steps
+    value = nq * world / (ms_step / 1e3)
+    pairs_s = pairs * world / (ms_step / 1e3)
+    gpu_launches = (launches["build"] + launches["query"]) * args.steps
+
+    # ---- query-only breakdown (untimed for the contract) ----
+    faces = wn.Faces.build(*geo, **kw)
+    for _ in range(2):
+        faces.query_raw(nq, fid.data_ptr(), uv.data_ptr(), wnd.data_ptr(), flg.data_ptr(), st.cuda_stream)
+    torch.cuda.synchronize()
+    q0 = torch.cuda.Event(enable_timing=True)
+    q1 = torch.cuda.Event(enable_timing=True)
+    q0.record(st)
+    nrep = 10
+    for _ in range(nrep):
+        faces.query_raw(nq, fid.data_ptr(), uv.data_ptr(), wnd.data_ptr(), flg.data_ptr(), st.cuda_stream)
+    q1.record(st)
+    torch.cuda.synchronize()
+    q_ms = q0.elapsed_time(q1) / nrep
+    faces.set_counters(True)
+    faces.query_raw(nq, fid.data_ptr(), uv.data_ptr(), wnd.data_ptr(), flg.data_ptr(), st.cuda_stream)
+    cnt = faces.counters()
+    faces.set_counters(False)
+    info = faces.info()
+    flags = np.bincount(flg.cpu().numpy(), minlength=4).tolist()
+    faces.close()
+
+    # ---- e2e: public API with HOST buffers, copies inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
+        h_geo = [pin(a) for a in geo_np]
+        h_fid = pin(wl["face_id"])
+        h_uv = pin(wl["uv"])
+        h_w = torch.empty(nq, dtype=torch.float64).pin_memory()
+        h_f = torch.empty(nq, dtype=torch.uint8).pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in h_geo) + h_fid.numel() * 4 + h_uv.numel() * 8
+        d2h = nq * 9
+
+        def e2e_step():
+            g = [t.to(dev, non_blocking=True) for t in h_geo]
+            f = h_fid.to(dev, non_blocking=True)
+            q = h_uv.to(dev, non_blocking=True)
+            fc = wn.Faces.build(*g, **kw)
+            r = fc.query(f, q)
+            h_w.copy_(r.winding, non_blocking=True)
+            h_f.copy_(r.flag, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            fc.close()
+
+        e2e_step()
+        ksteps = max(3, min(args.steps, 10))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for _ in range(ksteps):
+            e2e_step()
+        b.record(st)
+        torch.cuda.synchronize()
+        et = a.elapsed_time(b)
+        if dist:
+            tt = torch.tensor([et], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        e2e = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
+
+    # ---- roofline of the dominant kernel (K3, k_query) ----
+    k3_avg = k3_ms / max(k3_n, 1)
+    flops = (FLOPS_PER_PAIR * cnt["pairs_tested"] + FLOPS_PER_NODE * cnt["nodes"] +
+             FLOPS_PER_EVAL * cnt["evals"])
+    achieved = flops / (k3_avg / 1e3) / 1e12
+    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "kernel": "wn::k_query<double>", "k3_ms": k3_avg, "k3_share_of_step": k3_avg / ms_step,
+                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 2 x 1.965 GHz (max clock)",
+                "units": {"pairs_tested": cnt["pairs_tested"], "nodes": cnt["nodes"], "evals": cnt["evals"]}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = _cpu_baseline(wl, args.cpu_seconds)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no datasets)",
+                "config": {"workload": WORKLOAD, "queries": nq, "input_segment_pairs": pairs,
+                           "parallelism": "independent batch per GPU" if world > 1 else "single GPU",
+                           "l2": "inputs larger than L2 (1.64 GB queries per step), no flush",
+                           "step": "wn_build_faces + wn_query + wn_free_faces",
+                           "angle_mode": args.angle_mode},
+                "pairs_per_s": pairs_s,
+                "query_only": {"ms": q_ms, "queries_per_s": nq / (q_ms / 1e3), "pairs_per_s": pairs / (q_ms / 1e3)},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "clocks": clocks, "counters": cnt, "faces_info": info, "flags": flags}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,146 @@
+/*
+ * wn.h -- C ABI of libwn: batched generalized-winding-number containment
+ * queries on trimmed faces, B200 (sm_100a) native.
+ *
+ * Problem (Sec. 4.1): "Given a test point p and a set of
+ * trimming curves {gamma_i} ... determine whether p lies within the trimmed
+ * region" by computing the generalized winding number
+ *     omega(p) = (1/2pi) * integral over the boundary of d(theta)
+ * (Sec. 3.2) and classifying p by it.  Curves are (rational) Bezier
+ * p-curves of degree 1..5; faces may be periodic in u and/or v
+ * (cylinder / torus, Sec. 4.3-4.5); loops of periodic faces are
+ * lifted to the universal covering space.
+ *
+ * Memory: every array argument is a DEVICE pointer unless marked [host].  The
+ * caller owns all input and output buffers; the library owns the faces handle
+ * and the records it built.  All GPU work is ordered on the given stream.
+ * Errors: functions return wn_status_t; a message for the calling thread is
+ * available from wn_last_error() until that thread's next libwn call.  No C++
+ * exception crosses this boundary.  Nothing here ever runs on the CPU in place
+ * of the GPU: without a usable CUDA device every call fails with WN_ERR_CUDA.
+ */
+#ifndef WN_H_
+#define WN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct wn_faces_s *wn_faces_t;
+
+typedef enum {
+  WN_OK = 0,
+  WN_ERR_ARG = 1,       /* NULL pointer, bad count, bad CSR, degree not in 1..5, bad option */
+  WN_ERR_GEOM = 2,      /* weight <= 0 or non-finite control point / weight / period */
+  WN_ERR_TOPOLOGY = 3,  /* a face violates Prop. 1 / B.1 / B.3 (see face_status) */
+  WN_ERR_CUDA = 4,      /* CUDA runtime error or no usable device */
+  WN_ERR_NOMEM = 5,     /* device allocation failed */
+  WN_ERR_UNSUPPORTED = 6/* valid input outside what this build implements (see face_status) */
+} wn_status_t;
+
+/* Per-face validation codes written to face_status by wn_build_faces. */
+enum {
+  WN_FACE_OK = 0,
+  WN_FACE_B1 = 1,          /* |class| > 1 on a uni-periodic axis (Prop. B.1) */
+  WN_FACE_UNBALANCED = 2,  /* #A != #B: loops not null-homologous (Prop. 1) */
+  WN_FACE_CLASS = 3,       /* mixed classes or gcd(|p|,|q|) != 1 (Props. B.3/B.4) */
+  WN_FACE_GENERAL_PQ = 4,  /* bi-periodic class (p,q) with p,q both nonzero: not implemented yet */
+  WN_FACE_PAIRING = 5,     /* PairLoops (Alg. 9) found no proper translate */
+  WN_FACE_GEOM = 6         /* bad degree / weight / non-finite data in this face */
+};
+
+typedef struct {                 /* [host] */
+  double eps;       /* on-boundary tolerance (Alg. 1 line 1) in face parameter units;
+                       <= 0 selects the default 1e-10 (fp64) / 1e-6 (fp32)  [reading R1]      */
+  int max_depth;    /* explicit-stack depth cap for Alg. 1's recursion (Lemma 2);
+                       0 selects 48; must be <= 64  [reading R6]                              */
+  int precision;    /* 0 = fp64 records and arithmetic, 1 = fp32 (inputs/outputs stay fp64)   */
+  int rule;         /* 0 = nonzero (|round(w)| >= 1, default), 1 = positive (round(w) >= 1)  [R10] */
+  int angle_mode;   /* 0 = telescoped branch-cut crossings (default),
+                       1 = literal per-chord atan2 (the paper's WindingNumberLineSegment)     */
+  int strict;       /* 1 = reject faces violating Prop. 1 (default); 0 = evaluate an
+                       unbalanced uni-periodic loop set anyway (single extended curves)        */
+} wn_options_t;
+
+/* Build the per-face records (segment prep K1, lifting K2a, copy emission K2c).
+ *   n_faces, n_loops, n_segs >= 0 (n_segs may be 0 only with n_loops == 0).
+ *   ctrl_uv       [sum(deg+1)][2] packed control points in STORED (possibly seam-
+ *                 discontinuous, reading R18) coordinates; the control points of
+ *                 segment s start at the exclusive prefix sum of (deg+1).
+ *   ctrl_w        [sum(deg+1)] weights > 0, or NULL for polynomial segments.
+ *   seg_degree    [n_segs] in 1..5.
+ *   loop_seg_off  [n_loops+1] CSR into segments; segment order = loop orientation
+ *                 (interior to the left).
+ *   face_loop_off [n_faces+1] CSR into loops.
+ *   face_periodic [n_faces] bit0 = periodic in u, bit1 = periodic in v.
+ *   face_domain   [n_faces][4] = (u0, Tu, v0, Tv); T used only on periodic axes (R17).
+ *   opts          [host] options, or NULL for defaults.
+ *   stream        cudaStream_t (0 = legacy default stream).
+ *   out           [host] receives the handle on WN_OK; untouched otherwise.
+ *   face_status   [n_faces] DEVICE int32 or NULL: WN_FACE_* per face.
+ * Performs one stream synchronisation (topology validation / planning).  The
+ * input buffers may be freed once it returns. */
+wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, const double *ctrl_uv,
+                           const double *ctrl_w, const int32_t *seg_degree,
+                           const int32_t *loop_seg_off, const int32_t *face_loop_off,
+                           const uint8_t *face_periodic, const double *face_domain,
+                           const wn_options_t *opts, void *stream, wn_faces_t *out,
+                           int32_t *face_status);
+
+/* Batched query (hot path: bucketing K4 + query kernel K3), fully asynchronous
+ * on `stream`; outputs are valid after the stream is synchronised.
+ *   n        number of queries (>= 0).
+ *   face_id  [n] int32 face index; any order (grouped input skips the sort).
+ *   uv       [n][2] float64 query points; periodic coordinates are reduced into
+ *            the base tile [u0,u0+T) (kept bit-exact when already inside).
+ *   winding  [n] float64 generalized winding number; NaN when flag is 2 or 3.
+ *   flag     [n] uint8: 0 outside, 1 inside, 2 on-boundary (within eps of a curve
+ *            point visited by Alg. 1, or depth cap), 3 invalid query (bad face_id,
+ *            non-finite uv).  Per-query problems never fail the batch.
+ * Concurrent calls on one handle from different streams are allowed. */
+wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face_id, const double *uv,
+                     double *winding, uint8_t *flag, void *stream);
+
+typedef struct {
+  int64_t n_records;     /* hot records (MOVE/SEG/GROUP/LINE/...) over all faces */
+  int64_t n_seg_records; /* SEG records (input segments x emitted lattice copies) */
+  int64_t n_groups;      /* cullable groups (closed loops and extended copies) */
+  int64_t n_lines;       /* LINE records (Eq. 5 / Eq. 8 line terms) */
+  int64_t bytes;         /* device bytes owned by the handle */
+  int32_t precision;     /* 0 fp64, 1 fp32 */
+  int32_t max_face_records;
+} wn_faces_info_t;
+
+wn_status_t wn_faces_info(wn_faces_t faces, wn_faces_info_t *out /* [host] */);
+
+/* Device-side event counters of the last wn_query on this handle, enabled by
+ * wn_set_counters(faces, 1) (adds atomics; for diagnostics, not for timing).
+ * out[host][8] = {pairs_tested, hard_pairs, nodes, evals, leaves, max_depth,
+ *                 groups_culled, on_boundary}. */
+wn_status_t wn_set_counters(wn_faces_t faces, int enable);
+wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [host][8] */);
+
+/* In-library timing of the query kernel K3 (CUDA events recorded on the
+ * launching stream around every K3 launch while enabled).  wn_get_timing
+ * waits for the recorded events, returns the summed K3 milliseconds and the
+ * number of K3 launches since the last wn_get_timing, and resets them. */
+wn_status_t wn_set_timing(wn_faces_t faces, int enable);
+wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, int64_t *k3_launches /* [host] */);
+
+/* Release the handle; the caller guarantees no query on it is in flight. */
+void wn_free_faces(wn_faces_t faces);
+
+/* Thread-local message for the last failing call on this thread ("" if none). */
+const char *wn_last_error(void);
+
+/* Number of kernel launches issued by the last wn_query / wn_build_faces on
+ * this thread (library kernels only; cub scans count as their kernels). */
+int32_t wn_last_query_launches(void);
+int32_t wn_last_build_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WN_H_ */

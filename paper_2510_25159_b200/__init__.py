@@ -1,0 +1,245 @@
+"""paper_2510_25159_b200 -- B200-native batched generalized-winding-number
+containment queries on trimmed faces (arXiv 2510.25159).
+
+Thin ctypes binding over the C ABI in include/wn.h (libwn.so, built in-tree for
+sm_100a).  This module only marshals arguments: every step of the path runs in
+the CUDA kernels of libwn.  There is no CPU fallback: without the extension or
+without a CUDA device every entry point raises.
+
+    import paper_2510_25159_b200 as wn
+    faces = wn.Faces.build(ctrl_uv, ctrl_w, seg_degree, loop_seg_off, face_loop_off,
+                           face_periodic, face_domain)        # torch CUDA tensors or numpy
+    winding, flag = faces.query(face_id, uv)                   # torch CUDA tensors
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIBPATH = os.path.join(_HERE, "libwn.so")
+_lib = None
+
+WN_OK = 0
+STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4: "WN_ERR_CUDA",
+          5: "WN_ERR_NOMEM", 6: "WN_ERR_UNSUPPORTED"}
+FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
+EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
+           "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
+           "wn_last_build_launches"]
+COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
+                 "groups_culled_warps", "on_boundary"]
+
+
+class WNError(RuntimeError):
+    def __init__(self, status, msg, face_status=None):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+        self.face_status = face_status
+
+
+class Options(C.Structure):
+    _fields_ = [("eps", C.c_double), ("max_depth", C.c_int), ("precision", C.c_int),
+                ("rule", C.c_int), ("angle_mode", C.c_int), ("strict", C.c_int)]
+
+
+class FacesInfo(C.Structure):
+    _fields_ = [("n_records", C.c_int64), ("n_seg_records", C.c_int64), ("n_groups", C.c_int64),
+                ("n_lines", C.c_int64), ("bytes", C.c_int64), ("precision", C.c_int32),
+                ("max_face_records", C.c_int32)]
+
+
+def lib_path():
+    return _LIBPATH
+
+
+def load():
+    """Load libwn.so (build it first with `python -m paper_2510_25159_b200._build`)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIBPATH):
+            raise ImportError("libwn.so not built (run __graft_entry__.build() or "
+                              "python -m paper_2510_25159_b200._build); there is no CPU fallback")
+        L = C.CDLL(_LIBPATH)
+        vp = C.c_void_p
+        L.wn_build_faces.restype = C.c_int
+        L.wn_build_faces.argtypes = [C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, vp, vp, vp,
+                                     C.POINTER(Options), vp, C.POINTER(vp), vp]
+        L.wn_query.restype = C.c_int
+        L.wn_query.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp]
+        L.wn_faces_info.restype = C.c_int
+        L.wn_faces_info.argtypes = [vp, C.POINTER(FacesInfo)]
+        L.wn_set_counters.restype = C.c_int
+        L.wn_set_counters.argtypes = [vp, C.c_int]
+        L.wn_get_counters.restype = C.c_int
+        L.wn_get_counters.argtypes = [vp, vp, C.POINTER(C.c_int64)]
+        L.wn_set_timing.restype = C.c_int
+        L.wn_set_timing.argtypes = [vp, C.c_int]
+        L.wn_get_timing.restype = C.c_int
+        L.wn_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.wn_last_build_launches.restype = C.c_int32
+        L.wn_last_build_launches.argtypes = []
+        L.wn_free_faces.restype = None
+        L.wn_free_faces.argtypes = [vp]
+        L.wn_last_error.restype = C.c_char_p
+        L.wn_last_error.argtypes = []
+        L.wn_last_query_launches.restype = C.c_int32
+        L.wn_last_query_launches.argtypes = []
+        _lib = L
+    return _lib
+
+
+def last_error():
+    return load().wn_last_error().decode()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(x, dtype, device):
+    """numpy / torch -> contiguous CUDA tensor of dtype (marshalling only)."""
+    torch = _torch()
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(x))
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream, device):
+    torch = _torch()
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass
+class QueryResult:
+    winding: "object"
+    flag: "object"
+
+
+class Faces:
+    """A built face set (owns the device records of libwn)."""
+
+    def __init__(self, handle, device, n_faces, options):
+        self._h = handle
+        self.device = device
+        self.n_faces = n_faces
+        self.options = options
+
+    @classmethod
+    def build(cls, ctrl_uv, ctrl_w, seg_degree, loop_seg_off, face_loop_off, face_periodic,
+              face_domain, eps=0.0, max_depth=0, precision=0, rule=0, angle_mode=0, strict=True,
+              device=None, stream=None):
+        torch = _torch()
+        L = load()
+        if not torch.cuda.is_available():
+            raise WNError(4, "no CUDA device (libwn has no CPU fallback)")
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        ctrl = _dev(ctrl_uv, torch.float64, device).reshape(-1, 2)
+        w = _dev(ctrl_w, torch.float64, device)
+        deg = _dev(seg_degree, torch.int32, device)
+        lso = _dev(loop_seg_off, torch.int32, device)
+        flo = _dev(face_loop_off, torch.int32, device)
+        per = _dev(face_periodic, torch.uint8, device)
+        dom = _dev(face_domain, torch.float64, device).reshape(-1, 4)
+        nf, nl, ns = flo.numel() - 1, lso.numel() - 1, deg.numel()
+        status = torch.zeros(max(nf, 1), dtype=torch.int32, device=device)
+        opts = Options(float(eps), int(max_depth), int(precision), int(rule), int(angle_mode), int(bool(strict)))
+        h = C.c_void_p()
+        with torch.cuda.device(device):
+            rc = L.wn_build_faces(nf, nl, ns, _ptr(ctrl), _ptr(w), _ptr(deg), _ptr(lso), _ptr(flo),
+                                  _ptr(per), _ptr(dom), C.byref(opts), _stream(stream, device), C.byref(h),
+                                  _ptr(status))
+        if rc != WN_OK:
+            raise WNError(rc, last_error(), status[:nf].cpu().numpy())
+        return cls(h, device, nf, opts)
+
+    @classmethod
+    def from_workload(cls, wl, **kw):
+        return cls.build(wl["ctrl_uv"], wl["ctrl_w"], wl["seg_degree"], wl["loop_seg_off"],
+                         wl["face_loop_off"], wl["face_periodic"], wl["face_domain"], **kw)
+
+    def query(self, face_id, uv, out=None, stream=None):
+        """(winding float64 [n], flag uint8 [n]) as CUDA tensors; asynchronous on `stream`."""
+        torch = _torch()
+        fid = _dev(face_id, torch.int32, self.device)
+        q = _dev(uv, torch.float64, self.device).reshape(-1, 2)
+        n = fid.numel()
+        if out is None:
+            wnd = torch.empty(n, dtype=torch.float64, device=self.device)
+            flg = torch.empty(n, dtype=torch.uint8, device=self.device)
+        else:
+            wnd, flg = out
+        with torch.cuda.device(self.device):
+            rc = load().wn_query(self._h, n, _ptr(fid), _ptr(q), _ptr(wnd), _ptr(flg),
+                                 _stream(stream, self.device))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        return QueryResult(wnd, flg)
+
+    def query_raw(self, n, face_id_ptr, uv_ptr, winding_ptr, flag_ptr, stream_handle):
+        """Pointer-level call (already-resident buffers; used by bench.py)."""
+        rc = load().wn_query(self._h, int(n), C.c_void_p(face_id_ptr), C.c_void_p(uv_ptr),
+                             C.c_void_p(winding_ptr), C.c_void_p(flag_ptr), C.c_void_p(stream_handle))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+
+    def info(self):
+        inf = FacesInfo()
+        rc = load().wn_faces_info(self._h, C.byref(inf))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        return {k: getattr(inf, k) for k, _ in FacesInfo._fields_}
+
+    def set_counters(self, enable=True):
+        load().wn_set_counters(self._h, int(bool(enable)))
+
+    def counters(self, stream=None):
+        arr = (C.c_int64 * 8)()
+        rc = load().wn_get_counters(self._h, _stream(stream, self.device), arr)
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        return dict(zip(COUNTER_NAMES, list(arr)))
+
+    def set_timing(self, enable=True):
+        load().wn_set_timing(self._h, int(bool(enable)))
+
+    def timing(self):
+        """(summed K3 milliseconds, K3 launches) since the last call (waits on events)."""
+        ms = C.c_double()
+        n = C.c_int64()
+        rc = load().wn_get_timing(self._h, C.byref(ms), C.byref(n))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        return ms.value, n.value
+
+    def close(self):
+        if self._h:
+            load().wn_free_faces(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def last_query_launches():
+    return int(load().wn_last_query_launches())
+
+
+def last_build_launches():
+    return int(load().wn_last_build_launches())

@@ -1,0 +1,926 @@
+// wn_build.cu -- build side of libwn: segment prep (K1), lifting (K2a), the
+// host planner that enumerates lattice copies / line terms / pairs (K2b, native
+// C++), pairing probes run through the query kernel (Algs. 7-9), and record
+// emission (K2c).  PAPER.md is cited as P:<line>.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "wn_common.cuh"
+
+namespace wn {
+
+static thread_local char g_err[512] = "";
+thread_local int32_t g_build_launches = 0;
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+wn_status_t cuda_fail(cudaError_t e, const char *what) {
+  set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  return (e == cudaErrorMemoryAllocation) ? WN_ERR_NOMEM : WN_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------------------
+// K0: degree check -> control-point counts (prefix-summed into offsets)
+// ---------------------------------------------------------------------------
+__global__ void k_deg(int32_t n_segs, const int32_t *__restrict__ deg, int32_t *__restrict__ cnt,
+                      int32_t *__restrict__ bad) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s > n_segs) return;
+  if (s == n_segs) { cnt[s] = 0; return; }
+  const int n = deg[s];
+  const bool ok = n >= 1 && n <= 5;
+  cnt[s] = ok ? n + 1 : 0;
+  if (!ok) atomicOr(bad, 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1: segment prep.  Derivative bound B of Lemma 1: polynomial
+// hodograph bound max_i n|P_i - P_{i-1}|; rational: the minimum
+// of Floater's two bounds n(W/w)max|P_i-P_j| and n(W/w)^2 max|P_i-P_{i-1}|
+// (reading R8).  Root span S0 = min(B, control-polygon length)
+// (reading R9: arc length <= polygon length for positive weights, and the
+// Lemma 1 proof P:1086-1092 only needs arc length <= span).
+// ---------------------------------------------------------------------------
+__global__ void k_prep(int32_t n_segs, const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
+                       const double *__restrict__ ctrl, const double *__restrict__ w,
+                       double2 *__restrict__ prep, uint8_t *__restrict__ serr) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_segs) return;
+  const int n = deg[s];
+  const int o = coff[s];
+  double P[6][2], W[6];
+  bool err = false;
+  double wmax = 0.0, wmin = INFINITY;
+  for (int j = 0; j <= n; ++j) {
+    P[j][0] = ctrl[2 * (o + j)];
+    P[j][1] = ctrl[2 * (o + j) + 1];
+    W[j] = w ? w[o + j] : 1.0;
+    err |= !isfinite(P[j][0]) || !isfinite(P[j][1]) || !isfinite(W[j]) || !(W[j] > 0.0);
+    wmax = fmax(wmax, W[j]);
+    wmin = fmin(wmin, W[j]);
+  }
+  double dmax = 0.0, lpoly = 0.0, diam = 0.0;
+  for (int j = 1; j <= n; ++j) {
+    const double l = hypot(P[j][0] - P[j - 1][0], P[j][1] - P[j - 1][1]);
+    dmax = fmax(dmax, l);
+    lpoly += l;
+  }
+  double B;
+  if (wmax == wmin) {
+    B = n * dmax;
+  } else {
+    for (int i = 0; i <= n; ++i)
+      for (int j = i + 1; j <= n; ++j) diam = fmax(diam, hypot(P[j][0] - P[i][0], P[j][1] - P[i][1]));
+    const double r = wmax / wmin;
+    B = fmin(n * r * diam, n * r * r * dmax);
+  }
+  prep[s] = make_double2(B, fmin(B, lpoly));
+  serr[s] = err ? 1 : 0;
+}
+
+__global__ void k_loop_face(int32_t n_faces, const int32_t *__restrict__ face_off, int32_t *__restrict__ loop_face) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_faces) return;
+  for (int l = face_off[f]; l < face_off[f + 1]; ++l) loop_face[l] = f;
+}
+
+__device__ __forceinline__ double lat(double x, int k, double T) { return __dadd_rn(x, __dmul_rn((double)k, T)); }
+
+// ---------------------------------------------------------------------------
+// K2a: lifting to the universal covering space (Sec. 4.3).  Loops
+// are stored seam-discontinuously (R18); segment i is translated by the lattice
+// vector nearest to continuing from the lifted end of segment i-1 (R17/R18).
+// Homology class = round(closure / T).  Junctions that are not
+// bit-continuous after lifting are recorded as chain breaks.
+// ---------------------------------------------------------------------------
+__global__ void k_lift(int32_t n_loops, const int32_t *__restrict__ loop_off, const int32_t *__restrict__ loop_face,
+                       const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
+                       const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
+                       const double *__restrict__ ctrl, const uint8_t *__restrict__ serr,
+                       int2 *__restrict__ shift, uint8_t *__restrict__ brk, LoopInfo *__restrict__ info) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= n_loops) return;
+  const int f = loop_face[l];
+  const int pu = face_per[f] & 1, pv = (face_per[f] >> 1) & 1;
+  const double Tu = face_dom[4 * f + 1], Tv = face_dom[4 * f + 3];
+  int ku = 0, kv = 0, nbrk = 0, err = 0;
+  double ex = 0, ey = 0, sx = 0, sy = 0;
+  double xmin = INFINITY, ymin = INFINITY, xmax = -INFINITY, ymax = -INFINITY;
+  const int s0 = loop_off[l], s1 = loop_off[l + 1];
+  for (int s = s0; s < s1; ++s) {
+    const int n = deg[s];
+    const int o = coff[s];
+    err |= serr[s];
+    const double x0 = ctrl[2 * o], y0 = ctrl[2 * o + 1];
+    if (s > s0) {
+      if (pu) ku = (int)round(__ddiv_rn(__dsub_rn(ex, x0), Tu));
+      if (pv) kv = (int)round(__ddiv_rn(__dsub_rn(ey, y0), Tv));
+    }
+    shift[s] = make_int2(ku, kv);
+    const double lx0 = pu ? lat(x0, ku, Tu) : x0, ly0 = pv ? lat(y0, kv, Tv) : y0;
+    if (s > s0) {
+      const bool b = !(lx0 == ex && ly0 == ey);
+      brk[s] = b;
+      nbrk += b;
+    } else {
+      brk[s] = 0;
+      sx = lx0;
+      sy = ly0;
+    }
+    for (int j = 0; j <= n; ++j) {
+      const double x = pu ? lat(ctrl[2 * (o + j)], ku, Tu) : ctrl[2 * (o + j)];
+      const double y = pv ? lat(ctrl[2 * (o + j) + 1], kv, Tv) : ctrl[2 * (o + j) + 1];
+      xmin = fmin(xmin, x); xmax = fmax(xmax, x);
+      ymin = fmin(ymin, y); ymax = fmax(ymax, y);
+      if (j == n) { ex = x; ey = y; }
+    }
+  }
+  LoopInfo I;
+  I.cu = (pu && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ex, sx), Tu)) : 0;
+  I.cv = (pv && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ey, sy), Tv)) : 0;
+  I.nbrk = nbrk;
+  I.closed = (s1 > s0) && ex == sx && ey == sy;
+  I.err = err;
+  I.nseg = s1 - s0;
+  I.sx = sx;
+  I.sy = sy;
+  I.bb[0] = xmin; I.bb[1] = ymin; I.bb[2] = xmax; I.bb[3] = ymax;
+  info[l] = I;
+}
+
+// ---------------------------------------------------------------------------
+// K2c: record emission, one thread per planned group.
+// ---------------------------------------------------------------------------
+template <typename R>
+struct Emit;
+
+__device__ __forceinline__ float f_dn(double x) { return __double2float_rd(x); }
+__device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
+
+template <typename R>
+__device__ void put_hot(Hot<R> *H, int r, R a, R b, R c, uint32_t meta);
+template <>
+__device__ void put_hot<double>(Hot<double> *H, int r, double a, double b, double c, uint32_t meta) {
+  Hot<double> h;
+  h.a = a; h.b = b; h.c = c; h.meta = meta; h.pad = 0;
+  H[r] = h;
+}
+template <>
+__device__ void put_hot<float>(Hot<float> *H, int r, float a, float b, float c, uint32_t meta) {
+  Hot<float> h;
+  h.a = a; h.b = b; h.c = c; h.meta = meta;
+  H[r] = h;
+}
+
+template <typename R>
+__device__ void put_group(Hot<R> *H, int r, double xmin, double ymin, double xmax, double ymax, uint32_t meta);
+template <>
+__device__ void put_group<double>(Hot<double> *H, int r, double xmin, double ymin, double xmax, double ymax,
+                                  uint32_t meta) {
+  Hot<double> h;
+  float2 lo = make_float2(f_dn(xmin), f_dn(ymin)), hi = make_float2(f_up(xmax), f_up(ymax));
+  memcpy(&h.a, &lo, 8);
+  memcpy(&h.b, &hi, 8);
+  h.c = 0.0; h.meta = meta; h.pad = 0;
+  H[r] = h;
+}
+template <>
+__device__ void put_group<float>(Hot<float> *H, int r, double xmin, double ymin, double xmax, double ymax,
+                                 uint32_t meta) {
+  Hot<float> h;
+  h.a = f_dn(xmin);
+  h.b = f_dn(ymin);
+  __half2 hi = __halves2half2(__float2half_ru(f_up(xmax)), __float2half_ru(f_up(ymax)));
+  memcpy(&h.c, &hi, 4);
+  h.meta = meta;
+  H[r] = h;
+}
+
+__device__ __forceinline__ double binom5(int n, int j) {
+  const double tab[6][6] = {{1, 0, 0, 0, 0, 0}, {1, 1, 0, 0, 0, 0}, {1, 2, 1, 0, 0, 0},
+                            {1, 3, 3, 1, 0, 0}, {1, 4, 6, 4, 1, 0}, {1, 5, 10, 10, 5, 1}};
+  return tab[n][j];
+}
+
+template <typename R>
+__global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, const int32_t *__restrict__ loop_off,
+                       const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
+                       const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
+                       const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
+                       const double *__restrict__ wts, const double2 *__restrict__ prep,
+                       const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
+                       const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
+                       Cold<R> *__restrict__ cold) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_groups) return;
+  const PlanGroup G = groups[g];
+  const int l = G.loop;
+  const int f = loop_face[l];
+  const int pu = face_per[f] & 1, pv = (face_per[f] >> 1) & 1;
+  const double Tu = face_dom[4 * f + 1], Tv = face_dom[4 * f + 3];
+  const LoopInfo I = info[l];
+  const uint32_t fa = (G.flags & PF_ANGLE) ? F_ANGLE : 0u;
+  // lifted + translated coordinate (two exact-op steps: lift, then translate)
+  auto X = [&](double x, int ks) { return pu ? lat(lat(x, ks, Tu), G.ku, Tu) : x; };
+  auto Y = [&](double y, int ks) { return pv ? lat(lat(y, ks, Tv), G.kv, Tv) : y; };
+  auto TX = [&](double x) { return pu ? lat(x, G.ku, Tu) : x; };
+  auto TY = [&](double y) { return pv ? lat(y, G.kv, Tv) : y; };
+  int r = G.rec_off;
+  if (G.kind == G_LINE) {
+    // omega(p, L) for the line through beta_0 along the extension vector (Eq. 5)
+    const double bx = TX(I.sx), by = TY(I.sy);
+    uint32_t meta = K_LINE;
+    double c;
+    if (I.cu != 0) { c = by; if (I.cu > 0) meta |= F_GE; }          // v = (+-T,0): left iff p.v >=/<= c
+    else { c = bx; meta |= F_AXISV; if (I.cv < 0) meta |= F_GE; }   // v = (0,+-T): left iff p.u <=/>= c
+    put_hot<R>(hot, r, (R)c, (R)0, (R)0, meta);
+    return;
+  }
+  if (G.flags & PF_CULL) {
+    const double xmin = TX(I.bb[0]) - G.M, xmax = TX(I.bb[2]) + G.M;
+    const double ymin = TY(I.bb[1]) - G.M, ymax = TY(I.bb[3]) + G.M;
+    put_group<R>(hot, r++, xmin, ymin, xmax, ymax, K_GROUP | ((uint32_t)(G.nrec - 1) << 8));
+  }
+  const int s0 = loop_off[l], s1 = loop_off[l + 1];
+  int cl = G.cold_local;
+  int cg = G.cold_off;
+  for (int s = s0; s < s1; ++s) {
+    const int n = deg[s];
+    const int o = coff[s];
+    const int2 k = shift[s];
+    double px[6], py[6];
+    for (int j = 0; j <= n; ++j) {
+      px[j] = X(ctrl[2 * (o + j)], k.x);
+      py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
+    }
+    if (s == s0) put_hot<R>(hot, r++, (R)px[0], (R)py[0], (R)0, K_MOVE | fa);
+    else if (brk[s]) put_hot<R>(hot, r++, (R)px[0], (R)py[0], (R)0, K_MOVEG | fa);
+    const double2 bp = prep[s];
+    // Eq. 1 root span with the R5 margin (relative + absolute); Eq. 2 uses B
+    double S0 = bp.y * (1.0 + rel) + G.M;
+    double Bm = bp.x * (1.0 + rel);
+    R S0r, Br;
+    if (sizeof(R) == 4) { S0r = (R)f_up(S0); Br = (R)f_up(Bm); } else { S0r = (R)S0; Br = (R)Bm; }
+    put_hot<R>(hot, r++, (R)px[n], (R)py[n], S0r, K_SEG | fa | ((uint32_t)cl << 8));
+    Cold<R> C;
+    C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
+    C.B = Br;
+    C.M = (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M;
+    C.n = n;
+    C.pad = 0;
+    for (int j = 0; j < 6; ++j) {
+      if (j <= n) {
+        const double wj = wts ? wts[o + j] : 1.0;
+        const double cw = binom5(n, j) * wj;
+        C.cx[j] = (R)(cw * px[j]);
+        C.cy[j] = (R)(cw * py[j]);
+        C.cw[j] = (R)cw;
+      } else {
+        C.cx[j] = C.cy[j] = C.cw[j] = (R)0;
+      }
+    }
+    cold[cg] = C;
+    ++cl;
+    ++cg;
+  }
+  if (G.flags & PF_TAIL_CLOSEG) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_CLOSEG | fa);
+  if (G.flags & PF_TAIL_XCH) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_XCH | fa);
+  if (G.flags & PF_TAIL_NCH) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_NCH | fa);
+}
+
+// ---------------------------------------------------------------------------
+// host planner
+// ---------------------------------------------------------------------------
+struct Plan {
+  std::vector<PlanGroup> groups;
+  std::vector<int32_t> rec_off;   // per target face + 1
+  std::vector<int32_t> cold_off;
+  int64_t n_lines = 0, n_cull = 0;
+  int32_t recs = 0, colds = 0;
+  int32_t face_rec0 = 0, face_cold0 = 0;
+  int cur_face = -1;
+
+  void begin_face(int f) {
+    cur_face = f;
+    face_rec0 = recs;
+    face_cold0 = colds;
+    rec_off.push_back(recs);
+    cold_off.push_back(colds);
+  }
+  void end() {
+    rec_off.push_back(recs);
+    cold_off.push_back(colds);
+  }
+  void add(int kind, int flags, int loop, int ku, int kv, const LoopInfo &I, double M) {
+    PlanGroup G;
+    G.kind = kind;
+    G.flags = flags;
+    G.loop = loop;
+    G.ku = ku;
+    G.kv = kv;
+    G.rec_off = recs;
+    G.cold_off = colds;
+    G.cold_local = colds - face_cold0;
+    G.face = cur_face;
+    G.M = M;
+    int nrec;
+    if (kind == G_LINE) {
+      nrec = 1;
+      ++n_lines;
+    } else {
+      nrec = ((flags & PF_CULL) ? 1 : 0) + 1 + I.nseg + I.nbrk +
+             ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
+      colds += I.nseg;
+      if (flags & PF_CULL) ++n_cull;
+    }
+    G.nrec = nrec;
+    recs += nrec;
+    groups.push_back(G);
+  }
+};
+
+static int gcd_i(int a, int b) {
+  a = std::abs(a); b = std::abs(b);
+  while (b) { int t = a % b; a = b; b = t; }
+  return a;
+}
+
+// lattice translates k with [lo + k T, hi + k T] meeting [t0 - m, t0 + T + m]
+static void k_range(double lo, double hi, double t0, double T, double m, int &k0, int &k1) {
+  k0 = (int)std::ceil((t0 - m - hi) / T) - 1;
+  k1 = (int)std::floor((t0 + T + m - lo) / T) + 1;
+  // tighten exactly (the +-1 guards the division rounding)
+  while (k0 <= k1 && !(lo + k0 * T <= t0 + T + m && hi + k0 * T >= t0 - m)) ++k0;
+  while (k1 >= k0 && !(lo + k1 * T <= t0 + T + m && hi + k1 * T >= t0 - m)) --k1;
+}
+
+struct FaceCtx {
+  uint8_t per;
+  double u0, Tu, v0, Tv;
+  double M;
+  bool angle;
+};
+
+// group flags for a closed / copy group
+static int loop_flags(const LoopInfo &I, bool angle, bool copy) {
+  int fl = angle ? PF_ANGLE : 0;
+  if (copy) {
+    fl |= angle ? PF_TAIL_NCH : PF_TAIL_XCH;
+    if (I.nbrk == 0) fl |= PF_CULL;
+  } else {
+    const bool closed = I.closed && I.nbrk == 0;
+    if (closed) fl |= PF_CULL;
+    else if (!angle) fl |= PF_TAIL_CLOSEG;
+  }
+  return fl;
+}
+
+// contractible loop in a (uni/bi/non-)periodic face: every translate meeting the tile
+static void plan_contractible(Plan &P, int l, const LoopInfo &I, const FaceCtx &C) {
+  const int fl = loop_flags(I, C.angle, false);
+  int i0 = 0, i1 = 0, j0 = 0, j1 = 0;
+  const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
+  if (C.per & 1) k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, i0, i1);
+  if (C.per & 2) k_range(I.bb[1], I.bb[3], C.v0, C.Tv, m, j0, j1);
+  for (int i = i0; i <= i1; ++i)
+    for (int j = j0; j <= j1; ++j) P.add(G_LOOP, fl, l, i, j, I, C.M);
+}
+
+// non-contractible loop along axis a (0 = u, 1 = v) at transverse translate jt:
+// copies (Eq. 5 rewritten with chords tiling L) meeting the tile
+static void plan_extended_copies(Plan &P, int l, const LoopInfo &I, const FaceCtx &C, int axis, int jt,
+                                 bool transverse_cull_tile) {
+  const int fl = loop_flags(I, C.angle, true);
+  const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
+  int k0, k1;
+  if (axis == 0) k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, k0, k1);
+  else k_range(I.bb[1], I.bb[3], C.v0, C.Tv, m, k0, k1);
+  if (transverse_cull_tile) {
+    // bi-periodic: the transverse translate must also meet the tile
+    const double lo = axis == 0 ? I.bb[1] + jt * C.Tv : I.bb[0] + jt * C.Tu;
+    const double hi = axis == 0 ? I.bb[3] + jt * C.Tv : I.bb[2] + jt * C.Tu;
+    const double t0 = axis == 0 ? C.v0 : C.u0, T = axis == 0 ? C.Tv : C.Tu;
+    if (!(lo <= t0 + T + m && hi >= t0 - m)) return;
+  }
+  for (int k = k0; k <= k1; ++k) {
+    if (axis == 0) P.add(G_COPY, fl, l, k, jt, I, C.M);
+    else P.add(G_COPY, fl, l, jt, k, I, C.M);
+  }
+}
+
+static double face_margin(const std::vector<LoopInfo> &L, int l0, int l1, const FaceCtx &C, bool fp32) {
+  double s = 1.0 + std::fabs(C.u0) + std::fabs(C.v0) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0);
+  for (int l = l0; l < l1; ++l)
+    for (int k = 0; k < 4; ++k) s = std::max(s, 1.0 + std::fabs(L[l].bb[k]) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0));
+  return fp32 ? std::ldexp(s, -17) : std::ldexp(s, -40);
+}
+
+}  // namespace wn
+
+using namespace wn;
+
+// ---------------------------------------------------------------------------
+// device buffers helper
+// ---------------------------------------------------------------------------
+namespace {
+struct DevBuf {
+  std::vector<void *> ptrs;
+  cudaStream_t st = 0;
+  ~DevBuf() {
+    for (void *p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  cudaError_t alloc(T **p, size_t count) {
+    cudaError_t e = cudaMallocAsync((void **)p, sizeof(T) * (count ? count : 1), st);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+void free_handle(wn_faces_t F) {
+  if (!F) return;
+  for (auto &pr : F->k3_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  cudaFree(F->hot);
+  cudaFree(F->cold);
+  cudaFree(F->face_rec_off);
+  cudaFree(F->face_cold_off);
+  cudaFree(F->face_order);
+  cudaFree(F->face_dom);
+  cudaFree(F->face_per);
+  cudaFree(F->face_ok);
+  cudaFree(F->counters);
+  delete F;
+}
+
+struct BuildCtx {
+  int32_t n_faces, n_loops, n_segs;
+  const double *ctrl, *w;
+  const int32_t *deg, *lso, *flo;
+  const uint8_t *per;
+  const double *dom;
+  int32_t *coff, *loop_face;
+  double2 *prep;
+  int2 *shift;
+  uint8_t *brk;
+  LoopInfo *info;
+  cudaStream_t st;
+};
+
+// emit the records of `plan` into a new handle whose faces carry `fper`/`fdom`
+template <typename R>
+wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<uint8_t> &fper,
+                        const std::vector<double> &fdom, wn_faces_t F) {
+  cudaStream_t st = B.st;
+  const int nf = (int)fper.size();
+  F->n_faces = nf;
+  F->n_records = plan.recs;
+  F->n_seg = plan.colds;
+  F->n_lines = plan.n_lines;
+  F->n_groups = plan.n_cull;
+  WN_CUDA(cudaMalloc(&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1)));
+  WN_CUDA(cudaMalloc(&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1)));
+  WN_CUDA(cudaMalloc(&F->face_rec_off, sizeof(int32_t) * (nf + 1)));
+  WN_CUDA(cudaMalloc(&F->face_cold_off, sizeof(int32_t) * (nf + 1)));
+  WN_CUDA(cudaMalloc(&F->face_order, sizeof(int32_t) * std::max(nf, 1)));
+  WN_CUDA(cudaMalloc(&F->face_dom, sizeof(double) * 4 * std::max(nf, 1)));
+  WN_CUDA(cudaMalloc(&F->face_per, std::max(nf, 1)));
+  WN_CUDA(cudaMalloc(&F->face_ok, std::max(nf, 1)));
+  WN_CUDA(cudaMalloc(&F->counters, 8 * sizeof(unsigned long long)));
+  F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
+  std::vector<int32_t> order(nf);
+  std::iota(order.begin(), order.end(), 0);
+  int32_t maxr = 0;
+  for (int f = 0; f < nf; ++f) maxr = std::max(maxr, plan.rec_off[f + 1] - plan.rec_off[f]);
+  F->max_face_records = maxr;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return (plan.rec_off[a + 1] - plan.rec_off[a]) > (plan.rec_off[b + 1] - plan.rec_off[b]);
+  });
+  std::vector<uint8_t> ok(nf, 1);
+  WN_CUDA(cudaMemcpyAsync(F->face_rec_off, plan.rec_off.data(), sizeof(int32_t) * (nf + 1), cudaMemcpyHostToDevice, st));
+  WN_CUDA(cudaMemcpyAsync(F->face_cold_off, plan.cold_off.data(), sizeof(int32_t) * (nf + 1), cudaMemcpyHostToDevice, st));
+  if (nf) {
+    WN_CUDA(cudaMemcpyAsync(F->face_order, order.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(F->face_dom, fdom.data(), sizeof(double) * 4 * nf, cudaMemcpyHostToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(F->face_per, fper.data(), nf, cudaMemcpyHostToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(F->face_ok, ok.data(), nf, cudaMemcpyHostToDevice, st));
+  }
+  const int ng = (int)plan.groups.size();
+  if (ng) {
+    PlanGroup *dg = nullptr;
+    WN_CUDA(cudaMallocAsync((void **)&dg, sizeof(PlanGroup) * ng, st));
+    WN_CUDA(cudaMemcpyAsync(dg, plan.groups.data(), sizeof(PlanGroup) * ng, cudaMemcpyHostToDevice, st));
+    const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
+    ++g_build_launches;
+    k_emit<R><<<(ng + 127) / 128, 128, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
+                                                 B.w, B.prep, B.shift, B.brk, B.info, rel, (Hot<R> *)F->hot,
+                                                 (Cold<R> *)F->cold);
+    WN_CUDA(cudaGetLastError());
+    WN_CUDA(cudaFreeAsync(dg, st));
+  }
+  return WN_OK;
+}
+
+}  // namespace
+
+extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, const double *ctrl_uv,
+                                      const double *ctrl_w, const int32_t *seg_degree,
+                                      const int32_t *loop_seg_off, const int32_t *face_loop_off,
+                                      const uint8_t *face_periodic, const double *face_domain,
+                                      const wn_options_t *opts, void *stream, wn_faces_t *out,
+                                      int32_t *face_status) {
+  set_error("");
+  g_build_launches = 0;
+  if (!out) { set_error("wn_build_faces: out == NULL"); return WN_ERR_ARG; }
+  if (n_faces < 0 || n_loops < 0 || n_segs < 0) { set_error("wn_build_faces: negative count"); return WN_ERR_ARG; }
+  if (!loop_seg_off || !face_loop_off || (n_faces > 0 && (!face_periodic || !face_domain)) ||
+      (n_segs > 0 && (!ctrl_uv || !seg_degree))) {
+    set_error("wn_build_faces: NULL array");
+    return WN_ERR_ARG;
+  }
+  wn_options_t O;
+  O.eps = 0; O.max_depth = 0; O.precision = 0; O.rule = 0; O.angle_mode = 0; O.strict = 1;
+  if (opts) O = *opts;
+  if (O.precision != 0 && O.precision != 1) { set_error("bad precision"); return WN_ERR_ARG; }
+  if (O.rule != 0 && O.rule != 1) { set_error("bad rule"); return WN_ERR_ARG; }
+  if (O.angle_mode != 0 && O.angle_mode != 1) { set_error("bad angle_mode"); return WN_ERR_ARG; }
+  if (O.max_depth < 0 || O.max_depth > 64) { set_error("max_depth must be in [0,64]"); return WN_ERR_ARG; }
+  const bool fp32 = O.precision == 1;
+  const double eps = O.eps > 0 ? O.eps : (fp32 ? 1e-6 : 1e-10);
+  const int maxd = O.max_depth > 0 ? O.max_depth : 48;
+  const bool angle = O.angle_mode == 1;
+  int dev = 0;
+  {
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf D;
+  D.st = st;
+
+  // --- host copies of the small CSR / face arrays ---
+  std::vector<int32_t> h_lso(n_loops + 1), h_flo(n_faces + 1);
+  std::vector<uint8_t> h_per(n_faces);
+  std::vector<double> h_dom(4 * (size_t)n_faces);
+  WN_CUDA(cudaMemcpyAsync(h_lso.data(), loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaMemcpyAsync(h_flo.data(), face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st));
+  if (n_faces) {
+    WN_CUDA(cudaMemcpyAsync(h_per.data(), face_periodic, n_faces, cudaMemcpyDeviceToHost, st));
+    WN_CUDA(cudaMemcpyAsync(h_dom.data(), face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st));
+  }
+  // --- K0: degrees -> control offsets ---
+  int32_t *d_cnt = nullptr, *d_bad = nullptr;
+  BuildCtx B{};
+  B.n_faces = n_faces; B.n_loops = n_loops; B.n_segs = n_segs;
+  B.ctrl = ctrl_uv; B.w = ctrl_w; B.deg = seg_degree; B.lso = loop_seg_off; B.flo = face_loop_off;
+  B.per = face_periodic; B.dom = face_domain; B.st = st;
+  WN_CUDA(D.alloc(&d_cnt, n_segs + 1));
+  WN_CUDA(D.alloc(&d_bad, 1));
+  WN_CUDA(D.alloc(&B.coff, n_segs + 1));
+  WN_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
+  k_deg<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, seg_degree, d_cnt, d_bad);
+  g_build_launches += 3;   // k_deg + cub scan (init + scan)
+  {
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, d_cnt, B.coff, n_segs + 1, st);
+    void *dt = nullptr;
+    WN_CUDA(D.alloc((char **)&dt, tmp));
+    cub::DeviceScan::ExclusiveSum(dt, tmp, d_cnt, B.coff, n_segs + 1, st);
+  }
+  int32_t h_bad = 0;
+  WN_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaStreamSynchronize(st));
+  // CSR / domain checks on the host
+  bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
+  for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
+  for (int f = 0; csr_ok && f < n_faces; ++f) csr_ok = h_flo[f] <= h_flo[f + 1];
+  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return WN_ERR_ARG; }
+  if (h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return WN_ERR_ARG; }
+  for (int f = 0; f < n_faces; ++f) {
+    const double *d = &h_dom[4 * f];
+    if ((h_per[f] & 1) && !(std::isfinite(d[0]) && std::isfinite(d[1]) && d[1] > 0)) {
+      set_error("face %d: bad u period", f);
+      return WN_ERR_GEOM;
+    }
+    if ((h_per[f] & 2) && !(std::isfinite(d[2]) && std::isfinite(d[3]) && d[3] > 0)) {
+      set_error("face %d: bad v period", f);
+      return WN_ERR_GEOM;
+    }
+  }
+  // --- K1 prep, loop->face, K2a lift ---
+  uint8_t *d_serr = nullptr;
+  WN_CUDA(D.alloc(&B.prep, n_segs));
+  WN_CUDA(D.alloc(&d_serr, n_segs));
+  WN_CUDA(D.alloc(&B.loop_face, n_loops));
+  WN_CUDA(D.alloc(&B.shift, n_segs));
+  WN_CUDA(D.alloc(&B.brk, n_segs));
+  WN_CUDA(D.alloc(&B.info, n_loops));
+  g_build_launches += (n_segs ? 1 : 0) + (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
+  if (n_segs) k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr);
+  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, face_loop_off, B.loop_face);
+  if (n_loops)
+    k_lift<<<(n_loops + 127) / 128, 128, 0, st>>>(n_loops, loop_seg_off, B.loop_face, face_periodic, face_domain,
+                                                 seg_degree, B.coff, ctrl_uv, d_serr, B.shift, B.brk, B.info);
+  WN_CUDA(cudaGetLastError());
+  std::vector<LoopInfo> L(n_loops);
+  if (n_loops) WN_CUDA(cudaMemcpyAsync(L.data(), B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaStreamSynchronize(st));
+
+  // --- K2b: validation + planning (host) ---
+  std::vector<int32_t> status(n_faces, WN_FACE_OK);
+  std::vector<FaceCtx> ctx(n_faces);
+  // pairing requests for bi-periodic faces
+  struct Cand { int face, alpha, beta, s; double px, py; };
+  std::vector<int> need_pair;
+  for (int f = 0; f < n_faces; ++f) {
+    FaceCtx &C = ctx[f];
+    C.per = h_per[f] & 3;
+    C.u0 = h_dom[4 * f]; C.Tu = h_dom[4 * f + 1]; C.v0 = h_dom[4 * f + 2]; C.Tv = h_dom[4 * f + 3];
+    if (!(C.per & 1)) { C.u0 = 0; C.Tu = 0; }
+    if (!(C.per & 2)) { C.v0 = 0; C.Tv = 0; }
+    C.angle = angle;
+    C.M = face_margin(L, h_flo[f], h_flo[f + 1], C, fp32);
+    int cp = 0, cq = 0, nA = 0, nB = 0;
+    for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
+      const LoopInfo &I = L[l];
+      if (I.err) status[f] = WN_FACE_GEOM;
+      if (I.nseg == 0 || (I.cu == 0 && I.cv == 0)) continue;
+      if (C.per == 1 && std::abs(I.cu) > 1) status[f] = WN_FACE_B1;
+      if (C.per == 2 && std::abs(I.cv) > 1) status[f] = WN_FACE_B1;
+      if (gcd_i(I.cu, I.cv) != 1 && !status[f]) status[f] = WN_FACE_CLASS;
+      if (cp == 0 && cq == 0) { cp = I.cu; cq = I.cv; }
+      if (I.cu == cp && I.cv == cq) ++nA;
+      else if (I.cu == -cp && I.cv == -cq) ++nB;
+      else if (!status[f]) status[f] = WN_FACE_CLASS;
+    }
+    if (status[f]) continue;
+    if (nA != nB && (O.strict || C.per == 3)) { status[f] = WN_FACE_UNBALANCED; continue; }
+    if (C.per == 3 && nA > 0) {
+      if (cp != 0 && cq != 0) { status[f] = WN_FACE_GENERAL_PQ; continue; }
+      need_pair.push_back(f);
+    }
+  }
+  bool any_bad = false;
+  for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
+
+  // --- pairing (Algs. 7-9) for bi-periodic faces via probe queries ---
+  // pair_beta[alpha] = beta, pair_s[alpha] = transverse translate of beta
+  std::vector<int> pair_beta(n_loops, -1), pair_s(n_loops, 0);
+  if (!any_bad && !need_pair.empty()) {
+    // virtual faces: one uni-periodic extended curve per non-contractible loop
+    std::vector<int> vface(n_loops, -1);
+    Plan VP;
+    std::vector<uint8_t> vper;
+    std::vector<double> vdom;
+    for (int f : need_pair) {
+      for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
+        const LoopInfo &I = L[l];
+        if (I.nseg == 0 || (I.cu == 0 && I.cv == 0)) continue;
+        FaceCtx C = ctx[f];
+        const int axis = (I.cu != 0) ? 0 : 1;
+        C.per = axis == 0 ? 1 : 2;
+        C.angle = false;
+        vface[l] = (int)vper.size();
+        vper.push_back(C.per);
+        vdom.insert(vdom.end(), {ctx[f].u0, ctx[f].Tu, ctx[f].v0, ctx[f].Tv});
+        VP.begin_face(vface[l]);
+        VP.add(G_LINE, 0, l, 0, 0, I, C.M);
+        plan_extended_copies(VP, l, I, C, axis, 0, false);
+      }
+    }
+    VP.end();
+    // candidates: beta translates along the transverse axis (R16 window)
+    std::vector<Cand> cands;
+    std::vector<int> cand_alpha_q;   // query index of ToLeft(cand, alpha)
+    struct QueryRec { int vf; double x, y; };
+    std::vector<QueryRec> qs;
+    for (int f : need_pair) {
+      const FaceCtx &C = ctx[f];
+      int cp = 0, cq = 0;
+      for (int l = h_flo[f]; l < h_flo[f + 1]; ++l)
+        if (L[l].nseg && (L[l].cu || L[l].cv)) { cp = L[l].cu; cq = L[l].cv; break; }
+      const int tax = (cp != 0) ? 1 : 0;                // transverse axis
+      const double Tt = tax ? C.Tv : C.Tu;
+      for (int la = h_flo[f]; la < h_flo[f + 1]; ++la) {
+        if (!(L[la].nseg && L[la].cu == cp && L[la].cv == cq)) continue;
+        for (int lb = h_flo[f]; lb < h_flo[f + 1]; ++lb) {
+          if (!(L[lb].nseg && L[lb].cu == -cp && L[lb].cv == -cq)) continue;
+          const double ext = tax ? (L[lb].bb[3] - L[lb].bb[1]) / Tt : (L[lb].bb[2] - L[lb].bb[0]) / Tt;
+          const double da = tax ? (L[la].bb[1] - L[lb].bb[1]) / Tt : (L[la].bb[0] - L[lb].bb[0]) / Tt;
+          const int J = 3 + (int)std::ceil(ext + std::fabs(da));
+          for (int s = -J; s <= J; ++s) {
+            Cand c{f, la, lb, s, L[lb].sx + (tax ? 0.0 : s * Tt), L[lb].sy + (tax ? s * Tt : 0.0)};
+            cands.push_back(c);
+            qs.push_back({vface[la], c.px, c.py});
+          }
+        }
+      }
+    }
+    // run probes through the query kernel on a temporary handle (fp64, crossing mode)
+    auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
+      wn_faces_t T = new wn_faces_s();
+      T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0;
+      wn_status_t rc = materialise<double>(B, VP, vper, vdom, T);
+      if (rc != WN_OK) { free_handle(T); return rc; }
+      const int nq = (int)Q.size();
+      std::vector<int32_t> hf(nq);
+      std::vector<double> huv(2 * (size_t)nq);
+      for (int i = 0; i < nq; ++i) { hf[i] = Q[i].vf; huv[2 * i] = Q[i].x; huv[2 * i + 1] = Q[i].y; }
+      int32_t *df = nullptr; double *duv = nullptr, *dw = nullptr; uint8_t *dfl = nullptr;
+      DevBuf Q2; Q2.st = st;
+      WN_CUDA(Q2.alloc(&df, nq)); WN_CUDA(Q2.alloc(&duv, 2 * (size_t)nq));
+      WN_CUDA(Q2.alloc(&dw, nq)); WN_CUDA(Q2.alloc(&dfl, nq));
+      WN_CUDA(cudaMemcpyAsync(df, hf.data(), sizeof(int32_t) * nq, cudaMemcpyHostToDevice, st));
+      WN_CUDA(cudaMemcpyAsync(duv, huv.data(), sizeof(double) * 2 * nq, cudaMemcpyHostToDevice, st));
+      rc = wn_query(T, nq, df, duv, dw, dfl, st);
+      g_build_launches += wn_last_query_launches();
+      res.resize(nq);
+      if (rc == WN_OK) {
+        WN_CUDA(cudaMemcpyAsync(res.data(), dw, sizeof(double) * nq, cudaMemcpyDeviceToHost, st));
+        WN_CUDA(cudaStreamSynchronize(st));
+      }
+      free_handle(T);
+      return rc;
+    };
+    std::vector<double> r1;
+    wn_status_t rc = run_probes(qs, r1);
+    if (rc != WN_OK) return rc;
+    // candidates left of alpha (ToLeft, Alg. 7: omega > 0)
+    std::vector<int> left;
+    for (size_t i = 0; i < cands.size(); ++i)
+      if (r1[i] > 0.0) left.push_back((int)i);
+    // pairwise ToLeft(c1, c2) among left candidates of the same alpha
+    std::vector<QueryRec> q2;
+    std::vector<std::pair<int, int>> q2pairs;
+    for (int i : left)
+      for (int j : left) {
+        if (i == j || cands[i].alpha != cands[j].alpha) continue;
+        const Cand &a = cands[i], &b = cands[j];
+        const FaceCtx &C = ctx[a.face];
+        const int tax = (L[a.alpha].cu != 0) ? 1 : 0;
+        const double Tt = tax ? C.Tv : C.Tu;
+        // omega(pt(c1) - s2*T_t e_t, beta2_ext) (translation identity, App. C.1)
+        q2.push_back({vface[b.beta], a.px - (tax ? 0.0 : b.s * Tt), a.py - (tax ? b.s * Tt : 0.0)});
+        q2pairs.push_back({i, j});
+      }
+    std::vector<double> r2;
+    if (!q2.empty()) {
+      rc = run_probes(q2, r2);
+      if (rc != WN_OK) return rc;
+    }
+    auto to_left = [&](int i, int j) {
+      for (size_t k = 0; k < q2pairs.size(); ++k)
+        if (q2pairs[k].first == i && q2pairs[k].second == j) return r2[k] > 0.0;
+      return false;
+    };
+    // Alg. 9 PairLoops: greedy nearest-left proper translate per alpha
+    std::vector<uint8_t> used(n_loops, 0);
+    for (int f : need_pair) {
+      for (int la = h_flo[f]; la < h_flo[f + 1]; ++la) {
+        bool is_alpha = false;
+        for (int i : left) if (cands[i].alpha == la) { is_alpha = true; break; }
+        const LoopInfo &Ia = L[la];
+        int cp = 0, cq = 0;
+        for (int l = h_flo[f]; l < h_flo[f + 1]; ++l)
+          if (L[l].nseg && (L[l].cu || L[l].cv)) { cp = L[l].cu; cq = L[l].cv; break; }
+        if (!(Ia.nseg && Ia.cu == cp && Ia.cv == cq)) continue;
+        int best = -1;
+        if (is_alpha)
+          for (int i : left) {
+            if (cands[i].alpha != la || used[cands[i].beta]) continue;
+            if (best < 0 || to_left(i, best)) best = i;
+          }
+        if (best < 0) { status[f] = WN_FACE_PAIRING; break; }
+        used[cands[best].beta] = 1;
+        pair_beta[la] = cands[best].beta;
+        pair_s[la] = cands[best].s;
+      }
+    }
+    for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
+  }
+  if (face_status && n_faces)
+    WN_CUDA(cudaMemcpyAsync(face_status, status.data(), sizeof(int32_t) * n_faces, cudaMemcpyHostToDevice, st));
+  if (any_bad) {
+    WN_CUDA(cudaStreamSynchronize(st));
+    int first = 0;
+    while (first < n_faces && !status[first]) ++first;
+    set_error("wn_build_faces: face %d invalid (code %d)", first, status[first]);
+    bool geom = false, unsup = false;
+    for (int f = 0; f < n_faces; ++f) { geom |= status[f] == WN_FACE_GEOM; unsup |= status[f] == WN_FACE_GENERAL_PQ; }
+    return geom ? WN_ERR_GEOM : (unsup ? WN_ERR_UNSUPPORTED : WN_ERR_TOPOLOGY);
+  }
+
+  // --- final plan ---
+  Plan P;
+  std::vector<double> fdom(4 * (size_t)n_faces);
+  for (int f = 0; f < n_faces; ++f) {
+    const FaceCtx &C = ctx[f];
+    fdom[4 * f] = C.u0; fdom[4 * f + 1] = C.Tu; fdom[4 * f + 2] = C.v0; fdom[4 * f + 3] = C.Tv;
+    P.begin_face(f);
+    for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
+      const LoopInfo &I = L[l];
+      if (I.nseg == 0) continue;
+      if (C.per == 0 || (I.cu == 0 && I.cv == 0)) {
+        plan_contractible(P, l, I, C);
+        continue;
+      }
+      const int axis = (I.cu != 0) ? 0 : 1;
+      if (C.per != 3) {
+        // uni-periodic non-contractible loop: omega(p,L) + copies (Eq. 5)
+        P.add(G_LINE, 0, l, 0, 0, I, C.M);
+        plan_extended_copies(P, l, I, C, axis, 0, false);
+        continue;
+      }
+      // bi-periodic: alpha loops drive Eq. 8 for their pair; beta loops are emitted with them
+      if (pair_beta[l] < 0) continue;
+      const int lb = pair_beta[l];
+      const int sb = pair_s[l];
+      const LoopInfo &Ib = L[lb];
+      const int tax = axis == 0 ? 1 : 0;
+      const double Tt = tax ? C.Tv : C.Tu, t0 = tax ? C.v0 : C.u0;
+      const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
+      // transverse window: every band offset j whose lines or copies can meet the tile
+      const double ca = tax ? I.sy : I.sx, cb = (tax ? Ib.sy : Ib.sx) + sb * Tt;
+      const double lo = std::min({ca, cb, tax ? I.bb[1] : I.bb[0], (tax ? Ib.bb[1] : Ib.bb[0]) + sb * Tt});
+      const double hi = std::max({ca, cb, tax ? I.bb[3] : I.bb[2], (tax ? Ib.bb[3] : Ib.bb[2]) + sb * Tt});
+      int j0, j1;
+      k_range(lo, hi, t0, Tt, m, j0, j1);
+      for (int j = j0; j <= j1; ++j) {
+        // Eq. 8 band j: omega(p, L_alpha) + omega(p, L_beta) only when the strip meets the tile
+        const double la_c = ca + j * Tt, lb_c = cb + j * Tt;
+        if (std::min(la_c, lb_c) <= t0 + Tt + m && std::max(la_c, lb_c) >= t0 - m) {
+          if (axis == 0) { P.add(G_LINE, 0, l, 0, j, I, C.M); P.add(G_LINE, 0, lb, 0, sb + j, Ib, C.M); }
+          else { P.add(G_LINE, 0, l, j, 0, I, C.M); P.add(G_LINE, 0, lb, sb + j, 0, Ib, C.M); }
+        }
+        plan_extended_copies(P, l, I, C, axis, j, true);
+        plan_extended_copies(P, lb, Ib, C, axis, sb + j, true);
+      }
+    }
+  }
+  P.end();
+  if (P.recs < 0 || P.colds >= (1 << 23) * 64) { set_error("too many records"); return WN_ERR_ARG; }
+  for (int f = 0; f < n_faces; ++f)
+    if (P.cold_off[f + 1] - P.cold_off[f] >= (1 << 23) || P.rec_off[f + 1] - P.rec_off[f] >= (1 << 24)) {
+      set_error("face %d: too many records for the 23/24-bit record indices", f);
+      return WN_ERR_ARG;
+    }
+
+  wn_faces_t F = new wn_faces_s();
+  F->precision = fp32 ? 1 : 0;
+  F->opt = O;
+  F->eps = eps;
+  F->max_depth = maxd;
+  F->device = dev;
+  std::vector<uint8_t> fper(n_faces);
+  for (int f = 0; f < n_faces; ++f) fper[f] = ctx[f].per;
+  wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, F) : materialise<double>(B, P, fper, fdom, F);
+  if (rc != WN_OK) { free_handle(F); return rc; }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build sync"); }
+  *out = F;
+  return WN_OK;
+}
+
+extern "C" wn_status_t wn_faces_info(wn_faces_t F, wn_faces_info_t *out) {
+  if (!F || !out) { set_error("wn_faces_info: NULL"); return WN_ERR_ARG; }
+  out->n_records = F->n_records;
+  out->n_seg_records = F->n_seg;
+  out->n_groups = F->n_groups;
+  out->n_lines = F->n_lines;
+  out->bytes = F->bytes;
+  out->precision = F->precision;
+  out->max_face_records = F->max_face_records;
+  return WN_OK;
+}
+
+extern "C" wn_status_t wn_set_counters(wn_faces_t F, int enable) {
+  if (!F) { set_error("wn_set_counters: NULL"); return WN_ERR_ARG; }
+  F->counters_on = enable ? 1 : 0;
+  return WN_OK;
+}
+
+extern "C" wn_status_t wn_get_counters(wn_faces_t F, void *stream, int64_t *out) {
+  if (!F || !out) { set_error("wn_get_counters: NULL"); return WN_ERR_ARG; }
+  unsigned long long h[8];
+  WN_CUDA(cudaMemcpyAsync(h, F->counters, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  WN_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
+  return WN_OK;
+}
+
+extern "C" void wn_free_faces(wn_faces_t F) { free_handle(F); }
+
+extern "C" const char *wn_last_error(void) { return wn::g_err; }
+
+extern "C" int32_t wn_last_build_launches(void) { return wn::g_build_launches; }

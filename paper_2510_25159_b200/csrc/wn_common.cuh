@@ -1,0 +1,190 @@
+// wn_common.cuh -- record layout, device primitives and the faces handle of
+// libwn (B200 / sm_100a).  PAPER.md is cited as P:<line>.
+//
+// Per face the build emits a flat "record program" (hot records, staged in
+// shared memory by the query kernel) plus one cold record per emitted curve
+// segment (read only by the recursion of hard pairs).
+// "Data layout in HBM".
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <utility>
+#include <vector>
+
+#include "../../include/wn.h"
+
+namespace wn {
+
+// ---------------------------------------------------------------------------
+// hot record kinds (meta & 0xF) and flag bits (meta bits 4..7); meta >> 8 = aux
+// ---------------------------------------------------------------------------
+enum : uint32_t {
+  K_SEG = 1,     // (a,b) = F1, c = root span S0 (Eq. 1 with R5 margin); aux = face-local cold index
+  K_MOVE = 2,    // (a,b) = chain start; sets group start A and the previous point
+  K_MOVEG = 3,   // (a,b) = next chain start after a gap; crossing mode adds the gap terms
+  K_GROUP = 4,   // cull header: bbox (float4 in a,b for fp64; a,b,c + next record for fp32); aux = records to skip
+  K_LINE = 5,    // a = line coordinate; omega(p,L) = +-1/2
+  K_XCH = 6,     // extended copy closing (crossing mode): -c(A -> Z)
+  K_NCH = 7,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
+  K_CLOSEG = 8,  // open contractible loop: gap chord Z -> A (crossing mode)
+  K_PAD = 9      // second half of an fp32 GROUP header
+};
+constexpr uint32_t F_ANGLE = 1u << 4;   // literal atan2 chord angles (angle_mode = 1)
+constexpr uint32_t F_AXISV = 1u << 5;   // LINE parallel to v: test the u coordinate
+constexpr uint32_t F_GE = 1u << 6;      // LINE: left iff q >= c (else q <= c)
+
+template <typename R>
+struct Hot;
+template <>
+struct __align__(32) Hot<double> {
+  double a, b, c;
+  uint32_t meta, pad;
+};
+template <>
+struct __align__(16) Hot<float> {
+  float a, b, c;
+  uint32_t meta;
+};
+
+// Cold record: exact chain end points, the derivative bound and Horner-ready
+// homogeneous coefficients c_j = C(n,j) w_j (x_j, y_j, 1) (O(n) evaluation,
+// Table 1).
+template <typename R>
+struct Cold {
+  R f0x, f0y, f1x, f1y;
+  R B;      // derivative bound (A.1) incl. relative margin
+  R M;      // absolute margin (R5)
+  int32_t n, pad;
+  R cx[6], cy[6], cw[6];
+};
+
+// hard-pair queue entry: q (8 bits) | angle (1 bit) | cold local index (23 bits)
+__host__ __device__ inline uint32_t hp_pack(int q, int angle, int cold) {
+  return (uint32_t)q | ((uint32_t)angle << 8) | ((uint32_t)cold << 9);
+}
+
+struct Tile {
+  int32_t face;
+  int32_t qcnt;
+  int64_t qbeg;
+};
+
+// build-plan group (host -> device), 32 B
+enum : int32_t { G_LOOP = 0, G_COPY = 1, G_LINE = 2 };
+enum : int32_t { PF_CULL = 1, PF_ANGLE = 2, PF_TAIL_CLOSEG = 4, PF_TAIL_XCH = 8, PF_TAIL_NCH = 16 };
+struct PlanGroup {
+  int32_t kind, flags;
+  int32_t loop;
+  int32_t ku, kv;       // lattice translate added to the lifted loop
+  int32_t rec_off;      // global hot record offset of this group
+  int32_t cold_off;     // global cold record offset of its first SEG
+  int32_t cold_local;   // face-local index of its first SEG
+  int32_t nrec;         // hot records of this group (incl. header)
+  int32_t face;         // target face
+  double M;             // absolute margin of the target face (R5)
+};
+
+// per-loop summary written by the lifting kernel (K2a), read by the planner
+struct LoopInfo {
+  int32_t cu, cv;       // homology class
+  int32_t nbrk;         // junctions that are not bit-continuous after lifting
+  int32_t closed;       // last end point == first start point (bitwise)
+  int32_t err;          // geometry error in one of its segments
+  int32_t nseg;
+  double sx, sy;        // lifted start point (beta_0)
+  double bb[4];         // lifted control-point box xmin, ymin, xmax, ymax
+};
+
+constexpr int QT = 256;          // queries per tile (one per thread)
+constexpr int NWARP = QT / 32;
+constexpr int QW = 128;          // per-warp hard-pair queue capacity
+constexpr int MAXD = 64;         // hard cap of the explicit stack
+constexpr double TWO_PI = 6.283185307179586476925286766559;
+
+// ---------------------------------------------------------------------------
+// device primitives
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double datan2(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ float datan2(float y, float x) { return atan2f(y, x); }
+
+// Branch-cut crossing of the chord a -> b (coordinates relative to p) with the
+// ray {p + s(-1,0), s >= 0}: the integer c with
+//     omega(p,a,b) = (theta(b) - theta(a)) / 2pi + c,
+// theta = atan2 in (-pi, pi].  Exact; valid when p
+// is not on the chord, which the ellipse margin guarantees for pruned chords.
+template <typename R>
+__device__ __forceinline__ int xcount(R ax, R ay, R bx, R by) {
+  bool ua = ay >= R(0), ub = by >= R(0);
+  if (ua == ub) return 0;
+  R cr = ax * by - ay * bx;
+  return ua ? (cr >= R(0) ? 1 : 0) : (cr < R(0) ? -1 : 0);
+}
+
+// Same, for chords p may lie on (gap / copy-closing chords): also covers the
+// horizontal chord through p, consistent with omega(p,a,b) = +1/2 there (R11).
+// `cr` must be the canonicalised cross product also fed to atan2.
+template <typename R>
+__device__ __forceinline__ int xcount_exact(R ax, R ay, R bx, R by, R cr) {
+  bool ua = ay >= R(0), ub = by >= R(0);
+  if (ua && !ub) return cr >= R(0) ? 1 : 0;
+  if (!ua && ub) return cr < R(0) ? -1 : 0;
+  if (ua && ub && ay == R(0) && by == R(0) && ax < R(0) && bx > R(0)) return 1;
+  return 0;
+}
+
+template <typename R>
+__device__ __forceinline__ R canon_cross(R ax, R ay, R bx, R by) {
+  R cr = ax * by - ay * bx;
+  return cr == R(0) ? R(0) : cr;   // -0 -> +0 (R11)
+}
+
+// omega(p,a,b) * 2pi = atan2(cross, dot) (R7, R11), coordinates relative to p
+template <typename R>
+__device__ __forceinline__ R chord_angle(R ax, R ay, R bx, R by) {
+  R cr = canon_cross(ax, ay, bx, by);
+  return datan2(cr, ax * bx + ay * by);
+}
+
+}  // namespace wn
+
+// ---------------------------------------------------------------------------
+// the faces handle
+// ---------------------------------------------------------------------------
+struct wn_faces_s {
+  int32_t n_faces = 0;
+  int precision = 0;
+  wn_options_t opt{};
+  double eps = 1e-10;
+  int max_depth = 48;
+  int device = 0;
+  void *hot = nullptr;             // Hot<R>[n_records]
+  void *cold = nullptr;            // Cold<R>[n_seg]
+  int32_t *face_rec_off = nullptr; // [n_faces+1]
+  int32_t *face_cold_off = nullptr;// [n_faces+1]
+  int32_t *face_order = nullptr;   // [n_faces] by cost, descending
+  double *face_dom = nullptr;      // [n_faces][4]
+  uint8_t *face_per = nullptr;     // [n_faces]
+  uint8_t *face_ok = nullptr;      // [n_faces]
+  unsigned long long *counters = nullptr;  // [8]
+  int counters_on = 0;
+  int timing_on = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k3_events;
+  int64_t n_records = 0, n_seg = 0, n_groups = 0, n_lines = 0, bytes = 0;
+  int32_t max_face_records = 0;
+};
+
+namespace wn {
+void set_error(const char *fmt, ...);
+wn_status_t cuda_fail(cudaError_t e, const char *what);
+}  // namespace wn
+
+#define WN_CUDA(call)                                          \
+  do {                                                         \
+    cudaError_t e__ = (call);                                  \
+    if (e__ != cudaSuccess) return wn::cuda_fail(e__, #call);  \
+  } while (0)

@@ -1,0 +1,197 @@
+"""GPU <-> oracle parity through the C ABI (-m gpu).
+
+Contract (BASELINE.json north_star): on every query the oracle
+certifies as COMPARABLE (farther than delta from every curve, winding farther
+than tol from a half-integer) the inside/outside flag is bit-exact and
+|omega_gpu - omega_oracle| <= 1e-9 (fp64) / 1e-4 (fp32, oracle on the fp32-
+rounded inputs, R19); the GPU never reports on-boundary there."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+import paper_2510_25159_b200 as wn  # noqa: E402
+from tests import helpers as H  # noqa: E402
+from wn_workloads import configs as G  # noqa: E402
+
+TOL64, TOL32 = 1e-9, 1e-4
+DELTA64, DELTA32 = 1e-9, 1e-5
+
+
+def _gpu(wl, face_id=None, uv=None, **kw):
+    faces = wn.Faces.from_workload(wl, **kw)
+    r = faces.query(wl["face_id"] if face_id is None else face_id, wl["uv"] if uv is None else uv)
+    torch.cuda.synchronize()
+    out = r.winding.cpu().numpy(), r.flag.cpu().numpy()
+    faces.close()
+    return out
+
+
+def _check(wl, w, fl, idx=None, fp32=False, min_cmp=0.9, **okw):
+    fid = wl["face_id"] if idx is None else wl["face_id"][idx]
+    uv = wl["uv"] if idx is None else wl["uv"][idx]
+    delta, tol = (DELTA32, TOL32) if fp32 else (DELTA64, TOL64)
+    r = oracle.query(wl, face_id=fid, uv=uv, delta=delta, tol=tol, **okw)
+    if idx is not None:
+        w, fl = w[idx], fl[idx]
+    cm = r["comparable"]
+    assert cm.mean() >= min_cmp, cm.mean()
+    assert not np.any(fl[cm] == 2), "GPU on-boundary on a certified-far query"
+    assert not np.any(fl[cm] == 3)
+    bad = np.nonzero(fl[cm] != r["flag"][cm])[0]
+    assert bad.size == 0, (bad.size, w[cm][bad[:5]], r["w"][cm][bad[:5]], uv[cm][bad[:5]])
+    err = np.abs(w[cm] - r["w"][cm])
+    assert err.max() <= tol, (err.max(), uv[cm][np.argmax(err)])
+    return err.max(), cm.mean()
+
+
+@pytest.mark.parametrize("angle_mode", [0, 1])
+def test_c1_full(angle_mode):
+    wl = G.gen_c1()
+    w, fl = _gpu(wl, angle_mode=angle_mode)
+    _check(wl, w, fl, min_cmp=0.999)
+
+
+@pytest.mark.parametrize("angle_mode", [0, 1])
+def test_c2_sampled(angle_mode):
+    wl = G.gen_c2(n_queries=60_000)
+    w, fl = _gpu(wl, angle_mode=angle_mode)
+    _check(wl, w, fl, min_cmp=0.85)
+    # the near-curve shell (1e-6) is part of the batch
+    assert wl["meta"]["near_mask"].sum() > 5000
+
+
+def test_c2_full_size_sampled():
+    """BASELINE configs[1] at full size (1M queries) in the bench launch
+    configuration; the oracle checks a 40k sample."""
+    wl = G.gen_c2()
+    w, fl = _gpu(wl)
+    idx = np.random.default_rng(0).choice(len(w), 40_000, replace=False)
+    _check(wl, w, fl, idx=idx, min_cmp=0.85)
+    assert np.all(fl != 3)
+
+
+@pytest.mark.parametrize("angle_mode", [0, 1])
+def test_c3_torus(angle_mode):
+    wl = G.gen_c3(n_queries=20_000)
+    w, fl = _gpu(wl, angle_mode=angle_mode)
+    _check(wl, w, fl, min_cmp=0.99)
+
+
+def test_c4_fp64():
+    wl = G.gen_c4(n_faces=200, n_deleted=20)
+    w, fl = _gpu(wl)
+    _check(wl, w, fl, min_cmp=0.95)
+
+
+def test_c4_fp32():
+    wl = G.to_fp32_inputs(G.gen_c4(n_faces=200, n_deleted=20))
+    w, fl = _gpu(wl, precision=1)
+    _check(wl, w, fl, fp32=True, min_cmp=0.95)
+
+
+@pytest.mark.parametrize("angle_mode", [0, 1])
+def test_c5_reduced(angle_mode):
+    wl = G.gen_c5(n_faces=120, grid=32)
+    w, fl = _gpu(wl, angle_mode=angle_mode)
+    _check(wl, w, fl, min_cmp=0.97)
+
+
+def test_c5_full_size_sampled():
+    """BASELINE configs[4] at full size (20,000 faces x 64x64 grid = 81.92M
+    queries), sampled oracle check."""
+    wl = G.gen_c5()
+    w, fl = _gpu(wl)
+    idx = np.random.default_rng(1).choice(len(w), 20_000, replace=False)
+    _check(wl, w, fl, idx=idx, min_cmp=0.97)
+
+
+# ----------------------------------------------------------------------------
+# edge cases
+# ----------------------------------------------------------------------------
+
+def test_unsorted_batch_equals_sorted():
+    wl = G.gen_c4(n_faces=50, q_per_face=300, n_deleted=5)   # 300: ragged tiles
+    w, fl = _gpu(wl)
+    perm = np.random.default_rng(2).permutation(len(w))
+    w2, fl2 = _gpu(wl, face_id=wl["face_id"][perm], uv=wl["uv"][perm])
+    assert np.array_equal(fl2, fl[perm])
+    assert np.array_equal(np.isnan(w2), np.isnan(w[perm]))
+    ok = ~np.isnan(w2)
+    assert np.max(np.abs(w2[ok] - w[perm][ok])) < 1e-12
+
+
+def test_invalid_queries_flag3_and_empty():
+    wl = G.gen_c1(n_queries=100)
+    fid = wl["face_id"].copy()
+    uv = wl["uv"].copy()
+    fid[3] = 7
+    fid[5] = -1
+    uv[9, 0] = np.nan
+    w, fl = _gpu(wl, face_id=fid, uv=uv)
+    assert fl[3] == 3 and fl[5] == 3 and fl[9] == 3
+    assert np.isnan(w[3]) and np.isnan(w[9])
+    assert np.all(fl[[0, 1, 2, 4, 6, 7, 8]] != 3)
+    faces = wn.Faces.from_workload(wl)
+    r = faces.query(np.zeros(0, np.int32), np.zeros((0, 2)))
+    assert r.winding.numel() == 0
+
+
+def test_on_boundary_exact_vertex():
+    wl = G.gen_c1(n_queries=10)
+    uv = wl["uv"].copy()
+    uv[0] = wl["ctrl_uv"][0]          # a segment end point: d = 0 < eps (Alg. 1 line 1)
+    w, fl = _gpu(wl, uv=uv)
+    assert fl[0] == 2 and np.isnan(w[0])
+
+
+def test_periodic_reduction_equals_in_tile():
+    wl = G.gen_c3(n_queries=3000)
+    T = wl["meta"]["T"]
+    w, fl = _gpu(wl)
+    shifted = wl["uv"] + np.array([T, -2 * T])
+    w2, fl2 = _gpu(wl, uv=shifted)
+    ok = fl != 2
+    assert np.array_equal(fl[ok], fl2[ok])
+    assert np.max(np.abs(w[ok] - w2[ok])) < 1e-9
+
+
+def test_single_extended_curve_nonstrict():
+    """Worked values S:301-302 / P:480-481 through the GPU (strict=0)."""
+    loop = H.line_loop((0.0, 0.5), (1.0, 0.5), n=3)
+    wl = H.make_wl([([loop], 1, (0.0, 1.0, 0.0, 1.0))], [(0.3, 0.8), (0.3, 0.2)])
+    w, fl = _gpu(wl, strict=False)
+    assert w[0] == pytest.approx(0.5, abs=1e-14) and w[1] == pytest.approx(-0.5, abs=1e-14)
+    with pytest.raises(wn.WNError) as ei:
+        wn.Faces.from_workload(wl)
+    assert ei.value.status == 3 and ei.value.face_status[0] == 2
+
+
+def test_bad_geometry_rejected():
+    wl = G.gen_c1(n_queries=10)
+    bad = dict(wl)
+    bad["ctrl_w"] = np.ones(len(wl["ctrl_uv"]))
+    bad["ctrl_w"][4] = -1.0
+    with pytest.raises(wn.WNError) as ei:
+        wn.Faces.from_workload(bad)
+    assert ei.value.status == 2
+    bad2 = dict(wl)
+    bad2["seg_degree"] = wl["seg_degree"].copy()
+    bad2["seg_degree"][0] = 7
+    with pytest.raises(wn.WNError) as ei:
+        wn.Faces.from_workload(bad2)
+    assert ei.value.status == 1
+
+
+def test_counters_and_info():
+    wl = G.gen_c2(n_queries=20_000)
+    faces = wn.Faces.from_workload(wl)
+    faces.set_counters(True)
+    faces.query(wl["face_id"], wl["uv"])
+    c = faces.counters()
+    info = faces.info()
+    assert info["n_seg_records"] == 80
+    assert c["pairs_tested"] > 0 and c["hard_pairs"] > 0 and c["max_depth"] <= 48
+    assert wn.last_query_launches() >= 1

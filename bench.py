@@ -59,6 +59,22 @@ def _env_int(k, d):
         return d
 
 
+def max_over_ranks(x, dist=None, device=None):
+    """Max of a per-rank scalar over all ranks (the timing rule: device time,
+    max over ranks).  dist=None -> single process."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def rank_seed(rank):
+    """Weak scaling: every rank runs its own independent C5 batch."""
+    return 5 + int(rank)
+
+
 def _clock_sampler(gpu_index):
     cmd = ["nvidia-smi", "-i", str(gpu_index),
            "--query-gpu=timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -186,7 +202,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    wl = G.gen_c5(seed=5 + rank)
+    wl = G.gen_c5(seed=rank_seed(rank))
     nq = len(wl["face_id"])
     pairs = G.n_input_pairs(wl)
     st = torch.cuda.current_stream(dev)
@@ -245,11 +261,7 @@ def main():
         dist.barrier()
     elapsed = e0.elapsed_time(e1)
     clocks = _clock_summary(clk, tw0, tw1) if rank == 0 else None
-    t_max = elapsed
-    if dist:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(elapsed, dist, dev)
     ms_step = t_max / args.steps
     value = nq * world / (ms_step / 1e3)
     pairs_s = pairs * world / (ms_step / 1e3)
@@ -312,11 +324,7 @@ def main():
             e2e_step()
         b.record(st)
         torch.cuda.synchronize()
-        et = a.elapsed_time(b)
-        if dist:
-            tt = torch.tensor([et], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            et = float(tt.item())
+        et = max_over_ranks(a.elapsed_time(b), dist, dev)
         e2e = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 

@@ -5,6 +5,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -17,6 +19,20 @@
 namespace wn {
 
 static thread_local char g_err[512] = "";
+
+// WN_TRACE=1: host-side phase timings of wn_build_faces on stderr
+struct Trace {
+  bool on = std::getenv("WN_TRACE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char *what) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[wn_build] %-28s %8.3f ms (total %8.3f)\n", what,
+            std::chrono::duration<double, std::milli>(now - last).count(),
+            std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 thread_local int32_t g_build_launches = 0;
 
 void set_error(const char *fmt, ...) {
@@ -169,18 +185,27 @@ struct Emit;
 __device__ __forceinline__ float f_dn(double x) { return __double2float_rd(x); }
 __device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 
+// write a point-like record: (x, y) exact, s = span of the conservative filter
 template <typename R>
-__device__ void put_hot(Hot<R> *H, int r, R a, R b, R c, uint32_t meta);
+__device__ void put_rec(Hot<R> *H, int r, double x, double y, double s, uint32_t meta);
 template <>
-__device__ void put_hot<double>(Hot<double> *H, int r, double a, double b, double c, uint32_t meta) {
+__device__ void put_rec<double>(Hot<double> *H, int r, double x, double y, double s, uint32_t meta) {
   Hot<double> h;
-  h.a = a; h.b = b; h.c = c; h.meta = meta; h.pad = 0;
+  h.fx = __double2float_rn(x);
+  h.fy = __double2float_rn(y);
+  h.fs = f_up(s);
+  h.meta = meta;
+  h.x = x;
+  h.y = y;
   H[r] = h;
 }
 template <>
-__device__ void put_hot<float>(Hot<float> *H, int r, float a, float b, float c, uint32_t meta) {
+__device__ void put_rec<float>(Hot<float> *H, int r, double x, double y, double s, uint32_t meta) {
   Hot<float> h;
-  h.a = a; h.b = b; h.c = c; h.meta = meta;
+  h.a = __double2float_rn(x);
+  h.b = __double2float_rn(y);
+  h.c = f_up(s);
+  h.meta = meta;
   H[r] = h;
 }
 
@@ -190,10 +215,12 @@ template <>
 __device__ void put_group<double>(Hot<double> *H, int r, double xmin, double ymin, double xmax, double ymax,
                                   uint32_t meta) {
   Hot<double> h;
-  float2 lo = make_float2(f_dn(xmin), f_dn(ymin)), hi = make_float2(f_up(xmax), f_up(ymax));
-  memcpy(&h.a, &lo, 8);
-  memcpy(&h.b, &hi, 8);
-  h.c = 0.0; h.meta = meta; h.pad = 0;
+  h.fx = f_dn(xmin);
+  h.fy = f_dn(ymin);
+  h.fs = f_up(xmax);
+  h.meta = meta;
+  h.x = ymax;
+  h.y = 0.0;
   H[r] = h;
 }
 template <>
@@ -245,7 +272,7 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     double c;
     if (I.cu != 0) { c = by; if (I.cu > 0) meta |= F_GE; }          // v = (+-T,0): left iff p.v >=/<= c
     else { c = bx; meta |= F_AXISV; if (I.cv < 0) meta |= F_GE; }   // v = (0,+-T): left iff p.u <=/>= c
-    put_hot<R>(hot, r, (R)c, (R)0, (R)0, meta);
+    put_rec<R>(hot, r, c, 0.0, 0.0, meta);
     return;
   }
   if (G.flags & PF_CULL) {
@@ -265,15 +292,16 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
       px[j] = X(ctrl[2 * (o + j)], k.x);
       py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
     }
-    if (s == s0) put_hot<R>(hot, r++, (R)px[0], (R)py[0], (R)0, K_MOVE | fa);
-    else if (brk[s]) put_hot<R>(hot, r++, (R)px[0], (R)py[0], (R)0, K_MOVEG | fa);
+    if (s == s0) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVE | fa);
+    else if (brk[s]) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVEG | fa);
     const double2 bp = prep[s];
-    // Eq. 1 root span with the R5 margin (relative + absolute); Eq. 2 uses B
-    double S0 = bp.y * (1.0 + rel) + G.M;
-    double Bm = bp.x * (1.0 + rel);
-    R S0r, Br;
-    if (sizeof(R) == 4) { S0r = (R)f_up(S0); Br = (R)f_up(Bm); } else { S0r = (R)S0; Br = (R)Bm; }
-    put_hot<R>(hot, r++, (R)px[n], (R)py[n], S0r, K_SEG | fa | ((uint32_t)cl << 8));
+    // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
+    // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
+    // see k_query; fp32 records: S0 (1 + 2^-17) + M32.  Eq. 2 uses B (cold).
+    const double S0 = (sizeof(R) == 8) ? bp.y * (1.0 + 0x1p-17) + G.M * 0x1p24 : bp.y * (1.0 + rel) + G.M;
+    const double Bm = bp.x * (1.0 + rel);
+    const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
+    put_rec<R>(hot, r++, px[n], py[n], S0, K_SEG | fa | ((uint32_t)cl << 8));
     Cold<R> C;
     C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
     C.B = Br;
@@ -295,9 +323,9 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     ++cl;
     ++cg;
   }
-  if (G.flags & PF_TAIL_CLOSEG) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_CLOSEG | fa);
-  if (G.flags & PF_TAIL_XCH) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_XCH | fa);
-  if (G.flags & PF_TAIL_NCH) put_hot<R>(hot, r++, (R)0, (R)0, (R)0, K_NCH | fa);
+  if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
+  if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
+  if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
 }
 
 // ---------------------------------------------------------------------------
@@ -460,6 +488,7 @@ void free_handle(wn_faces_t F) {
   cudaFree(F->face_dom);
   cudaFree(F->face_per);
   cudaFree(F->face_ok);
+  cudaFree(F->face_M);
   cudaFree(F->counters);
   delete F;
 }
@@ -481,7 +510,7 @@ struct BuildCtx {
 // emit the records of `plan` into a new handle whose faces carry `fper`/`fdom`
 template <typename R>
 wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<uint8_t> &fper,
-                        const std::vector<double> &fdom, wn_faces_t F) {
+                        const std::vector<double> &fdom, const std::vector<double> &fM, wn_faces_t F) {
   cudaStream_t st = B.st;
   const int nf = (int)fper.size();
   F->n_faces = nf;
@@ -497,6 +526,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   WN_CUDA(cudaMalloc(&F->face_dom, sizeof(double) * 4 * std::max(nf, 1)));
   WN_CUDA(cudaMalloc(&F->face_per, std::max(nf, 1)));
   WN_CUDA(cudaMalloc(&F->face_ok, std::max(nf, 1)));
+  WN_CUDA(cudaMalloc(&F->face_M, sizeof(double) * std::max(nf, 1)));
   WN_CUDA(cudaMalloc(&F->counters, 8 * sizeof(unsigned long long)));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
   std::vector<int32_t> order(nf);
@@ -515,6 +545,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     WN_CUDA(cudaMemcpyAsync(F->face_dom, fdom.data(), sizeof(double) * 4 * nf, cudaMemcpyHostToDevice, st));
     WN_CUDA(cudaMemcpyAsync(F->face_per, fper.data(), nf, cudaMemcpyHostToDevice, st));
     WN_CUDA(cudaMemcpyAsync(F->face_ok, ok.data(), nf, cudaMemcpyHostToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(F->face_M, fM.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, st));
   }
   const int ng = (int)plan.groups.size();
   if (ng) {
@@ -568,6 +599,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   cudaStream_t st = (cudaStream_t)stream;
   DevBuf D;
   D.st = st;
+  Trace tr;
 
   // --- host copies of the small CSR / face arrays ---
   std::vector<int32_t> h_lso(n_loops + 1), h_flo(n_faces + 1);
@@ -601,6 +633,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   int32_t h_bad = 0;
   WN_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
+  tr.mark("csr d2h + degree scan");
   // CSR / domain checks on the host
   bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
   for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
@@ -636,6 +669,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   std::vector<LoopInfo> L(n_loops);
   if (n_loops) WN_CUDA(cudaMemcpyAsync(L.data(), B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
+  tr.mark("prep + lift + info d2h");
 
   // --- K2b: validation + planning (host) ---
   std::vector<int32_t> status(n_faces, WN_FACE_OK);
@@ -682,7 +716,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     std::vector<int> vface(n_loops, -1);
     Plan VP;
     std::vector<uint8_t> vper;
-    std::vector<double> vdom;
+    std::vector<double> vdom, vM;
     for (int f : need_pair) {
       for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
         const LoopInfo &I = L[l];
@@ -694,6 +728,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
         vface[l] = (int)vper.size();
         vper.push_back(C.per);
         vdom.insert(vdom.end(), {ctx[f].u0, ctx[f].Tu, ctx[f].v0, ctx[f].Tv});
+        vM.push_back(C.M);
         VP.begin_face(vface[l]);
         VP.add(G_LINE, 0, l, 0, 0, I, C.M);
         plan_extended_copies(VP, l, I, C, axis, 0, false);
@@ -731,7 +766,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
       wn_faces_t T = new wn_faces_s();
       T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0;
-      wn_status_t rc = materialise<double>(B, VP, vper, vdom, T);
+      wn_status_t rc = materialise<double>(B, VP, vper, vdom, vM, T);
       if (rc != WN_OK) { free_handle(T); return rc; }
       const int nq = (int)Q.size();
       std::vector<int32_t> hf(nq);
@@ -821,6 +856,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     return geom ? WN_ERR_GEOM : (unsup ? WN_ERR_UNSUPPORTED : WN_ERR_TOPOLOGY);
   }
 
+  tr.mark("validate + pairing");
   // --- final plan ---
   Plan P;
   std::vector<double> fdom(4 * (size_t)n_faces);
@@ -876,6 +912,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       return WN_ERR_ARG;
     }
 
+  tr.mark("plan");
   wn_faces_t F = new wn_faces_s();
   F->precision = fp32 ? 1 : 0;
   F->opt = O;
@@ -884,10 +921,14 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   F->device = dev;
   std::vector<uint8_t> fper(n_faces);
   for (int f = 0; f < n_faces; ++f) fper[f] = ctx[f].per;
-  wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, F) : materialise<double>(B, P, fper, fdom, F);
+  std::vector<double> fM(n_faces);
+  for (int f = 0; f < n_faces; ++f) fM[f] = ctx[f].M;
+  wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, fM, F) : materialise<double>(B, P, fper, fdom, fM, F);
   if (rc != WN_OK) { free_handle(F); return rc; }
+  tr.mark("materialise (alloc+h2d+emit)");
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build sync"); }
+  tr.mark("final sync");
   *out = F;
   return WN_OK;
 }

@@ -38,10 +38,14 @@ constexpr uint32_t F_GE = 1u << 6;      // LINE: left iff q >= c (else q <= c)
 
 template <typename R>
 struct Hot;
+// fp64 records carry an fp32 copy of the point and an fp32 span for the
+// conservative single-precision filter of the root ellipse test, plus the exact
+// fp64 point used for every decision that affects the value.
 template <>
 struct __align__(32) Hot<double> {
-  double a, b, c;
-  uint32_t meta, pad;
+  float fx, fy, fs;   // fp32 point (nearest) and filter span (rounded up, margins included)
+  uint32_t meta;
+  double x, y;        // exact point (SEG/MOVE/MOVEG), line coordinate (LINE: x), GROUP: ymax in x
 };
 template <>
 struct __align__(16) Hot<float> {
@@ -70,6 +74,13 @@ struct Tile {
   int32_t face;
   int32_t qcnt;
   int64_t qbeg;
+};
+
+// global hard-pair queue entry (phase 2 runs in its own kernel)
+struct HardEntry {
+  double px, py;      // reduced query point
+  int32_t q;          // query index (output position)
+  uint32_t c;         // global cold record index | angle-mode bit 31
 };
 
 // build-plan group (host -> device), 32 B
@@ -170,6 +181,7 @@ struct wn_faces_s {
   double *face_dom = nullptr;      // [n_faces][4]
   uint8_t *face_per = nullptr;     // [n_faces]
   uint8_t *face_ok = nullptr;      // [n_faces]
+  double *face_M = nullptr;        // [n_faces] absolute margin M (R5) per face
   unsigned long long *counters = nullptr;  // [8]
   int counters_on = 0;
   int timing_on = 0;

@@ -14,6 +14,8 @@
 // explicit stack.  a8 reduces, classifies and stores.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+
 #include "wn_common.cuh"
 
 namespace wn {
@@ -74,6 +76,7 @@ struct QParams {
   const int32_t *face_cold_off;
   const double *face_dom;
   const uint8_t *face_per;
+  const double *face_M;
   const double *uv;
   double *winding;
   uint8_t *flag;
@@ -81,7 +84,12 @@ struct QParams {
   const int32_t *ntiles;
   const int32_t *perm;
   const int32_t *unsorted;
-  R eps;
+  HardEntry *hq;          // global hard-pair queue
+  int32_t *hq_count;
+  int32_t hq_cap;
+  int32_t *pend;          // queries with queued hard pairs
+  int32_t *pend_count;
+  double eps;
   int max_depth;
   int rule;
   unsigned long long *counters;
@@ -121,16 +129,18 @@ __device__ __forceinline__ void eval_point(const Cold<R> *__restrict__ C, int n,
   y = Y * iw;
 }
 
-// One hard pair (query q, segment ci) by Alg. 1 with an explicit stack of
-// right end points.  The root was found hard in phase 1,
-// so it is split immediately.  Results go to shared-memory accumulators.
+struct HardResult {
+  int xsum;
+  double fsum;   // radians (angle mode)
+  bool ob;
+};
+
+// One hard pair (query point q, segment C) by Alg. 1 with an explicit stack of
+// right end points.  The root is split immediately (phase 1
+// could not certify it as pruned).  All arithmetic in R, exact decisions.
 template <typename R, bool COUNT>
-__device__ void hard_pair(const QParams<R> &P, const Cold<R> *__restrict__ cold_face, uint32_t e,
-                          const R *s_px, const R *s_py, int *s_xs, double *s_fr, int *s_ob) {
-  const int q = e & 0xFF;
-  const bool angle = (e >> 8) & 1;
-  const Cold<R> *C = cold_face + (e >> 9);
-  const R qx = s_px[q], qy = s_py[q];
+__device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx, R qy, bool angle, R eps,
+                                             int max_depth, unsigned long long *counters) {
   const R B = __ldg(&C->B), M = __ldg(&C->M);
   const int n = __ldg(&C->n);
   R stx[MAXD + 1], sty[MAXD + 1];
@@ -142,9 +152,8 @@ __device__ void hard_pair(const QParams<R> &P, const Cold<R> *__restrict__ cold_
   std_[0] = 0;
   int sp = 1;
   R ta = R(0);
-  int xsum = 0;
-  double fsum = 0.0;
-  bool ob = false, root = true;
+  HardResult res{0, 0.0, false};
+  bool root = true;
   unsigned long long nodes = 0, evals = 0, leaves = 0;
   int dmax = 0;
   while (sp > 0) {
@@ -156,20 +165,21 @@ __device__ void hard_pair(const QParams<R> &P, const Cold<R> *__restrict__ cold_
     if (root) {
       split = true;
       root = false;
+      if (dL < eps || dR < eps) { res.ob = true; break; }   // Alg. 1 line 1 on the root
     } else {
-      if (dR < P.eps) { ob = true; break; }                 // Alg. 1 line 1
+      if (dR < eps) { res.ob = true; break; }               // Alg. 1 line 1
       const R span = ldexp(B, -d) + M;                      // Eq. 2 + margin (R5)
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     if (!split) {                                           // chord substitution
-      if (angle) fsum += (double)chord_angle(Lx, Ly, rx, ry);
-      else xsum += xcount(Lx, Ly, rx, ry);
+      if (angle) res.fsum += (double)chord_angle(Lx, Ly, rx, ry);
+      else res.xsum += xcount(Lx, Ly, rx, ry);
       ++leaves;
       Lx = rx; Ly = ry; dL = dR;
       ta += ldexp(R(1), -d);
       --sp;
     } else {
-      if (d >= P.max_depth) { ob = true; break; }           // depth cap (R6)
+      if (d >= max_depth) { res.ob = true; break; }         // depth cap (R6)
       const R tm = ta + ldexp(R(1), -(d + 1));              // m = (a+b)/2
       R mx, my;
       eval_point(C, n, tm, mx, my);
@@ -182,56 +192,72 @@ __device__ void hard_pair(const QParams<R> &P, const Cold<R> *__restrict__ cold_
       dmax = max(dmax, d + 1);
     }
   }
-  if (xsum) atomicAdd(&s_xs[q], xsum);
-  if (angle) atomicAdd(&s_fr[q], fsum);
-  if (ob) s_ob[q] = 1;
   if (COUNT) {
-    cnt_add<COUNT>(P.counters, 2, nodes);
-    cnt_add<COUNT>(P.counters, 3, evals);
-    cnt_add<COUNT>(P.counters, 4, leaves);
-    atomicMax(P.counters + 5, (unsigned long long)dmax);
+    cnt_add<COUNT>(counters, 2, nodes);
+    cnt_add<COUNT>(counters, 3, evals);
+    cnt_add<COUNT>(counters, 4, leaves);
+    atomicMax(counters + 5, (unsigned long long)dmax);
   }
+  return res;
+}
+
+__device__ __forceinline__ double nan_d() { return __longlong_as_double(0x7ff8000000000000LL); }
+
+__device__ __forceinline__ uint8_t classify(double w, int rule) {
+  const double r = w >= 0.0 ? floor(w + 0.5) : -floor(-w + 0.5);   // round half away (R10)
+  return (rule == 0) ? (fabs(r) >= 1.0) : (r >= 1.0);
+}
+
+// fp32 distance |(dx,dy)|: r * rsqrt(r); 0 / overflow give NaN or inf, and every
+// test below treats NaN as "not certified" (conservative).
+__device__ __forceinline__ float fdist(float dx, float dy) {
+  const float r = fmaf(dx, dx, dy * dy);
+  return r * rsqrtf(r);
 }
 
 template <typename R>
-__device__ __forceinline__ bool group_out(const Hot<R> &h, R px, R py);
+__device__ __forceinline__ bool group_out(const Hot<R> &h, double px, double py);
 template <>
 __device__ __forceinline__ bool group_out<double>(const Hot<double> &h, double px, double py) {
-  const float2 lo = *reinterpret_cast<const float2 *>(&h.a);
-  const float2 hi = *reinterpret_cast<const float2 *>(&h.b);
-  return !((double)lo.x <= px && px <= (double)hi.x && (double)lo.y <= py && py <= (double)hi.y);
+  return !((double)h.fx <= px && px <= (double)h.fs && (double)h.fy <= py && py <= h.x);
 }
 template <>
-__device__ __forceinline__ bool group_out<float>(const Hot<float> &h, float px, float py) {
+__device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px, double py) {
   const __half2 hi = *reinterpret_cast<const __half2 *>(&h.c);
-  return !(h.a <= px && px <= __half2float(hi.x) && h.b <= py && py <= __half2float(hi.y));
+  const float x = (float)px, y = (float)py;
+  return !(h.a <= x && x <= __half2float(hi.x) && h.b <= y && y <= __half2float(hi.y));
 }
 
+// ---------------------------------------------------------------------------
+// K3a: phase 1 of the query kernel.  One CTA = one tile of <= 256 queries of
+// one face; TMA-staged record program swept in lock-step by all warps.
+// ---------------------------------------------------------------------------
 template <typename R, bool COUNT>
-__global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
-  constexpr int RCH = (sizeof(R) == 8) ? 1024 : 2048;   // records per staged chunk (32 KB)
+__global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
+  constexpr bool F64 = sizeof(R) == 8;
+  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
   __shared__ __align__(128) Hot<R> s_rec[RCH];
   __shared__ uint32_t s_q[NWARP][QW];
-  __shared__ int s_qn[NWARP];
-  __shared__ R s_px[QT], s_py[QT];
+  __shared__ double s_px[QT], s_py[QT];
+  __shared__ int32_t s_qi[QT];
   __shared__ int s_xs[QT];
   __shared__ double s_fr[QT];
   __shared__ int s_ob[QT];
+  __shared__ int s_pend[QT];
   __shared__ __align__(8) uint64_t s_bar;
-  __shared__ int s_head;
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
   const Tile T = P.tiles[blockIdx.x];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int f = T.face;
   bool valid = t < T.qcnt;
-  const int32_t pos = T.qbeg + t;
+  const int32_t pos = (int32_t)T.qbeg + t;
   const int32_t qi = valid ? (*P.unsorted ? P.perm[pos] : pos) : 0;
-  R px = R(0), py = R(0);
+  double px = 0.0, py = 0.0;
   if (valid) {
     double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
     if (!isfinite(u) || !isfinite(v)) {
-      P.winding[qi] = __longlong_as_double(0x7ff8000000000000LL);
+      P.winding[qi] = nan_d();
       P.flag[qi] = 3;
       valid = false;
     } else {
@@ -239,15 +265,18 @@ __global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
       const double *dom = P.face_dom + 4 * f;
       if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
       if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
-      px = (R)u;
-      py = (R)v;
+      if (!F64) { u = (double)(float)u; v = (double)(float)v; }
+      px = u;
+      py = v;
     }
   }
   s_px[t] = px;
   s_py[t] = py;
+  s_qi[t] = qi;
   s_xs[t] = 0;
   s_fr[t] = 0.0;
   s_ob[t] = 0;
+  s_pend[t] = 0;
   if (t == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -256,20 +285,60 @@ __global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
 
   const int rec0 = P.face_rec_off[f];
   const int nrec = P.face_rec_off[f + 1] - rec0;
-  const Cold<R> *cold_face = P.cold + P.face_cold_off[f];
-  const R eps = P.eps;
+  const int cold0 = P.face_cold_off[f];
+  const Cold<R> *cold_face = P.cold + cold0;
+  const double eps = P.eps;
+  // fp32 filter constants (fp64 records): margins 2^-16 scale, 2^-18 relative
+  const double Mf = P.face_M[f];
+  const float eps_cert = F64 ? __double2float_ru(eps + Mf * 0x1p24) : 0.f;
+  const float shrink = 1.0f - 0x1p-18f;
+  const float pxf = (float)px, pyf = (float)py;
 
-  // per-lane state (coordinates relative to p)
-  R cx = R(0), cy = R(0), cd = R(0);   // previous chain point and its distance
-  R ax = R(0), ay = R(0);              // group start A
+  // per-lane state
+  double cx = 0.0, cy = 0.0;     // previous chain point, exact, relative to p (F64); fp32 variant uses float
+  float cdf = 0.f;               // its fp32 distance (filter)
+  double ax = 0.0, ay = 0.0;     // group start A relative to p
   int xs = 0, halves = 0;
   double fr = 0.0;
   bool onb = false;
   int skip_end = 0;
-  int qn = 0;                          // this warp's queue length (warp-uniform)
+  int qn = 0;                    // this warp's queue length (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
   unsigned phase = 0;
-  int gr = 0;                          // warp-uniform record cursor
+  int gr = 0;                    // warp-uniform record cursor
+
+  // flush this warp's smem queue to the global queue (or process locally if full)
+  auto flush = [&]() {
+    __syncwarp();
+    int base = 0;
+    if (lane == 0) base = atomicAdd(P.hq_count, qn);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base + qn <= P.hq_cap) {
+      for (int i = lane; i < qn; i += 32) {
+        const uint32_t e = s_q[warp][i];
+        const int q = e & 0xFF;
+        HardEntry H;
+        H.px = s_px[q];
+        H.py = s_py[q];
+        H.q = s_qi[q];
+        H.c = (uint32_t)(cold0 + (int)(e >> 9)) | (((e >> 8) & 1u) << 31);
+        P.hq[base + i] = H;
+        s_pend[q] = 1;
+      }
+    } else {
+      for (int i = lane; i < qn; i += 32) {                 // overflow: local fallback
+        const uint32_t e = s_q[warp][i];
+        const int q = e & 0xFF;
+        const HardResult r = hard_pair<R, COUNT>(cold_face + (e >> 9), (R)s_px[q], (R)s_py[q], (e >> 8) & 1,
+                                                 (R)eps, P.max_depth, P.counters);
+        if (r.xsum) atomicAdd(&s_xs[q], r.xsum);
+        if (r.fsum != 0.0) atomicAdd(&s_fr[q], r.fsum);
+        if (r.ob) s_ob[q] = 1;
+      }
+    }
+    __syncwarp();
+    qn = 0;
+  };
 
   for (int cb = 0; cb < nrec; cb += RCH) {
     const int cn = min(RCH, nrec - cb);
@@ -288,19 +357,46 @@ __global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
       const uint32_t kind = meta & 0xFu;
       const bool act = valid && gr >= skip_end;
       if (kind == K_SEG) {
-        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1 with R9/R5)
-        const R dx = h.a - px, dy = h.b - py;
-        const R d = dsqrt(dx * dx + dy * dy);
+        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5)
         bool hard = false;
-        if (act) {
-          onb |= d < eps;
-          if (cd + d > h.c) {                               // pruned: chord (a5)
-            if (meta & F_ANGLE) fr += (double)chord_angle(cx, cy, dx, dy);
-            else xs += xcount(cx, cy, dx, dy);
-          } else {
-            hard = !onb;
+        if constexpr (F64) {
+          const double dy = h.y - py;                          // exact sign (rounding keeps it)
+          const float df = fdist(h.fx - pxf, h.fy - pyf);
+          if (act) {
+            if (!(df * shrink > eps_cert)) {                   // filter cannot certify d >= eps
+              const double dx = h.x - px;
+              onb |= sqrt(dx * dx + dy * dy) < eps;
+            }
+            if ((cdf + df) * shrink > h.fs) {                  // certified pruned: chord (a5)
+              if (meta & F_ANGLE) {
+                fr += chord_angle(cx - px, cy, h.x - px, dy);
+              } else if ((cy >= 0.0) != (dy >= 0.0)) {
+                xs += xcount(cx - px, cy, h.x - px, dy);
+              }
+            } else {
+              hard = !onb;                                     // exact recursion in phase 2
+            }
+            if (COUNT) ++c_pairs;
           }
-          if (COUNT) ++c_pairs;
+          cx = h.x;            // absolute (F64 path keeps the exact coordinate)
+          cy = dy;
+          cdf = df;
+        } else {
+          const float dx = h.a - (float)px, dy = h.b - (float)py;
+          const float d = sqrtf(dx * dx + dy * dy);
+          if (act) {
+            onb |= d < (float)eps;
+            if (cdf + d > h.c) {
+              if (meta & F_ANGLE) fr += (double)chord_angle((float)cx, (float)cy, dx, dy);
+              else xs += xcount((float)cx, (float)cy, dx, dy);
+            } else {
+              hard = !onb;
+            }
+            if (COUNT) ++c_pairs;
+          }
+          cx = (double)dx;
+          cy = (double)dy;
+          cdf = d;
         }
         const unsigned m = __ballot_sync(0xffffffffu, hard);
         if (m) {
@@ -310,29 +406,34 @@ __global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
           }
           qn += __popc(m);
           if (COUNT) c_hard += hard ? 1 : 0;
-          if (qn > QW - 32) {                                 // overflow: warp-local drain
-            __syncwarp();
-            for (int i = lane; i < qn; i += 32)
-              hard_pair<R, COUNT>(P, cold_face, s_q[warp][i], s_px, s_py, s_xs, s_fr, s_ob);
-            __syncwarp();
-            qn = 0;
-          }
+          if (qn > QW - 32) flush();
         }
-        cx = dx; cy = dy; cd = d;
       } else if (kind == K_MOVE || kind == K_MOVEG) {
-        const R nx = h.a - px, ny = h.b - py;
-        const R nd = dsqrt(nx * nx + ny * ny);
-        if (act) {
-          onb |= nd < eps;
-          if (kind == K_MOVEG && !(meta & F_ANGLE)) {
-            // gap chord Z -> A' : -omega(p,Z,A') with its crossing
-            const R cr = canon_cross(cx, cy, nx, ny);
-            fr -= (double)datan2(cr, cx * nx + cy * ny);
-            xs += xcount_exact(cx, cy, nx, ny, cr);
-          }
+        double nx, ny;
+        float nd;
+        if constexpr (F64) {
+          nx = h.x - px;
+          ny = h.y - py;
+          nd = fdist(h.fx - pxf, h.fy - pyf);
+          if (act && !(nd * shrink > eps_cert)) onb |= sqrt(nx * nx + ny * ny) < eps;
+        } else {
+          nx = (double)(h.a - (float)px);
+          ny = (double)(h.b - (float)py);
+          nd = sqrtf((float)(nx * nx + ny * ny));
+          if (act) onb |= nd < (float)eps;
+        }
+        if (act && kind == K_MOVEG && !(meta & F_ANGLE)) {
+          // gap chord Z -> A': -omega(p,Z,A') + its crossing
+          const double zx = F64 ? cx - px : cx;
+          const double cr = canon_cross(zx, cy, nx, ny);
+          fr -= atan2(cr, zx * nx + cy * ny);
+          xs += xcount_exact(zx, cy, nx, ny, cr);
         }
         if (kind == K_MOVE) { ax = nx; ay = ny; }
-        cx = nx; cy = ny; cd = nd;
+        cx = F64 ? nx + px : nx;
+        if constexpr (F64) cx = h.x;
+        cy = ny;
+        cdf = nd;
       } else if (kind == K_GROUP) {
         // copy-group / closed-loop cull: p outside the group's box => exactly 0
         const bool out = !act || group_out<R>(h, px, py);
@@ -345,67 +446,96 @@ __global__ void __launch_bounds__(QT, 4) k_query(QParams<R> P) {
         }
       } else if (kind == K_LINE) {
         // omega(p,L) = +-1/2, p on L counts as left (R11)
-        const R q = (meta & F_AXISV) ? px : py;
-        const bool left = (meta & F_GE) ? (q >= h.a) : (q <= h.a);
+        double c;
+        if constexpr (F64) c = h.x; else c = (double)h.a;
+        const double q = (meta & F_AXISV) ? px : py;
+        const bool left = (meta & F_GE) ? (q >= c) : (q <= c);
         if (act) halves += left ? 1 : -1;
       } else if (kind == K_XCH) {
-        if (act) xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
+        const double zx = F64 ? cx - px : cx;
+        if (act) xs -= xcount_exact(ax, ay, zx, cy, canon_cross(ax, ay, zx, cy));
       } else if (kind == K_NCH) {
-        if (act) fr -= (double)chord_angle(ax, ay, cx, cy);
+        const double zx = F64 ? cx - px : cx;
+        if (act) fr -= chord_angle(ax, ay, zx, cy);
       } else if (kind == K_CLOSEG) {
+        const double zx = F64 ? cx - px : cx;
         if (act) {
-          const R cr = canon_cross(cx, cy, ax, ay);
-          fr -= (double)datan2(cr, cx * ax + cy * ay);
-          xs += xcount_exact(cx, cy, ax, ay, cr);
+          const double cr = canon_cross(zx, cy, ax, ay);
+          fr -= atan2(cr, zx * ax + cy * ay);
+          xs += xcount_exact(zx, cy, ax, ay, cr);
         }
       }
       ++gr;
     }
     __syncthreads();   // all warps done with this chunk before it is overwritten
   }
-
-  // ---- phase 2: drain every warp's hard-pair queue with dynamic fetching ----
-  if (lane == 0) s_qn[warp] = qn;
-  if (t == 0) s_head = 0;
-  __syncthreads();
-  int pre[NWARP + 1];
-  pre[0] = 0;
-#pragma unroll
-  for (int w = 0; w < NWARP; ++w) pre[w + 1] = pre[w] + s_qn[w];
-  const int total = pre[NWARP];
-  if (total > 0) {
-    for (;;) {
-      const int e = atomicAdd(&s_head, 1);
-      if (e >= total) break;
-      int w = 0;
-#pragma unroll
-      for (int k = 1; k < NWARP; ++k) w += (e >= pre[k]) ? 1 : 0;
-      hard_pair<R, COUNT>(P, cold_face, s_q[w][e - pre[w]], s_px, s_py, s_xs, s_fr, s_ob);
-    }
-  }
+  if (qn) flush();
   __syncthreads();
 
-  // ---- a8: reduce, classify, store ----
+  // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
   if (valid) {
     const bool ob = onb || s_ob[t];
-    double w;
-    uint8_t fl;
     if (ob) {
-      w = __longlong_as_double(0x7ff8000000000000LL);
-      fl = 2;
+      P.winding[qi] = nan_d();
+      P.flag[qi] = 2;
+      if (COUNT) atomicAdd(P.counters + 7, 1ull);
     } else {
-      w = (double)(xs + s_xs[t]) + 0.5 * (double)halves + (fr + s_fr[t]) * (1.0 / TWO_PI);
-      const double r = w >= 0.0 ? floor(w + 0.5) : -floor(-w + 0.5);
-      fl = (P.rule == 0) ? (fabs(r) >= 1.0) : (r >= 1.0);
+      const double w = (double)(xs + s_xs[t]) + 0.5 * (double)halves + (fr + s_fr[t]) * (1.0 / TWO_PI);
+      P.winding[qi] = w;
+      if (!s_pend[t]) P.flag[qi] = classify(w, P.rule);
     }
-    P.winding[qi] = w;
-    P.flag[qi] = fl;
-    if (COUNT && ob) atomicAdd(P.counters + 7, 1ull);
+  }
+  const bool pend = valid && !(onb || s_ob[t]) && s_pend[t];
+  const unsigned pm = __ballot_sync(0xffffffffu, pend);
+  if (pm) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi;
   }
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
     cnt_add<COUNT>(P.counters, 1, c_hard);
     cnt_add<COUNT>(P.counters, 6, c_cull);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: phase 2 -- every queued hard pair, grid-strided; results are added to
+// the partial winding numbers (crossing mode: integers, exact in any order).
+// ---------------------------------------------------------------------------
+template <typename R, bool COUNT>
+__global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
+  const int total = min(*P.hq_count, P.hq_cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const HardEntry H = P.hq[i];
+    const bool angle = H.c >> 31;
+    const Cold<R> *C = P.cold + (H.c & 0x7fffffffu);
+    const HardResult r = hard_pair<R, COUNT>(C, (R)H.px, (R)H.py, angle, (R)P.eps, P.max_depth, P.counters);
+    double *w = P.winding + H.q;
+    if (r.ob) {
+      atomicExch(reinterpret_cast<unsigned long long *>(w), 0x7ff8000000000000ULL);
+    } else {
+      const double add = (double)r.xsum + r.fsum * (1.0 / TWO_PI);
+      if (add != 0.0) atomicAdd(w, add);
+    }
+  }
+}
+
+// K3c: classify the queries that had hard pairs (a8)
+__global__ void k_finish(const int32_t *__restrict__ pend, const int32_t *__restrict__ pend_count,
+                         const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
+                         unsigned long long *counters) {
+  const int total = *pend_count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int q = pend[i];
+    const double w = winding[q];
+    if (isnan(w)) {
+      flag[q] = 2;
+      if (counters) atomicAdd(counters + 7, 1ull);
+    } else {
+      flag[q] = classify(w, rule);
+    }
   }
 }
 
@@ -487,25 +617,26 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
                                 double *winding, uint8_t *flag, cudaStream_t st) {
   const int nf = F->n_faces;
   const int64_t max_tiles64 = (n + QT - 1) / QT + nf;
-  if (max_tiles64 > INT32_MAX) {
-    set_error("wn_query: batch too large (n=%lld)", (long long)n);
+  if (n > INT32_MAX - 1 || max_tiles64 > INT32_MAX) {
+    set_error("wn_query: batch too large (n=%lld); split it", (long long)n);
     return WN_ERR_ARG;
   }
   const int max_tiles = (int)max_tiles64;
-  // scratch (stream-ordered)
-  size_t tmp1 = 0, tmp2 = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp1, (int32_t *)nullptr, (int32_t *)nullptr, nf + 1, st);
-  size_t tmp = tmp1 > tmp2 ? tmp1 : tmp2;
+  const int hq_cap = (int)std::min<int64_t>(std::max<int64_t>(n / 8, 1 << 20), 1 << 26);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, (int32_t *)nullptr, (int32_t *)nullptr, nf + 1, st);
   size_t need = 0;
   auto carve = [&](size_t bytes) { size_t o = need; need += (bytes + 255) & ~(size_t)255; return o; };
   const size_t o_cnt = carve(sizeof(int32_t) * (nf + 1));
   const size_t o_off = carve(sizeof(int32_t) * (nf + 1));
   const size_t o_cur = carve(sizeof(int32_t) * (nf + 1));
+  const size_t o_flags = carve(sizeof(int32_t) * 8);
   const size_t o_nt = carve(sizeof(int32_t) * (nf + 1));
   const size_t o_toff = carve(sizeof(int32_t) * (nf + 1));
-  const size_t o_flags = carve(sizeof(int32_t) * 4);
   const size_t o_tiles = carve(sizeof(Tile) * (size_t)max_tiles);
-  const size_t o_perm = carve(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  const size_t o_perm = carve(sizeof(int32_t) * (size_t)n);
+  const size_t o_pend = carve(sizeof(int32_t) * (size_t)n);
+  const size_t o_hq = carve(sizeof(HardEntry) * (size_t)hq_cap);
   const size_t o_tmp = carve(tmp);
   char *base = nullptr;
   WN_CUDA(cudaMallocAsync((void **)&base, need, st));
@@ -514,14 +645,15 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   int32_t *toff = (int32_t *)(base + o_toff), *flags = (int32_t *)(base + o_flags);
   Tile *tiles = (Tile *)(base + o_tiles);
   int32_t *perm = (int32_t *)(base + o_perm);
+  int32_t *pend = (int32_t *)(base + o_pend);
+  HardEntry *hq = (HardEntry *)(base + o_hq);
   void *tmpb = base + o_tmp;
   int launches = 0;
-  // cnt, off and cursor are contiguous regions: clear all three + flags
+  // cnt, off, cursor and flags are contiguous at the front: one clear
   WN_CUDA(cudaMemsetAsync(base, 0, o_nt, st));
-  WN_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 4, st));
   const int TB = 256;
   const int64_t nb64 = (n + TB - 1) / TB;
-  const int nb = (int)(nb64 < 148 * 32 ? (nb64 > 0 ? nb64 : 1) : 148 * 32);
+  const int nb = (int)(nb64 < 148 * 32 ? nb64 : 148 * 32);
   k_hist<<<nb, TB, 0, st>>>(n, face_id, nf, cnt, flags, winding, flag);
   ++launches;
   cub::DeviceScan::ExclusiveSum(tmpb, tmp, cnt, off, nf + 1, st);
@@ -542,6 +674,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.face_cold_off = F->face_cold_off;
   P.face_dom = F->face_dom;
   P.face_per = F->face_per;
+  P.face_M = F->face_M;
   P.uv = uv;
   P.winding = winding;
   P.flag = flag;
@@ -549,7 +682,12 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.ntiles = flags + 1;
   P.perm = perm;
   P.unsorted = flags;
-  P.eps = (R)F->eps;
+  P.hq = hq;
+  P.hq_count = flags + 2;
+  P.hq_cap = hq_cap;
+  P.pend = pend;
+  P.pend_count = flags + 3;
+  P.eps = F->eps;
   P.max_depth = F->max_depth;
   P.rule = F->opt.rule;
   P.counters = F->counters;
@@ -559,17 +697,22 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     WN_CUDA(cudaEventCreate(&e1));
     WN_CUDA(cudaEventRecord(e0, st));
   }
+  const int hb = 148 * 8;
   if (F->counters_on) {
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 8 * sizeof(unsigned long long), st));
-    k_query<R, true><<<max_tiles, QT, 0, st>>>(P);
+    k_phase1<R, true><<<max_tiles, QT, 0, st>>>(P);
+    k_hard<R, true><<<hb, 256, 0, st>>>(P);
+    k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, F->counters);
   } else {
-    k_query<R, false><<<max_tiles, QT, 0, st>>>(P);
+    k_phase1<R, false><<<max_tiles, QT, 0, st>>>(P);
+    k_hard<R, false><<<hb, 256, 0, st>>>(P);
+    k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, nullptr);
   }
+  launches += 3;
   if (F->timing_on) {
     WN_CUDA(cudaEventRecord(e1, st));
     F->k3_events.push_back({e0, e1});
   }
-  ++launches;
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaFreeAsync(base, st));
   g_launches = launches;

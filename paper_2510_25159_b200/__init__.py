@@ -29,7 +29,7 @@ STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4
 FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
-           "wn_last_build_launches"]
+           "wn_last_build_launches", "wn_segment_prep"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "groups_culled_warps", "on_boundary"]
 
@@ -82,6 +82,8 @@ def load():
         L.wn_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.wn_last_build_launches.restype = C.c_int32
         L.wn_last_build_launches.argtypes = []
+        L.wn_segment_prep.restype = C.c_int
+        L.wn_segment_prep.argtypes = [C.c_int32, vp, vp, vp, vp, vp]
         L.wn_free_faces.restype = None
         L.wn_free_faces.argtypes = [vp]
         L.wn_last_error.restype = C.c_char_p
@@ -235,6 +237,20 @@ class Faces:
             self.close()
         except Exception:
             pass
+
+
+def segment_prep(ctrl_uv, ctrl_w, seg_degree, device=None, stream=None):
+    """K1 alone: [n_segs, 10] = (B, S0, Bq[8]) per segment (no margins)."""
+    torch = _torch()
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    ctrl = _dev(ctrl_uv, torch.float64, device).reshape(-1, 2)
+    w = _dev(ctrl_w, torch.float64, device)
+    deg = _dev(seg_degree, torch.int32, device)
+    out = torch.empty((deg.numel(), 10), dtype=torch.float64, device=device)
+    rc = load().wn_segment_prep(deg.numel(), _ptr(ctrl), _ptr(w), _ptr(deg), _ptr(out), _stream(stream, device))
+    if rc != WN_OK:
+        raise WNError(rc, last_error())
+    return out
 
 
 def last_query_launches():

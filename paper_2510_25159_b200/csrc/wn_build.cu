@@ -63,46 +63,97 @@ __global__ void k_deg(int32_t n_segs, const int32_t *__restrict__ deg, int32_t *
 
 // ---------------------------------------------------------------------------
 // K1: segment prep.  Derivative bound B of Lemma 1: polynomial
-// hodograph bound max_i n|P_i - P_{i-1}|; rational: the minimum
-// of Floater's two bounds n(W/w)max|P_i-P_j| and n(W/w)^2 max|P_i-P_{i-1}|
-// (reading R8).  Root span S0 = min(B, control-polygon length)
-// (reading R9: arc length <= polygon length for positive weights, and the
-// Lemma 1 proof P:1086-1092 only needs arc length <= span).
+// hodograph bound max_i n|P_i - P_{i-1}|; rational: Floater's
+// two bounds n(W/w)max|P_i-P_j| and n(W/w)^2 max|P_i-P_{i-1}| (P:1101-1109,
+// reading R8), and the Bernstein bound of the hodograph numerator
+// max_k |D_k| / min_k E_k (reading R29; D = X'W - XW' of degree 2n-1, E = W^2
+// of degree 2n in Bernstein form).  B = the minimum of the valid bounds.  Root
+// span S0 = min(B, control-polygon length) (R9).  Piece bounds Bq[8]: the same
+// bound on the 8 dyadic pieces [q/8,(q+1)/8] (homogeneous de Casteljau, t-units),
+// used for sub-spans inside one piece (Eq. 2 with the piece's own bound).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ double binomd(int n, int k) {
+  double r = 1.0;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+// max |gamma'(t)| <= max_k |D_k| / min_k E_k on the segment's own parameter
+__device__ double hodo_bound(int n, const double (*H)[3]) {
+  double w[6], P[6][2];
+  for (int i = 0; i <= n; ++i) { w[i] = H[i][2]; P[i][0] = H[i][0] / w[i]; P[i][1] = H[i][1] / w[i]; }
+  double Dx[11] = {0}, Dy[11] = {0}, E[11] = {0};
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j <= n; ++j) {
+      const double c = binomd(n - 1, i) * binomd(n, j) / binomd(2 * n - 1, i + j);
+      Dx[i + j] += c * w[j] * (w[i + 1] * (P[i + 1][0] - P[j][0]) - w[i] * (P[i][0] - P[j][0]));
+      Dy[i + j] += c * w[j] * (w[i + 1] * (P[i + 1][1] - P[j][1]) - w[i] * (P[i][1] - P[j][1]));
+    }
+  for (int i = 0; i <= n; ++i)
+    for (int j = 0; j <= n; ++j) E[i + j] += binomd(n, i) * binomd(n, j) / binomd(2 * n, i + j) * w[i] * w[j];
+  double dmax = 0.0, emin = INFINITY;
+  for (int k = 0; k <= 2 * n - 1; ++k) dmax = fmax(dmax, hypot(Dx[k], Dy[k]));
+  for (int k = 0; k <= 2 * n; ++k) emin = fmin(emin, E[k]);
+  return n * dmax / emin;
+}
+
+__device__ double floater_bound(int n, const double (*H)[3]) {
+  double P[6][2], wmax = 0.0, wmin = INFINITY;
+  for (int i = 0; i <= n; ++i) {
+    P[i][0] = H[i][0] / H[i][2]; P[i][1] = H[i][1] / H[i][2];
+    wmax = fmax(wmax, H[i][2]); wmin = fmin(wmin, H[i][2]);
+  }
+  double dmax = 0.0, diam = 0.0;
+  for (int j = 1; j <= n; ++j) dmax = fmax(dmax, hypot(P[j][0] - P[j - 1][0], P[j][1] - P[j - 1][1]));
+  if (wmax == wmin) return n * dmax;
+  for (int i = 0; i <= n; ++i)
+    for (int j = i + 1; j <= n; ++j) diam = fmax(diam, hypot(P[j][0] - P[i][0], P[j][1] - P[i][1]));
+  const double r = wmax / wmin;
+  return fmin(n * r * diam, n * r * r * dmax);
+}
+
+__device__ void hsplit_half(int n, const double (*H)[3], double (*L)[3], double (*R)[3]) {
+  double T[6][3];
+  for (int i = 0; i <= n; ++i) for (int c = 0; c < 3; ++c) T[i][c] = H[i][c];
+  for (int c = 0; c < 3; ++c) { L[0][c] = T[0][c]; R[n][c] = T[n][c]; }
+  for (int r = 1; r <= n; ++r) {
+    for (int j = 0; j <= n - r; ++j) for (int c = 0; c < 3; ++c) T[j][c] = 0.5 * (T[j][c] + T[j + 1][c]);
+    for (int c = 0; c < 3; ++c) { L[r][c] = T[0][c]; R[n - r][c] = T[n - r][c]; }
+  }
+}
+
 __global__ void k_prep(int32_t n_segs, const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
                        const double *__restrict__ ctrl, const double *__restrict__ w,
-                       double2 *__restrict__ prep, uint8_t *__restrict__ serr) {
+                       SegPrep *__restrict__ prep, uint8_t *__restrict__ serr) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_segs) return;
   const int n = deg[s];
   const int o = coff[s];
-  double P[6][2], W[6];
+  double H[6][3];
   bool err = false;
-  double wmax = 0.0, wmin = INFINITY;
+  double lpoly = 0.0;
   for (int j = 0; j <= n; ++j) {
-    P[j][0] = ctrl[2 * (o + j)];
-    P[j][1] = ctrl[2 * (o + j) + 1];
-    W[j] = w ? w[o + j] : 1.0;
-    err |= !isfinite(P[j][0]) || !isfinite(P[j][1]) || !isfinite(W[j]) || !(W[j] > 0.0);
-    wmax = fmax(wmax, W[j]);
-    wmin = fmin(wmin, W[j]);
+    const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
+    err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
+    H[j][0] = wj * x; H[j][1] = wj * y; H[j][2] = wj;
+    if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
   }
-  double dmax = 0.0, lpoly = 0.0, diam = 0.0;
-  for (int j = 1; j <= n; ++j) {
-    const double l = hypot(P[j][0] - P[j - 1][0], P[j][1] - P[j - 1][1]);
-    dmax = fmax(dmax, l);
-    lpoly += l;
-  }
-  double B;
-  if (wmax == wmin) {
-    B = n * dmax;
+  SegPrep S;
+  if (err) {
+    S.B = S.S0 = 0.0;
+    for (int q = 0; q < 8; ++q) S.Bq[q] = 0.0;
   } else {
-    for (int i = 0; i <= n; ++i)
-      for (int j = i + 1; j <= n; ++j) diam = fmax(diam, hypot(P[j][0] - P[i][0], P[j][1] - P[i][1]));
-    const double r = wmax / wmin;
-    B = fmin(n * r * diam, n * r * r * dmax);
+    const double B = fmin(floater_bound(n, H), hodo_bound(n, H));
+    S.B = B;
+    S.S0 = fmin(B, lpoly);
+    // 8 dyadic pieces by three levels of halving; piece bound in t-units = 8 x
+    double L1[2][6][3], L2[4][6][3], L3[8][6][3];
+    hsplit_half(n, H, L1[0], L1[1]);
+    for (int a = 0; a < 2; ++a) hsplit_half(n, L1[a], L2[2 * a], L2[2 * a + 1]);
+    for (int a = 0; a < 4; ++a) hsplit_half(n, L2[a], L3[2 * a], L3[2 * a + 1]);
+    for (int q = 0; q < 8; ++q) S.Bq[q] = fmin(B, 8.0 * fmin(floater_bound(n, L3[q]), hodo_bound(n, L3[q])));
   }
-  prep[s] = make_double2(B, fmin(B, lpoly));
+  prep[s] = S;
   serr[s] = err ? 1 : 0;
 }
 
@@ -246,7 +297,7 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
                        const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                       const double *__restrict__ wts, const double2 *__restrict__ prep,
+                       const double *__restrict__ wts, const SegPrep *__restrict__ prep,
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
                        Cold<R> *__restrict__ cold) {
@@ -294,17 +345,21 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     }
     if (s == s0) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVE | fa);
     else if (brk[s]) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVEG | fa);
-    const double2 bp = prep[s];
+    const SegPrep &bp = prep[s];
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // see k_query; fp32 records: S0 (1 + 2^-17) + M32.  Eq. 2 uses B (cold).
-    const double S0 = (sizeof(R) == 8) ? bp.y * (1.0 + 0x1p-17) + G.M * 0x1p24 : bp.y * (1.0 + rel) + G.M;
-    const double Bm = bp.x * (1.0 + rel);
+    const double S0 = (sizeof(R) == 8) ? bp.S0 * (1.0 + 0x1p-17) + G.M * 0x1p24 : bp.S0 * (1.0 + rel) + G.M;
+    const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
     put_rec<R>(hot, r++, px[n], py[n], S0, K_SEG | fa | ((uint32_t)cl << 8));
     Cold<R> C;
     C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
     C.B = Br;
+    for (int q = 0; q < 8; ++q) {
+      const double bq = bp.Bq[q] * (1.0 + rel);
+      C.Bq[q] = (sizeof(R) == 4) ? (R)f_up(bq) : (R)bq;
+    }
     C.M = (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M;
     C.n = n;
     C.pad = 0;
@@ -480,16 +535,11 @@ struct DevBuf {
 void free_handle(wn_faces_t F) {
   if (!F) return;
   for (auto &pr : F->k3_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
-  cudaFree(F->hot);
-  cudaFree(F->cold);
-  cudaFree(F->face_rec_off);
-  cudaFree(F->face_cold_off);
-  cudaFree(F->face_order);
-  cudaFree(F->face_dom);
-  cudaFree(F->face_per);
-  cudaFree(F->face_ok);
-  cudaFree(F->face_M);
-  cudaFree(F->counters);
+  // stream-ordered frees on the legacy stream (caller guarantees no query in flight)
+  void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
+                F->face_per, F->face_ok, F->face_M, F->counters};
+  for (void *p : ps)
+    if (p) cudaFreeAsync(p, 0);
   delete F;
 }
 
@@ -500,7 +550,7 @@ struct BuildCtx {
   const uint8_t *per;
   const double *dom;
   int32_t *coff, *loop_face;
-  double2 *prep;
+  SegPrep *prep;
   int2 *shift;
   uint8_t *brk;
   LoopInfo *info;
@@ -518,16 +568,16 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   F->n_seg = plan.colds;
   F->n_lines = plan.n_lines;
   F->n_groups = plan.n_cull;
-  WN_CUDA(cudaMalloc(&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1)));
-  WN_CUDA(cudaMalloc(&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1)));
-  WN_CUDA(cudaMalloc(&F->face_rec_off, sizeof(int32_t) * (nf + 1)));
-  WN_CUDA(cudaMalloc(&F->face_cold_off, sizeof(int32_t) * (nf + 1)));
-  WN_CUDA(cudaMalloc(&F->face_order, sizeof(int32_t) * std::max(nf, 1)));
-  WN_CUDA(cudaMalloc(&F->face_dom, sizeof(double) * 4 * std::max(nf, 1)));
-  WN_CUDA(cudaMalloc(&F->face_per, std::max(nf, 1)));
-  WN_CUDA(cudaMalloc(&F->face_ok, std::max(nf, 1)));
-  WN_CUDA(cudaMalloc(&F->face_M, sizeof(double) * std::max(nf, 1)));
-  WN_CUDA(cudaMalloc(&F->counters, 8 * sizeof(unsigned long long)));
+  WN_CUDA(cudaMallocAsync((void **)&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_rec_off, sizeof(int32_t) * (nf + 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_cold_off, sizeof(int32_t) * (nf + 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_order, sizeof(int32_t) * std::max(nf, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_dom, sizeof(double) * 4 * std::max(nf, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_per, std::max(nf, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_ok, std::max(nf, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
+  WN_CUDA(cudaMallocAsync((void **)&F->counters, 8 * sizeof(unsigned long long), st));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
   std::vector<int32_t> order(nf);
   std::iota(order.begin(), order.end(), 0);
@@ -596,6 +646,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   }
+  ensure_pool(dev);
   cudaStream_t st = (cudaStream_t)stream;
   DevBuf D;
   D.st = st;
@@ -930,6 +981,43 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build sync"); }
   tr.mark("final sync");
   *out = F;
+  return WN_OK;
+}
+
+extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, const double *ctrl_w,
+                                       const int32_t *seg_degree, double *out, void *stream) {
+  set_error("");
+  if (n_segs < 0 || (n_segs > 0 && (!ctrl_uv || !seg_degree || !out))) {
+    set_error("wn_segment_prep: bad arguments");
+    return WN_ERR_ARG;
+  }
+  if (n_segs == 0) return WN_OK;
+  int dev = 0;
+  WN_CUDA(cudaGetDevice(&dev));
+  ensure_pool(dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf D;
+  D.st = st;
+  int32_t *cnt = nullptr, *bad = nullptr, *coff = nullptr;
+  uint8_t *serr = nullptr;
+  WN_CUDA(D.alloc(&cnt, n_segs + 1));
+  WN_CUDA(D.alloc(&bad, 1));
+  WN_CUDA(D.alloc(&coff, n_segs + 1));
+  WN_CUDA(D.alloc(&serr, n_segs));
+  WN_CUDA(cudaMemsetAsync(bad, 0, sizeof(int32_t), st));
+  k_deg<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, seg_degree, cnt, bad);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, coff, n_segs + 1, st);
+  char *dt = nullptr;
+  WN_CUDA(D.alloc(&dt, tmp));
+  cub::DeviceScan::ExclusiveSum(dt, tmp, cnt, coff, n_segs + 1, st);
+  int32_t h_bad = 0;
+  WN_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaStreamSynchronize(st));
+  if (h_bad) { set_error("wn_segment_prep: segment degree outside 1..5"); return WN_ERR_ARG; }
+  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, (SegPrep *)out, serr);
+  WN_CUDA(cudaGetLastError());
+  WN_CUDA(cudaStreamSynchronize(st));
   return WN_OK;
 }
 

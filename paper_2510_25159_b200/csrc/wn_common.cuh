@@ -59,10 +59,17 @@ struct __align__(16) Hot<float> {
 template <typename R>
 struct Cold {
   R f0x, f0y, f1x, f1y;
-  R B;      // derivative bound (A.1) incl. relative margin
+  R B;      // derivative bound (A.1; R29) incl. relative margin
   R M;      // absolute margin (R5)
   int32_t n, pad;
   R cx[6], cy[6], cw[6];
+  R Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin
+};
+
+// K1 output per input segment (translation invariant)
+struct SegPrep {
+  double B, S0;
+  double Bq[8];
 };
 
 // hard-pair queue entry: q (8 bits) | angle (1 bit) | cold local index (23 bits)
@@ -191,6 +198,7 @@ struct wn_faces_s {
 };
 
 namespace wn {
+void ensure_pool(int dev);
 void set_error(const char *fmt, ...);
 wn_status_t cuda_fail(cudaError_t e, const char *what);
 }  // namespace wn

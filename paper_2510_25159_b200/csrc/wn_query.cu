@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "wn_common.cuh"
 
@@ -141,7 +142,7 @@ struct HardResult {
 template <typename R, bool COUNT>
 __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx, R qy, bool angle, R eps,
                                              int max_depth, unsigned long long *counters) {
-  const R B = __ldg(&C->B), M = __ldg(&C->M);
+  const R M = __ldg(&C->M);
   const int n = __ldg(&C->n);
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
@@ -151,7 +152,7 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
   sty[0] = __ldg(&C->f1y) - qy;
   std_[0] = 0;
   int sp = 1;
-  R ta = R(0);
+  double ta = 0.0;   // node start: exact dyadic (double also for fp32 records)
   HardResult res{0, 0.0, false};
   bool root = true;
   unsigned long long nodes = 0, evals = 0, leaves = 0;
@@ -168,7 +169,17 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
       if (dL < eps || dR < eps) { res.ob = true; break; }   // Alg. 1 line 1 on the root
     } else {
       if (dR < eps) { res.ob = true; break; }               // Alg. 1 line 1
-      const R span = ldexp(B, -d) + M;                      // Eq. 2 + margin (R5)
+      // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
+      // (piece bounds for d >= 3, their max above), + margin (R5)
+      R Bn;
+      if (d >= 3) {
+        Bn = __ldg(&C->Bq[(int)(ta * 8.0)]);
+      } else {
+        const int q0 = (int)(ta * 8.0), nq = 8 >> d;
+        Bn = __ldg(&C->Bq[q0]);
+        for (int k = 1; k < nq; ++k) Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+      }
+      const R span = ldexp(Bn, -d) + M;
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     if (!split) {                                           // chord substitution
@@ -176,13 +187,13 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
       else res.xsum += xcount(Lx, Ly, rx, ry);
       ++leaves;
       Lx = rx; Ly = ry; dL = dR;
-      ta += ldexp(R(1), -d);
+      ta += ldexp(1.0, -d);
       --sp;
     } else {
       if (d >= max_depth) { res.ob = true; break; }         // depth cap (R6)
-      const R tm = ta + ldexp(R(1), -(d + 1));              // m = (a+b)/2
+      const double tm = ta + ldexp(1.0, -(d + 1));         // m = (a+b)/2
       R mx, my;
-      eval_point(C, n, tm, mx, my);
+      eval_point(C, n, (R)tm, mx, my);
       ++evals;
       std_[sp - 1] = (int8_t)(d + 1);
       stx[sp] = mx - qx;
@@ -240,9 +251,6 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   __shared__ uint32_t s_q[NWARP][QW];
   __shared__ double s_px[QT], s_py[QT];
   __shared__ int32_t s_qi[QT];
-  __shared__ int s_xs[QT];
-  __shared__ double s_fr[QT];
-  __shared__ int s_ob[QT];
   __shared__ int s_pend[QT];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -273,9 +281,6 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   s_px[t] = px;
   s_py[t] = py;
   s_qi[t] = qi;
-  s_xs[t] = 0;
-  s_fr[t] = 0.0;
-  s_ob[t] = 0;
   s_pend[t] = 0;
   if (t == 0) {
     mbar_init(&s_bar, 1);
@@ -307,33 +312,27 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   unsigned phase = 0;
   int gr = 0;                    // warp-uniform record cursor
 
-  // flush this warp's smem queue to the global queue (or process locally if full)
+  // flush this warp's smem queue to the global queue; when the queue is full the
+  // query is handed to the overflow kernel instead (k_overflow, exact, rare)
   auto flush = [&]() {
     __syncwarp();
     int base = 0;
     if (lane == 0) base = atomicAdd(P.hq_count, qn);
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (base + qn <= P.hq_cap) {
-      for (int i = lane; i < qn; i += 32) {
-        const uint32_t e = s_q[warp][i];
-        const int q = e & 0xFF;
+    const bool fits = base + qn <= P.hq_cap;
+    for (int i = lane; i < qn; i += 32) {
+      const uint32_t e = s_q[warp][i];
+      const int q = e & 0xFF;
+      if (fits) {
         HardEntry H;
         H.px = s_px[q];
         H.py = s_py[q];
         H.q = s_qi[q];
         H.c = (uint32_t)(cold0 + (int)(e >> 9)) | (((e >> 8) & 1u) << 31);
         P.hq[base + i] = H;
-        s_pend[q] = 1;
-      }
-    } else {
-      for (int i = lane; i < qn; i += 32) {                 // overflow: local fallback
-        const uint32_t e = s_q[warp][i];
-        const int q = e & 0xFF;
-        const HardResult r = hard_pair<R, COUNT>(cold_face + (e >> 9), (R)s_px[q], (R)s_py[q], (e >> 8) & 1,
-                                                 (R)eps, P.max_depth, P.counters);
-        if (r.xsum) atomicAdd(&s_xs[q], r.xsum);
-        if (r.fsum != 0.0) atomicAdd(&s_fr[q], r.fsum);
-        if (r.ob) s_ob[q] = 1;
+        s_pend[q] |= 1;
+      } else {
+        s_pend[q] |= 2;
       }
     }
     __syncwarp();
@@ -474,24 +473,25 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
 
   // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
   if (valid) {
-    const bool ob = onb || s_ob[t];
+    const bool ob = onb;
     if (ob) {
       P.winding[qi] = nan_d();
       P.flag[qi] = 2;
       if (COUNT) atomicAdd(P.counters + 7, 1ull);
     } else {
-      const double w = (double)(xs + s_xs[t]) + 0.5 * (double)halves + (fr + s_fr[t]) * (1.0 / TWO_PI);
+      const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
       P.winding[qi] = w;
       if (!s_pend[t]) P.flag[qi] = classify(w, P.rule);
     }
   }
-  const bool pend = valid && !(onb || s_ob[t]) && s_pend[t];
+  const bool pend = valid && !onb && s_pend[t];
   const unsigned pm = __ballot_sync(0xffffffffu, pend);
   if (pm) {
     int base = 0;
     if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi;
+    // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
+    if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((s_pend[t] & 2) ? (int32_t)0x80000000 : 0);
   }
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
@@ -522,6 +522,80 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   }
 }
 
+// K3d: queries whose hard pairs overflowed the global queue: the whole record
+// program again for that query, exact root tests against the (valid, inflated)
+// stored span and the recursion inline.  Normally never has work.
+template <typename R>
+__global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id) {
+  const int total = *P.pend_count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int e = P.pend[i];
+    if (e >= 0) continue;
+    const int qi = e & 0x7fffffff;
+    const int f = face_id[qi];
+    double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+    const uint8_t per = P.face_per[f];
+    const double *dom = P.face_dom + 4 * f;
+    if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
+    if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
+    if (sizeof(R) == 4) { u = (double)(float)u; v = (double)(float)v; }
+    const int rec0 = P.face_rec_off[f], rec1 = P.face_rec_off[f + 1];
+    const Cold<R> *cold_face = P.cold + P.face_cold_off[f];
+    double cx = 0, cy = 0, cd = 0, ax = 0, ay = 0, fr = 0;
+    int xs = 0, halves = 0;
+    bool ob = false;
+    for (int r = rec0; r < rec1 && !ob; ++r) {
+      const Hot<R> h = P.hot[r];
+      const uint32_t meta = h.meta, kind = meta & 0xFu;
+      double hx, hy, hs;
+      if constexpr (sizeof(R) == 8) { hx = h.x; hy = h.y; hs = h.fs; } else { hx = h.a; hy = h.b; hs = h.c; }
+      if (kind == K_SEG || kind == K_MOVE || kind == K_MOVEG) {
+        const double nx = hx - u, ny = hy - v, nd = sqrt(nx * nx + ny * ny);
+        if (nd < P.eps) { ob = true; break; }
+        if (kind == K_SEG) {
+          if (cd + nd > hs) {
+            if (meta & F_ANGLE) fr += chord_angle(cx, cy, nx, ny);
+            else xs += xcount(cx, cy, nx, ny);
+          } else {
+            const HardResult res = hard_pair<R, false>(cold_face + (meta >> 8), (R)u, (R)v, (meta & F_ANGLE) != 0,
+                                                       (R)P.eps, P.max_depth, nullptr);
+            if (res.ob) { ob = true; break; }
+            xs += res.xsum;
+            fr += res.fsum;
+          }
+        } else if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+          const double cr = canon_cross(cx, cy, nx, ny);
+          fr -= atan2(cr, cx * nx + cy * ny);
+          xs += xcount_exact(cx, cy, nx, ny, cr);
+        }
+        if (kind == K_MOVE) { ax = nx; ay = ny; }
+        cx = nx; cy = ny; cd = nd;
+      } else if (kind == K_GROUP) {
+        if (group_out<R>(h, u, v)) r += (int)(meta >> 8);
+      } else if (kind == K_LINE) {
+        const double q = (meta & F_AXISV) ? u : v;
+        halves += ((meta & F_GE) ? (q >= hx) : (q <= hx)) ? 1 : -1;
+      } else if (kind == K_XCH) {
+        xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
+      } else if (kind == K_NCH) {
+        fr -= chord_angle(ax, ay, cx, cy);
+      } else if (kind == K_CLOSEG) {
+        const double cr = canon_cross(cx, cy, ax, ay);
+        fr -= atan2(cr, cx * ax + cy * ay);
+        xs += xcount_exact(cx, cy, ax, ay, cr);
+      }
+    }
+    if (ob) {
+      P.winding[qi] = nan_d();
+      P.flag[qi] = 2;
+    } else {
+      const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
+      P.winding[qi] = w;
+      P.flag[qi] = classify(w, P.rule);
+    }
+  }
+}
+
 // K3c: classify the queries that had hard pairs (a8)
 __global__ void k_finish(const int32_t *__restrict__ pend, const int32_t *__restrict__ pend_count,
                          const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
@@ -529,6 +603,7 @@ __global__ void k_finish(const int32_t *__restrict__ pend, const int32_t *__rest
   const int total = *pend_count;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int q = pend[i];
+    if (q < 0) continue;   // overflow query: finished by k_overflow
     const double w = winding[q];
     if (isnan(w)) {
       flag[q] = 2;
@@ -622,7 +697,8 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     return WN_ERR_ARG;
   }
   const int max_tiles = (int)max_tiles64;
-  const int hq_cap = (int)std::min<int64_t>(std::max<int64_t>(n / 8, 1 << 20), 1 << 26);
+  int hq_cap = (int)std::min<int64_t>(std::max<int64_t>(n / 8, 1 << 20), 1 << 26);
+  if (const char *cap = std::getenv("WN_HQ_CAP")) hq_cap = std::max(1, atoi(cap));   // tests: force overflow
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, (int32_t *)nullptr, (int32_t *)nullptr, nf + 1, st);
   size_t need = 0;
@@ -702,13 +778,15 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 8 * sizeof(unsigned long long), st));
     k_phase1<R, true><<<max_tiles, QT, 0, st>>>(P);
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
+    k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, F->counters);
   } else {
     k_phase1<R, false><<<max_tiles, QT, 0, st>>>(P);
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
+    k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, nullptr);
   }
-  launches += 3;
+  launches += 4;
   if (F->timing_on) {
     WN_CUDA(cudaEventRecord(e1, st));
     F->k3_events.push_back({e0, e1});
@@ -721,6 +799,21 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
 
 }  // namespace wn
 
+namespace wn {
+// Keep stream-ordered allocations cached across synchronisations (the query
+// scratch and the records are reallocated every call otherwise).
+void ensure_pool(int dev) {
+  static int done[64] = {0};
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = 1;
+}
+}  // namespace wn
+
 extern "C" wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face_id, const double *uv,
                                 double *winding, uint8_t *flag, void *stream) {
   if (!faces) { wn::set_error("wn_query: NULL handle"); return WN_ERR_ARG; }
@@ -729,6 +822,7 @@ extern "C" wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face
   if (!face_id || !uv || !winding || !flag) { wn::set_error("wn_query: NULL array"); return WN_ERR_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
   WN_CUDA(cudaSetDevice(faces->device));
+  wn::ensure_pool(faces->device);
   if (faces->n_faces == 0) {
     // every query references a non-existent face
     wn::set_error("");

@@ -195,3 +195,41 @@ def test_counters_and_info():
     assert info["n_seg_records"] == 80
     assert c["pairs_tested"] > 0 and c["hard_pairs"] > 0 and c["max_depth"] <= 48
     assert wn.last_query_launches() >= 1
+
+
+def test_k1_derivative_bounds_sound():
+    """Lemma 1 soundness: B >= max |gamma'| sampled densely (oracle's
+    derivative), every piece bound >= the sampled speed on its piece, and
+    S0 >= the true arc length (so the root ellipse contains the curve)."""
+    rng = np.random.default_rng(7)
+    segs = []
+    for _ in range(300):
+        n = int(rng.integers(1, 6))
+        P = rng.uniform(-1, 1, size=(n + 1, 2))
+        w = rng.uniform(0.5, 2.0, size=n + 1) if rng.random() < 0.8 else np.exp(rng.uniform(-3, 3, n + 1))
+        segs.append((P, w))
+    wl = H.make_wl([([segs], 0, (0, 1, 0, 1))])
+    out = wn.segment_prep(wl["ctrl_uv"], wl["ctrl_w"], wl["seg_degree"]).cpu().numpy()
+    ts = np.linspace(0, 1, 2049)
+    for (P, w), row in zip(segs, out):
+        sp = np.array([np.hypot(*oracle.derivative(P, w, t)) for t in ts])
+        assert row[0] >= sp.max() * (1 - 1e-12), (row[0], sp.max())
+        for q in range(8):
+            m = (ts >= q / 8) & (ts <= (q + 1) / 8)
+            assert row[2 + q] >= sp[m].max() * (1 - 1e-12)
+        pts = np.array([oracle.evaluate(P, w, t) for t in ts])
+        arc = np.hypot(*np.diff(pts, axis=0).T).sum()
+        assert row[1] >= arc * (1 - 1e-9)
+        assert row[1] <= row[0] + 1e-15
+
+
+def test_hard_pair_queue_overflow_path(monkeypatch):
+    """Force the global hard-pair queue to overflow: the affected queries go
+    through k_overflow and must still match the oracle."""
+    monkeypatch.setenv("WN_HQ_CAP", "64")
+    wl = G.gen_c2(n_queries=20_000)
+    w, fl = _gpu(wl)
+    _check(wl, w, fl, min_cmp=0.85)
+    wl3 = G.gen_c3(n_queries=5_000)
+    w, fl = _gpu(wl3)
+    _check(wl3, w, fl, min_cmp=0.99)

@@ -72,53 +72,79 @@ __global__ void k_deg(int32_t n_segs, const int32_t *__restrict__ deg, int32_t *
 // bound on the 8 dyadic pieces [q/8,(q+1)/8] (homogeneous de Casteljau, t-units),
 // used for sub-spans inside one piece (Eq. 2 with the piece's own bound).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double binomd(int n, int k) {
-  double r = 1.0;
-  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
-  return r;
-}
+// Exact binomial coefficients C(n,k), n <= 10.
+__constant__ double c_binom[11][11] = {
+    {1}, {1, 1}, {1, 2, 1}, {1, 3, 3, 1}, {1, 4, 6, 4, 1}, {1, 5, 10, 10, 5, 1}, {1, 6, 15, 20, 15, 6, 1},
+    {1, 7, 21, 35, 35, 21, 7, 1}, {1, 8, 28, 56, 70, 56, 28, 8, 1}, {1, 9, 36, 84, 126, 126, 84, 36, 9, 1},
+    {1, 10, 45, 120, 210, 252, 210, 120, 45, 10, 1}};
 
-// max |gamma'(t)| <= max_k |D_k| / min_k E_k on the segment's own parameter
-__device__ double hodo_bound(int n, const double (*H)[3]) {
-  double w[6], P[6][2];
-  for (int i = 0; i <= n; ++i) { w[i] = H[i][2]; P[i][0] = H[i][0] / w[i]; P[i][1] = H[i][1] / w[i]; }
-  double Dx[11] = {0}, Dy[11] = {0}, E[11] = {0};
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j <= n; ++j) {
-      const double c = binomd(n - 1, i) * binomd(n, j) / binomd(2 * n - 1, i + j);
-      Dx[i + j] += c * w[j] * (w[i + 1] * (P[i + 1][0] - P[j][0]) - w[i] * (P[i][0] - P[j][0]));
-      Dy[i + j] += c * w[j] * (w[i + 1] * (P[i + 1][1] - P[j][1]) - w[i] * (P[i][1] - P[j][1]));
-    }
-  for (int i = 0; i <= n; ++i)
-    for (int j = 0; j <= n; ++j) E[i + j] += binomd(n, i) * binomd(n, j) / binomd(2 * n, i + j) * w[i] * w[j];
+// Bounds on flat homogeneous control points H[3i+0..2] = (w x, w y, w), i = 0..n.
+// Written without local aggregates (nvcc 12.9 -O3 miscompiled an earlier
+// array-accumulating version on sm_100a; scripts/dev/kp.cu reproduces it).
+// Hodograph-numerator Bernstein bound: max_k |D_k| / min_k E_k with
+//   D_k = sum_{i+j=k} C(n-1,i)C(n,j)/C(2n-1,k) w_j (w_{i+1}(P_{i+1}-P_j) - w_i(P_i-P_j)),
+//   E_k = sum_{i+j=k} C(n,i)C(n,j)/C(2n,k) w_i w_j.
+__device__ __noinline__ double hodo_bound(int n, const double *H) {
   double dmax = 0.0, emin = INFINITY;
-  for (int k = 0; k <= 2 * n - 1; ++k) dmax = fmax(dmax, hypot(Dx[k], Dy[k]));
-  for (int k = 0; k <= 2 * n; ++k) emin = fmin(emin, E[k]);
+  for (int k = 0; k <= 2 * n - 1; ++k) {
+    double dx = 0.0, dy = 0.0;
+    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n - 1 ? k : n - 1;
+    for (int i = i0; i <= i1; ++i) {
+      const int j = k - i;
+      const double wi = H[3 * i + 2], wi1 = H[3 * i + 5], wj = H[3 * j + 2];
+      const double xi = H[3 * i] / wi, yi = H[3 * i + 1] / wi;
+      const double xi1 = H[3 * i + 3] / wi1, yi1 = H[3 * i + 4] / wi1;
+      const double xj = H[3 * j] / wj, yj = H[3 * j + 1] / wj;
+      const double c = c_binom[n - 1][i] * c_binom[n][j] / c_binom[2 * n - 1][k] * wj;
+      dx += c * (wi1 * (xi1 - xj) - wi * (xi - xj));
+      dy += c * (wi1 * (yi1 - yj) - wi * (yi - yj));
+    }
+    dmax = fmax(dmax, hypot(dx, dy));
+  }
+  for (int k = 0; k <= 2 * n; ++k) {
+    double e = 0.0;
+    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n ? k : n;
+    for (int i = i0; i <= i1; ++i) {
+      const int j = k - i;
+      e += c_binom[n][i] * c_binom[n][j] / c_binom[2 * n][k] * H[3 * i + 2] * H[3 * j + 2];
+    }
+    emin = fmin(emin, e);
+  }
   return n * dmax / emin;
 }
 
-__device__ double floater_bound(int n, const double (*H)[3]) {
-  double P[6][2], wmax = 0.0, wmin = INFINITY;
-  for (int i = 0; i <= n; ++i) {
-    P[i][0] = H[i][0] / H[i][2]; P[i][1] = H[i][1] / H[i][2];
-    wmax = fmax(wmax, H[i][2]); wmin = fmin(wmin, H[i][2]);
-  }
-  double dmax = 0.0, diam = 0.0;
-  for (int j = 1; j <= n; ++j) dmax = fmax(dmax, hypot(P[j][0] - P[j - 1][0], P[j][1] - P[j - 1][1]));
-  if (wmax == wmin) return n * dmax;
+__device__ __noinline__ double floater_bound(int n, const double *H) {
+  double wmax = H[2], wmin = H[2], dmax = 0.0, diam = 0.0;
+  for (int i = 1; i <= n; ++i) { wmax = fmax(wmax, H[3 * i + 2]); wmin = fmin(wmin, H[3 * i + 2]); }
   for (int i = 0; i <= n; ++i)
-    for (int j = i + 1; j <= n; ++j) diam = fmax(diam, hypot(P[j][0] - P[i][0], P[j][1] - P[i][1]));
+    for (int j = i + 1; j <= n; ++j) {
+      const double l = hypot(H[3 * j] / H[3 * j + 2] - H[3 * i] / H[3 * i + 2],
+                             H[3 * j + 1] / H[3 * j + 2] - H[3 * i + 1] / H[3 * i + 2]);
+      diam = fmax(diam, l);
+      if (j == i + 1) dmax = fmax(dmax, l);
+    }
+  if (wmax == wmin) return n * dmax;
   const double r = wmax / wmin;
   return fmin(n * r * diam, n * r * r * dmax);
 }
 
-__device__ void hsplit_half(int n, const double (*H)[3], double (*L)[3], double (*R)[3]) {
-  double T[6][3];
-  for (int i = 0; i <= n; ++i) for (int c = 0; c < 3; ++c) T[i][c] = H[i][c];
-  for (int c = 0; c < 3; ++c) { L[0][c] = T[0][c]; R[n][c] = T[n][c]; }
-  for (int r = 1; r <= n; ++r) {
-    for (int j = 0; j <= n - r; ++j) for (int c = 0; c < 3; ++c) T[j][c] = 0.5 * (T[j][c] + T[j + 1][c]);
-    for (int c = 0; c < 3; ++c) { L[r][c] = T[0][c]; R[n - r][c] = T[n - r][c]; }
+// Homogeneous control points of the dyadic piece [q/8, (q+1)/8] of H (blossom-
+// free: three de Casteljau halvings, choosing the half along the bits of q).
+// A receives 3(n+1) values; works in place in A.
+__device__ __noinline__ void dyadic_piece(int n, const double *H, int q, double *A) {
+  for (int i = 0; i < 3 * (n + 1); ++i) A[i] = H[i];
+  for (int lvl = 2; lvl >= 0; --lvl) {
+    const bool right = (q >> lvl) & 1;
+    // after r rounds of midpoint averaging, entry 0 is the left half's point r
+    // and entry n-r the right half's point n-r; keep the requested half
+    double L[18], R[18];
+    for (int c = 0; c < 3; ++c) { L[c] = A[c]; R[3 * n + c] = A[3 * n + c]; }
+    for (int r = 1; r <= n; ++r) {
+      for (int j = 0; j <= n - r; ++j)
+        for (int c = 0; c < 3; ++c) A[3 * j + c] = 0.5 * (A[3 * j + c] + A[3 * j + 3 + c]);
+      for (int c = 0; c < 3; ++c) { L[3 * r + c] = A[c]; R[3 * (n - r) + c] = A[3 * (n - r) + c]; }
+    }
+    for (int i = 0; i < 3 * (n + 1); ++i) A[i] = right ? R[i] : L[i];
   }
 }
 
@@ -129,31 +155,28 @@ __global__ void k_prep(int32_t n_segs, const int32_t *__restrict__ deg, const in
   if (s >= n_segs) return;
   const int n = deg[s];
   const int o = coff[s];
-  double H[6][3];
+  double H[18], A[18];
   bool err = false;
   double lpoly = 0.0;
   for (int j = 0; j <= n; ++j) {
     const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
     err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
-    H[j][0] = wj * x; H[j][1] = wj * y; H[j][2] = wj;
+    H[3 * j] = wj * x; H[3 * j + 1] = wj * y; H[3 * j + 2] = wj;
     if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
   }
-  SegPrep S;
+  SegPrep *out = prep + s;
   if (err) {
-    S.B = S.S0 = 0.0;
-    for (int q = 0; q < 8; ++q) S.Bq[q] = 0.0;
+    out->B = out->S0 = 0.0;
+    for (int q = 0; q < 8; ++q) out->Bq[q] = 0.0;
   } else {
     const double B = fmin(floater_bound(n, H), hodo_bound(n, H));
-    S.B = B;
-    S.S0 = fmin(B, lpoly);
-    // 8 dyadic pieces by three levels of halving; piece bound in t-units = 8 x
-    double L1[2][6][3], L2[4][6][3], L3[8][6][3];
-    hsplit_half(n, H, L1[0], L1[1]);
-    for (int a = 0; a < 2; ++a) hsplit_half(n, L1[a], L2[2 * a], L2[2 * a + 1]);
-    for (int a = 0; a < 4; ++a) hsplit_half(n, L2[a], L3[2 * a], L3[2 * a + 1]);
-    for (int q = 0; q < 8; ++q) S.Bq[q] = fmin(B, 8.0 * fmin(floater_bound(n, L3[q]), hodo_bound(n, L3[q])));
+    out->B = B;
+    out->S0 = fmin(B, lpoly);
+    for (int q = 0; q < 8; ++q) {
+      dyadic_piece(n, H, q, A);
+      out->Bq[q] = fmin(B, 8.0 * fmin(floater_bound(n, A), hodo_bound(n, A)));
+    }
   }
-  prep[s] = S;
   serr[s] = err ? 1 : 0;
 }
 
@@ -300,7 +323,7 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
                        const double *__restrict__ wts, const SegPrep *__restrict__ prep,
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
-                       Cold<R> *__restrict__ cold) {
+                       Cold<R> *__restrict__ cold, int dbg_flags) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_groups) return;
   const PlanGroup G = groups[g];
@@ -349,7 +372,8 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // see k_query; fp32 records: S0 (1 + 2^-17) + M32.  Eq. 2 uses B (cold).
-    const double S0 = (sizeof(R) == 8) ? bp.S0 * (1.0 + 0x1p-17) + G.M * 0x1p24 : bp.S0 * (1.0 + rel) + G.M;
+    const double S0r = (dbg_flags & 2) ? bp.B : bp.S0;
+    const double S0 = (sizeof(R) == 8) ? S0r * (1.0 + 0x1p-17) + G.M * 0x1p24 : S0r * (1.0 + rel) + G.M;
     const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
     put_rec<R>(hot, r++, px[n], py[n], S0, K_SEG | fa | ((uint32_t)cl << 8));
@@ -357,7 +381,7 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
     C.B = Br;
     for (int q = 0; q < 8; ++q) {
-      const double bq = bp.Bq[q] * (1.0 + rel);
+      const double bq = (dbg_flags & 1 ? bp.B : bp.Bq[q]) * (1.0 + rel);
       C.Bq[q] = (sizeof(R) == 4) ? (R)f_up(bq) : (R)bq;
     }
     C.M = (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M;
@@ -606,7 +630,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     ++g_build_launches;
     k_emit<R><<<(ng + 127) / 128, 128, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
                                                  B.w, B.prep, B.shift, B.brk, B.info, rel, (Hot<R> *)F->hot,
-                                                 (Cold<R> *)F->cold);
+                                                 (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());
     WN_CUDA(cudaFreeAsync(dg, st));
   }

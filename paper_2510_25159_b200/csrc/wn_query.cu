@@ -319,11 +319,10 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
     int base = 0;
     if (lane == 0) base = atomicAdd(P.hq_count, qn);
     base = __shfl_sync(0xffffffffu, base, 0);
-    const bool fits = base + qn <= P.hq_cap;
     for (int i = lane; i < qn; i += 32) {
       const uint32_t e = s_q[warp][i];
       const int q = e & 0xFF;
-      if (fits) {
+      if (base + i < P.hq_cap) {   // slots past the capacity are never read by k_hard
         HardEntry H;
         H.px = s_px[q];
         H.py = s_py[q];

@@ -372,8 +372,10 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // see k_query; fp32 records: S0 (1 + 2^-17) + M32.  Eq. 2 uses B (cold).
-    const double S0r = (dbg_flags & 2) ? bp.B : bp.S0;
-    const double S0 = (sizeof(R) == 8) ? S0r * (1.0 + 0x1p-17) + G.M * 0x1p24 : S0r * (1.0 + rel) + G.M;
+    // fp64 records: the fp32 filter span; its (1 - 2^-18) error shrink is folded
+    // in as a further factor (1 + 2^-17)
+    const double S0 = (sizeof(R) == 8) ? (bp.S0 * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17)
+                                       : bp.S0 * (1.0 + rel) + G.M;
     const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
     put_rec<R>(hot, r++, px[n], py[n], S0, K_SEG | fa | ((uint32_t)cl << 8));
@@ -982,8 +984,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   P.end();
   if (P.recs < 0 || P.colds >= (1 << 23) * 64) { set_error("too many records"); return WN_ERR_ARG; }
   for (int f = 0; f < n_faces; ++f)
-    if (P.cold_off[f + 1] - P.cold_off[f] >= (1 << 23) || P.rec_off[f + 1] - P.rec_off[f] >= (1 << 24)) {
-      set_error("face %d: too many records for the 23/24-bit record indices", f);
+    if (P.cold_off[f + 1] - P.cold_off[f] >= (1 << 22) || P.rec_off[f + 1] - P.rec_off[f] >= (1 << 24)) {
+      set_error("face %d: too many records for the 22/24-bit record indices", f);
       return WN_ERR_ARG;
     }
 

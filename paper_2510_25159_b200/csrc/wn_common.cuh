@@ -72,10 +72,13 @@ struct SegPrep {
   double Bq[8];
 };
 
-// hard-pair queue entry: q (8 bits) | angle (1 bit) | cold local index (23 bits)
+// hard-pair queue entry (shared memory): q (9 bits) | angle (1 bit) | cold local index (22 bits)
 __host__ __device__ inline uint32_t hp_pack(int q, int angle, int cold) {
-  return (uint32_t)q | ((uint32_t)angle << 8) | ((uint32_t)cold << 9);
+  return (uint32_t)q | ((uint32_t)angle << 9) | ((uint32_t)cold << 10);
 }
+__host__ __device__ inline int hp_q(uint32_t e) { return (int)(e & 0x1FFu); }
+__host__ __device__ inline int hp_angle(uint32_t e) { return (int)((e >> 9) & 1u); }
+__host__ __device__ inline int hp_cold(uint32_t e) { return (int)(e >> 10); }
 
 struct Tile {
   int32_t face;
@@ -116,8 +119,10 @@ struct LoopInfo {
   double bb[4];         // lifted control-point box xmin, ymin, xmax, ymax
 };
 
-constexpr int QT = 256;          // queries per tile (one per thread)
-constexpr int NWARP = QT / 32;
+constexpr int NTH = 256;         // threads per query CTA
+constexpr int QPT = 2;           // adjacent queries per thread (ILP; records shared)
+constexpr int QT = NTH * QPT;    // queries per tile
+constexpr int NWARP = NTH / 32;
 constexpr int QW = 128;          // per-warp hard-pair queue capacity
 constexpr int MAXD = 64;         // hard cap of the explicit stack
 constexpr double TWO_PI = 6.283185307179586476925286766559;

@@ -240,13 +240,63 @@ __device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px,
 }
 
 // ---------------------------------------------------------------------------
-// K3a: phase 1 of the query kernel.  One CTA = one tile of <= 256 queries of
-// one face; TMA-staged record program swept in lock-step by all warps.
+// K3a: phase 1 of the query kernel.  One CTA (NTH threads) = one tile of up to
+// QT = NTH x QPT queries of one face, QPT adjacent queries per thread; the
+// face's TMA-staged record program is swept in lock-step by all warps, so every
+// record is one broadcast shared-memory read shared by 2 x 32 queries.
 // ---------------------------------------------------------------------------
+template <typename R>
+struct HotView;
+template <>
+struct HotView<double> {   // explicit ld.shared of one 32-B record
+  float fx, fy, fs;
+  uint32_t meta;
+  double x, y;
+  __device__ __forceinline__ void load(unsigned a) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(fx), "=f"(fy), "=f"(fs), "=r"(meta)
+                 : "r"(a));
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + 16));
+  }
+};
+template <>
+struct HotView<float> {
+  float fx, fy, fs;
+  uint32_t meta;
+  double x, y;   // fp32 records: (x, y) = (fx, fy) promoted
+  __device__ __forceinline__ void load(unsigned a) {
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(fx), "=f"(fy), "=f"(fs), "=r"(meta)
+                 : "r"(a));
+    x = fx;
+    y = fy;
+  }
+};
+
+__device__ __forceinline__ bool group_out_v(const HotView<double> &h, double px, double py) {
+  return !((double)h.fx <= px && px <= (double)h.fs && (double)h.fy <= py && py <= h.x);
+}
+__device__ __forceinline__ bool group_out_v(const HotView<float> &h, double px, double py) {
+  uint32_t c = __float_as_uint(h.fs);
+  const __half2 hi = *reinterpret_cast<const __half2 *>(&c);
+  const float x = (float)px, y = (float)py;
+  return !(h.fx <= x && x <= __half2float(hi.x) && h.fy <= y && y <= __half2float(hi.y));
+}
+
+// approximate fp32 |(dx,dy)| with flush-to-zero rsqrt (1 MUFU); a zero or
+// overflowing argument gives NaN/inf and every filter test treats it as
+// "not certified" (conservative)
+__device__ __forceinline__ float fdist_ftz(float dx, float dy) {
+  const float r = fmaf(dx, dx, dy * dy);
+  float rs;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(r));
+  return r * rs;
+}
+
 template <typename R, bool COUNT>
-__global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
+__global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
-  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
+  constexpr int RCH = F64 ? 960 : 1920;                  // records per staged chunk (30 KB)
   __shared__ __align__(128) Hot<R> s_rec[RCH];
   __shared__ uint32_t s_q[NWARP][QW];
   __shared__ double s_px[QT], s_py[QT];
@@ -258,30 +308,42 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   const Tile T = P.tiles[blockIdx.x];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int f = T.face;
-  bool valid = t < T.qcnt;
-  const int32_t pos = (int32_t)T.qbeg + t;
-  const int32_t qi = valid ? (*P.unsorted ? P.perm[pos] : pos) : 0;
-  double px = 0.0, py = 0.0;
-  if (valid) {
-    double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
-    if (!isfinite(u) || !isfinite(v)) {
-      P.winding[qi] = nan_d();
-      P.flag[qi] = 3;
-      valid = false;
-    } else {
-      const uint8_t per = P.face_per[f];
-      const double *dom = P.face_dom + 4 * f;
-      if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
-      if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
-      if (!F64) { u = (double)(float)u; v = (double)(float)v; }
-      px = u;
-      py = v;
+  const uint8_t per = P.face_per[f];
+  const double *dom = P.face_dom + 4 * f;
+  bool valid[QPT];
+  int32_t qi[QPT];
+  double px[QPT], py[QPT];
+  float pxf[QPT], pyf[QPT];
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    const int ql = QPT * t + k;
+    valid[k] = ql < T.qcnt;
+    const int32_t pos = (int32_t)T.qbeg + ql;
+    qi[k] = valid[k] ? (*P.unsorted ? P.perm[pos] : pos) : 0;
+    double u = 0.0, v = 0.0;
+    if (valid[k]) {
+      u = P.uv[2 * (int64_t)qi[k]];
+      v = P.uv[2 * (int64_t)qi[k] + 1];
+      if (!isfinite(u) || !isfinite(v)) {
+        P.winding[qi[k]] = nan_d();
+        P.flag[qi[k]] = 3;
+        valid[k] = false;
+        u = v = 0.0;
+      } else {
+        if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
+        if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
+        if (!F64) { u = (double)(float)u; v = (double)(float)v; }
+      }
     }
+    px[k] = u;
+    py[k] = v;
+    pxf[k] = (float)u;
+    pyf[k] = (float)v;
+    s_px[ql] = u;
+    s_py[ql] = v;
+    s_qi[ql] = qi[k];
+    s_pend[ql] = 0;
   }
-  s_px[t] = px;
-  s_py[t] = py;
-  s_qi[t] = qi;
-  s_pend[t] = 0;
   if (t == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -291,29 +353,30 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   const int rec0 = P.face_rec_off[f];
   const int nrec = P.face_rec_off[f + 1] - rec0;
   const int cold0 = P.face_cold_off[f];
-  const Cold<R> *cold_face = P.cold + cold0;
   const double eps = P.eps;
-  // fp32 filter constants (fp64 records): margins 2^-16 scale, 2^-18 relative
-  const double Mf = P.face_M[f];
-  const float eps_cert = F64 ? __double2float_ru(eps + Mf * 0x1p24) : 0.f;
-  const float shrink = 1.0f - 0x1p-18f;
-  const float pxf = (float)px, pyf = (float)py;
+  // fp32-filter constant: a distance df > eps_c certifies d >= eps
+  // (fp64 records; margins 2^-16 scale + 2^-17 relative)
+  const float eps_c = F64 ? __double2float_ru((eps + P.face_M[f] * 0x1p24) * (1.0 + 0x1p-17)) : (float)eps;
 
-  // per-lane state
-  double cx = 0.0, cy = 0.0;     // previous chain point, exact, relative to p (F64); fp32 variant uses float
-  float cdf = 0.f;               // its fp32 distance (filter)
-  double ax = 0.0, ay = 0.0;     // group start A relative to p
-  int xs = 0, halves = 0;
-  double fr = 0.0;
-  bool onb = false;
-  int skip_end = 0;
+  // record-stream state (warp-uniform): previous chain point, group start A
+  double prx = 0.0, pry = 0.0, gax = 0.0, gay = 0.0;
+  // per-query state
+  float cdf[QPT];
+  bool up[QPT], onb[QPT];
+  int xs[QPT], halves[QPT], skip_end[QPT];
+  double fr[QPT];
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    cdf[k] = 0.f; up[k] = false; onb[k] = false; xs[k] = 0; halves[k] = 0; skip_end[k] = 0; fr[k] = 0.0;
+  }
   int qn = 0;                    // this warp's queue length (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
   unsigned phase = 0;
   int gr = 0;                    // warp-uniform record cursor
+  const unsigned sbase = smem_u32(s_rec);
 
-  // flush this warp's smem queue to the global queue; when the queue is full the
-  // query is handed to the overflow kernel instead (k_overflow, exact, rare)
+  // flush this warp's smem queue to the global queue; pairs that do not fit
+  // hand their query to the overflow kernel (k_overflow, exact, rare)
   auto flush = [&]() {
     __syncwarp();
     int base = 0;
@@ -321,17 +384,17 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
     base = __shfl_sync(0xffffffffu, base, 0);
     for (int i = lane; i < qn; i += 32) {
       const uint32_t e = s_q[warp][i];
-      const int q = e & 0xFF;
+      const int q = hp_q(e);
       if (base + i < P.hq_cap) {   // slots past the capacity are never read by k_hard
         HardEntry H;
         H.px = s_px[q];
         H.py = s_py[q];
         H.q = s_qi[q];
-        H.c = (uint32_t)(cold0 + (int)(e >> 9)) | (((e >> 8) & 1u) << 31);
+        H.c = (uint32_t)(cold0 + hp_cold(e)) | ((uint32_t)hp_angle(e) << 31);
         P.hq[base + i] = H;
-        s_pend[q] |= 1;
+        atomicOr(&s_pend[q], 1);
       } else {
-        s_pend[q] |= 2;
+        atomicOr(&s_pend[q], 2);
       }
     }
     __syncwarp();
@@ -350,117 +413,130 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
     phase ^= 1u;
     const int ce = cb + cn;
     while (gr < ce) {
-      const Hot<R> h = s_rec[gr - cb];
+      HotView<R> h;
+      h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
       const uint32_t meta = h.meta;
       const uint32_t kind = meta & 0xFu;
-      const bool act = valid && gr >= skip_end;
-      if (kind == K_SEG) {
+      if (__builtin_expect(kind == K_SEG, 1)) {
         // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5)
-        bool hard = false;
-        if constexpr (F64) {
-          const double dy = h.y - py;                          // exact sign (rounding keeps it)
-          const float df = fdist(h.fx - pxf, h.fy - pyf);
+        bool hard[QPT];
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          const bool act = valid[k] && gr >= skip_end[k];
+          bool u1;
+          float df;
+          if constexpr (F64) {
+            u1 = h.y >= py[k];                                 // exact side of the branch cut
+            df = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+          } else {
+            u1 = h.fy >= pyf[k];
+            const float dx = h.fx - pxf[k], dy = h.fy - pyf[k];
+            df = sqrtf(dx * dx + dy * dy);
+          }
+          hard[k] = false;
           if (act) {
-            if (!(df * shrink > eps_cert)) {                   // filter cannot certify d >= eps
-              const double dx = h.x - px;
-              onb |= sqrt(dx * dx + dy * dy) < eps;
+            if (!(df > eps_c)) {                               // filter cannot certify d >= eps
+              if constexpr (F64) {
+                const double dx = h.x - px[k], dy = h.y - py[k];
+                onb[k] |= sqrt(dx * dx + dy * dy) < eps;
+              } else {
+                onb[k] = true;
+              }
             }
-            if ((cdf + df) * shrink > h.fs) {                  // certified pruned: chord (a5)
+            if (cdf[k] + df > h.fs) {                          // certified pruned: chord (a5)
               if (meta & F_ANGLE) {
-                fr += chord_angle(cx - px, cy, h.x - px, dy);
-              } else if ((cy >= 0.0) != (dy >= 0.0)) {
-                xs += xcount(cx - px, cy, h.x - px, dy);
+                if constexpr (F64) fr[k] += chord_angle(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
+                else fr[k] += (double)chord_angle((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
+              } else if (u1 != up[k]) {
+                if constexpr (F64) xs[k] += xcount(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
+                else xs[k] += xcount((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
               }
             } else {
-              hard = !onb;                                     // exact recursion in phase 2
+              hard[k] = !onb[k];                               // exact recursion in phase 2
             }
             if (COUNT) ++c_pairs;
           }
-          cx = h.x;            // absolute (F64 path keeps the exact coordinate)
-          cy = dy;
-          cdf = df;
-        } else {
-          const float dx = h.a - (float)px, dy = h.b - (float)py;
-          const float d = sqrtf(dx * dx + dy * dy);
-          if (act) {
-            onb |= d < (float)eps;
-            if (cdf + d > h.c) {
-              if (meta & F_ANGLE) fr += (double)chord_angle((float)cx, (float)cy, dx, dy);
-              else xs += xcount((float)cx, (float)cy, dx, dy);
-            } else {
-              hard = !onb;
-            }
-            if (COUNT) ++c_pairs;
-          }
-          cx = (double)dx;
-          cy = (double)dy;
-          cdf = d;
+          cdf[k] = df;
+          up[k] = u1;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, hard);
-        if (m) {
-          if (hard) {
-            const int slot = qn + __popc(m & ((1u << lane) - 1u));
-            s_q[warp][slot] = hp_pack(t, (meta & F_ANGLE) ? 1 : 0, (int)(meta >> 8));
+        prx = h.x;
+        pry = h.y;
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
+          if (m) {
+            if (hard[k]) {
+              const int slot = qn + __popc(m & ((1u << lane) - 1u));
+              s_q[warp][slot] = hp_pack(QPT * t + k, (meta & F_ANGLE) ? 1 : 0, (int)(meta >> 8));
+            }
+            qn += __popc(m);
+            if (COUNT) c_hard += hard[k] ? 1 : 0;
+            if (qn > QW - 32) flush();
           }
-          qn += __popc(m);
-          if (COUNT) c_hard += hard ? 1 : 0;
-          if (qn > QW - 32) flush();
         }
       } else if (kind == K_MOVE || kind == K_MOVEG) {
-        double nx, ny;
-        float nd;
-        if constexpr (F64) {
-          nx = h.x - px;
-          ny = h.y - py;
-          nd = fdist(h.fx - pxf, h.fy - pyf);
-          if (act && !(nd * shrink > eps_cert)) onb |= sqrt(nx * nx + ny * ny) < eps;
-        } else {
-          nx = (double)(h.a - (float)px);
-          ny = (double)(h.b - (float)py);
-          nd = sqrtf((float)(nx * nx + ny * ny));
-          if (act) onb |= nd < (float)eps;
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          const bool act = valid[k] && gr >= skip_end[k];
+          const double nx = h.x - px[k], ny = h.y - py[k];
+          float nd;
+          if constexpr (F64) nd = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+          else nd = sqrtf((float)(nx * nx + ny * ny));
+          if (act) {
+            if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : true;
+            if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+              // gap chord Z -> A': -omega(p,Z,A') + its crossing
+              const double zx = prx - px[k], zy = pry - py[k];
+              const double cr = canon_cross(zx, zy, nx, ny);
+              fr[k] -= atan2(cr, zx * nx + zy * ny);
+              xs[k] += xcount_exact(zx, zy, nx, ny, cr);
+            }
+          }
+          cdf[k] = nd;
+          up[k] = F64 ? (h.y >= py[k]) : (h.fy >= pyf[k]);
         }
-        if (act && kind == K_MOVEG && !(meta & F_ANGLE)) {
-          // gap chord Z -> A': -omega(p,Z,A') + its crossing
-          const double zx = F64 ? cx - px : cx;
-          const double cr = canon_cross(zx, cy, nx, ny);
-          fr -= atan2(cr, zx * nx + cy * ny);
-          xs += xcount_exact(zx, cy, nx, ny, cr);
-        }
-        if (kind == K_MOVE) { ax = nx; ay = ny; }
-        cx = F64 ? nx + px : nx;
-        if constexpr (F64) cx = h.x;
-        cy = ny;
-        cdf = nd;
+        if (kind == K_MOVE) { gax = h.x; gay = h.y; }
+        prx = h.x;
+        pry = h.y;
       } else if (kind == K_GROUP) {
         // copy-group / closed-loop cull: p outside the group's box => exactly 0
-        const bool out = !act || group_out<R>(h, px, py);
+        bool out[QPT], all = true;
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          out[k] = !(valid[k] && gr >= skip_end[k]) || group_out_v(h, px[k], py[k]);
+          all &= out[k];
+        }
         const int skip = (int)(meta >> 8);
-        if (__all_sync(0xffffffffu, out)) {
+        if (__all_sync(0xffffffffu, all)) {
           gr += skip;
           if (COUNT && lane == 0) ++c_cull;
-        } else if (out && act) {
-          skip_end = gr + 1 + skip;
+        } else {
+#pragma unroll
+          for (int k = 0; k < QPT; ++k)
+            if (out[k] && valid[k] && gr >= skip_end[k]) skip_end[k] = gr + 1 + skip;
         }
       } else if (kind == K_LINE) {
         // omega(p,L) = +-1/2, p on L counts as left (R11)
-        double c;
-        if constexpr (F64) c = h.x; else c = (double)h.a;
-        const double q = (meta & F_AXISV) ? px : py;
-        const bool left = (meta & F_GE) ? (q >= c) : (q <= c);
-        if (act) halves += left ? 1 : -1;
-      } else if (kind == K_XCH) {
-        const double zx = F64 ? cx - px : cx;
-        if (act) xs -= xcount_exact(ax, ay, zx, cy, canon_cross(ax, ay, zx, cy));
-      } else if (kind == K_NCH) {
-        const double zx = F64 ? cx - px : cx;
-        if (act) fr -= chord_angle(ax, ay, zx, cy);
-      } else if (kind == K_CLOSEG) {
-        const double zx = F64 ? cx - px : cx;
-        if (act) {
-          const double cr = canon_cross(zx, cy, ax, ay);
-          fr -= atan2(cr, zx * ax + cy * ay);
-          xs += xcount_exact(zx, cy, ax, ay, cr);
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          const double q = (meta & F_AXISV) ? px[k] : py[k];
+          const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
+          if (valid[k] && gr >= skip_end[k]) halves[k] += left ? 1 : -1;
+        }
+      } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          if (!(valid[k] && gr >= skip_end[k])) continue;
+          const double zx = prx - px[k], zy = pry - py[k], ax = gax - px[k], ay = gay - py[k];
+          if (kind == K_XCH) {
+            xs[k] -= xcount_exact(ax, ay, zx, zy, canon_cross(ax, ay, zx, zy));
+          } else if (kind == K_NCH) {
+            fr[k] -= chord_angle(ax, ay, zx, zy);
+          } else {
+            const double cr = canon_cross(zx, zy, ax, ay);
+            fr[k] -= atan2(cr, zx * ax + zy * ay);
+            xs[k] += xcount_exact(zx, zy, ax, ay, cr);
+          }
         }
       }
       ++gr;
@@ -471,26 +547,30 @@ __global__ void __launch_bounds__(QT, 4) k_phase1(QParams<R> P) {
   __syncthreads();
 
   // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
-  if (valid) {
-    const bool ob = onb;
-    if (ob) {
-      P.winding[qi] = nan_d();
-      P.flag[qi] = 2;
-      if (COUNT) atomicAdd(P.counters + 7, 1ull);
-    } else {
-      const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
-      P.winding[qi] = w;
-      if (!s_pend[t]) P.flag[qi] = classify(w, P.rule);
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) {
+    const int ql = QPT * t + k;
+    const int pnd = s_pend[ql];
+    if (valid[k]) {
+      if (onb[k]) {
+        P.winding[qi[k]] = nan_d();
+        P.flag[qi[k]] = 2;
+        if (COUNT) atomicAdd(P.counters + 7, 1ull);
+      } else {
+        const double w = (double)xs[k] + 0.5 * (double)halves[k] + fr[k] * (1.0 / TWO_PI);
+        P.winding[qi[k]] = w;
+        if (!pnd) P.flag[qi[k]] = classify(w, P.rule);
+      }
     }
-  }
-  const bool pend = valid && !onb && s_pend[t];
-  const unsigned pm = __ballot_sync(0xffffffffu, pend);
-  if (pm) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
-    if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((s_pend[t] & 2) ? (int32_t)0x80000000 : 0);
+    const bool pend = valid[k] && !onb[k] && pnd;
+    const unsigned pm = __ballot_sync(0xffffffffu, pend);
+    if (pm) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
+      if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi[k] | ((pnd & 2) ? (int32_t)0x80000000 : 0);
+    }
   }
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
@@ -775,12 +855,12 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const int hb = 148 * 8;
   if (F->counters_on) {
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 8 * sizeof(unsigned long long), st));
-    k_phase1<R, true><<<max_tiles, QT, 0, st>>>(P);
+    k_phase1<R, true><<<max_tiles, NTH, 0, st>>>(P);
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, F->counters);
   } else {
-    k_phase1<R, false><<<max_tiles, QT, 0, st>>>(P);
+    k_phase1<R, false><<<max_tiles, NTH, 0, st>>>(P);
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, nullptr);

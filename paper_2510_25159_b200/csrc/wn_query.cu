@@ -362,12 +362,13 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   double prx = 0.0, pry = 0.0, gax = 0.0, gay = 0.0;
   // per-query state
   float cdf[QPT];
-  bool up[QPT], onb[QPT];
+  bool up[QPT], onb[QPT], act[QPT];
   int xs[QPT], halves[QPT], skip_end[QPT];
   double fr[QPT];
 #pragma unroll
   for (int k = 0; k < QPT; ++k) {
-    cdf[k] = 0.f; up[k] = false; onb[k] = false; xs[k] = 0; halves[k] = 0; skip_end[k] = 0; fr[k] = 0.0;
+    cdf[k] = 0.f; up[k] = false; onb[k] = false; act[k] = valid[k];
+    xs[k] = 0; halves[k] = 0; skip_end[k] = 0; fr[k] = 0.0;
   }
   int qn = 0;                    // this warp's queue length (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
@@ -418,124 +419,141 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
       const uint32_t meta = h.meta;
       const uint32_t kind = meta & 0xFu;
       if (__builtin_expect(kind == K_SEG, 1)) {
-        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5)
-        bool hard[QPT];
+        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5).
+        // Fast path (branch-free): fp32 filter certifies "pruned, no crossing,
+        // d >= eps"; anything else takes the exact slow path below.
+        float df[QPT];
+        bool u1[QPT], pr[QPT], need[QPT];
+        bool any = false;
 #pragma unroll
         for (int k = 0; k < QPT; ++k) {
-          const bool act = valid[k] && gr >= skip_end[k];
-          bool u1;
-          float df;
           if constexpr (F64) {
-            u1 = h.y >= py[k];                                 // exact side of the branch cut
-            df = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+            u1[k] = h.y >= py[k];                              // exact side of the branch cut
+            df[k] = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
           } else {
-            u1 = h.fy >= pyf[k];
+            u1[k] = h.fy >= pyf[k];
             const float dx = h.fx - pxf[k], dy = h.fy - pyf[k];
-            df = sqrtf(dx * dx + dy * dy);
+            df[k] = sqrtf(dx * dx + dy * dy);
           }
-          hard[k] = false;
-          if (act) {
-            if (!(df > eps_c)) {                               // filter cannot certify d >= eps
-              if constexpr (F64) {
-                const double dx = h.x - px[k], dy = h.y - py[k];
-                onb[k] |= sqrt(dx * dx + dy * dy) < eps;
+          pr[k] = cdf[k] + df[k] > h.fs;                       // certified pruned
+          need[k] = act[k] && (!pr[k] || !(df[k] > eps_c) || u1[k] != up[k] || (meta & F_ANGLE));
+          any |= need[k];
+          if (COUNT && act[k]) ++c_pairs;
+        }
+        if (__any_sync(0xffffffffu, any)) {
+          bool hard[QPT];
+#pragma unroll
+          for (int k = 0; k < QPT; ++k) {
+            hard[k] = false;
+            if (need[k]) {
+              if (!(df[k] > eps_c)) {                          // filter cannot certify d >= eps
+                if constexpr (F64) {
+                  const double dx = h.x - px[k], dy = h.y - py[k];
+                  onb[k] |= sqrt(dx * dx + dy * dy) < eps;
+                } else {
+                  onb[k] |= df[k] < (float)eps;
+                }
+              }
+              if (pr[k]) {                                     // pruned: chord (a5)
+                if (meta & F_ANGLE) {
+                  if constexpr (F64) fr[k] += chord_angle(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
+                  else fr[k] += (double)chord_angle((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
+                } else if (u1[k] != up[k]) {
+                  if constexpr (F64) xs[k] += xcount(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
+                  else xs[k] += xcount((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
+                }
               } else {
-                onb[k] = true;
+                hard[k] = !onb[k];                             // exact recursion in phase 2
               }
             }
-            if (cdf[k] + df > h.fs) {                          // certified pruned: chord (a5)
-              if (meta & F_ANGLE) {
-                if constexpr (F64) fr[k] += chord_angle(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
-                else fr[k] += (double)chord_angle((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
-              } else if (u1 != up[k]) {
-                if constexpr (F64) xs[k] += xcount(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
-                else xs[k] += xcount((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
-              }
-            } else {
-              hard[k] = !onb[k];                               // exact recursion in phase 2
-            }
-            if (COUNT) ++c_pairs;
           }
-          cdf[k] = df;
-          up[k] = u1;
+#pragma unroll
+          for (int k = 0; k < QPT; ++k) {
+            const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
+            if (m) {
+              if (hard[k]) {
+                const int slot = qn + __popc(m & ((1u << lane) - 1u));
+                s_q[warp][slot] = hp_pack(QPT * t + k, (meta & F_ANGLE) ? 1 : 0, (int)(meta >> 8));
+              }
+              qn += __popc(m);
+              if (COUNT) c_hard += hard[k] ? 1 : 0;
+              if (qn > QW - 32) flush();
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < QPT; ++k) {
+          cdf[k] = df[k];
+          up[k] = u1[k];
         }
         prx = h.x;
         pry = h.y;
+      } else {
+        // group boundaries: a culled query becomes active again after its group
 #pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
-          if (m) {
-            if (hard[k]) {
-              const int slot = qn + __popc(m & ((1u << lane) - 1u));
-              s_q[warp][slot] = hp_pack(QPT * t + k, (meta & F_ANGLE) ? 1 : 0, (int)(meta >> 8));
+        for (int k = 0; k < QPT; ++k) act[k] = valid[k] && gr >= skip_end[k];
+        if (kind == K_MOVE || kind == K_MOVEG) {
+#pragma unroll
+          for (int k = 0; k < QPT; ++k) {
+            const double nx = h.x - px[k], ny = h.y - py[k];
+            float nd;
+            if constexpr (F64) nd = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+            else nd = sqrtf((float)(nx * nx + ny * ny));
+            if (act[k]) {
+              if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
+              if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+                // gap chord Z -> A': -omega(p,Z,A') + its crossing
+                const double zx = prx - px[k], zy = pry - py[k];
+                const double cr = canon_cross(zx, zy, nx, ny);
+                fr[k] -= atan2(cr, zx * nx + zy * ny);
+                xs[k] += xcount_exact(zx, zy, nx, ny, cr);
+              }
             }
-            qn += __popc(m);
-            if (COUNT) c_hard += hard[k] ? 1 : 0;
-            if (qn > QW - 32) flush();
+            cdf[k] = nd;
+            up[k] = F64 ? (h.y >= py[k]) : (h.fy >= pyf[k]);
           }
-        }
-      } else if (kind == K_MOVE || kind == K_MOVEG) {
+          if (kind == K_MOVE) { gax = h.x; gay = h.y; }
+          prx = h.x;
+          pry = h.y;
+        } else if (kind == K_GROUP) {
+          // copy-group / closed-loop cull: p outside the group's box => exactly 0
+          bool out[QPT], all = true;
 #pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          const bool act = valid[k] && gr >= skip_end[k];
-          const double nx = h.x - px[k], ny = h.y - py[k];
-          float nd;
-          if constexpr (F64) nd = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
-          else nd = sqrtf((float)(nx * nx + ny * ny));
-          if (act) {
-            if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : true;
-            if (kind == K_MOVEG && !(meta & F_ANGLE)) {
-              // gap chord Z -> A': -omega(p,Z,A') + its crossing
-              const double zx = prx - px[k], zy = pry - py[k];
-              const double cr = canon_cross(zx, zy, nx, ny);
-              fr[k] -= atan2(cr, zx * nx + zy * ny);
-              xs[k] += xcount_exact(zx, zy, nx, ny, cr);
-            }
+          for (int k = 0; k < QPT; ++k) {
+            out[k] = !act[k] || group_out_v(h, px[k], py[k]);
+            all &= out[k];
           }
-          cdf[k] = nd;
-          up[k] = F64 ? (h.y >= py[k]) : (h.fy >= pyf[k]);
-        }
-        if (kind == K_MOVE) { gax = h.x; gay = h.y; }
-        prx = h.x;
-        pry = h.y;
-      } else if (kind == K_GROUP) {
-        // copy-group / closed-loop cull: p outside the group's box => exactly 0
-        bool out[QPT], all = true;
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          out[k] = !(valid[k] && gr >= skip_end[k]) || group_out_v(h, px[k], py[k]);
-          all &= out[k];
-        }
-        const int skip = (int)(meta >> 8);
-        if (__all_sync(0xffffffffu, all)) {
-          gr += skip;
-          if (COUNT && lane == 0) ++c_cull;
-        } else {
-#pragma unroll
-          for (int k = 0; k < QPT; ++k)
-            if (out[k] && valid[k] && gr >= skip_end[k]) skip_end[k] = gr + 1 + skip;
-        }
-      } else if (kind == K_LINE) {
-        // omega(p,L) = +-1/2, p on L counts as left (R11)
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          const double q = (meta & F_AXISV) ? px[k] : py[k];
-          const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
-          if (valid[k] && gr >= skip_end[k]) halves[k] += left ? 1 : -1;
-        }
-      } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          if (!(valid[k] && gr >= skip_end[k])) continue;
-          const double zx = prx - px[k], zy = pry - py[k], ax = gax - px[k], ay = gay - py[k];
-          if (kind == K_XCH) {
-            xs[k] -= xcount_exact(ax, ay, zx, zy, canon_cross(ax, ay, zx, zy));
-          } else if (kind == K_NCH) {
-            fr[k] -= chord_angle(ax, ay, zx, zy);
+          const int skip = (int)(meta >> 8);
+          if (__all_sync(0xffffffffu, all)) {
+            gr += skip;
+            if (COUNT && lane == 0) ++c_cull;
           } else {
-            const double cr = canon_cross(zx, zy, ax, ay);
-            fr[k] -= atan2(cr, zx * ax + zy * ay);
-            xs[k] += xcount_exact(zx, zy, ax, ay, cr);
+#pragma unroll
+            for (int k = 0; k < QPT; ++k)
+              if (out[k] && act[k]) { skip_end[k] = gr + 1 + skip; act[k] = false; }
+          }
+        } else if (kind == K_LINE) {
+          // omega(p,L) = +-1/2, p on L counts as left (R11)
+#pragma unroll
+          for (int k = 0; k < QPT; ++k) {
+            const double q = (meta & F_AXISV) ? px[k] : py[k];
+            const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
+            if (act[k]) halves[k] += left ? 1 : -1;
+          }
+        } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
+#pragma unroll
+          for (int k = 0; k < QPT; ++k) {
+            if (!act[k]) continue;
+            const double zx = prx - px[k], zy = pry - py[k], ax = gax - px[k], ay = gay - py[k];
+            if (kind == K_XCH) {
+              xs[k] -= xcount_exact(ax, ay, zx, zy, canon_cross(ax, ay, zx, zy));
+            } else if (kind == K_NCH) {
+              fr[k] -= chord_angle(ax, ay, zx, zy);
+            } else {
+              const double cr = canon_cross(zx, zy, ax, ay);
+              fr[k] -= atan2(cr, zx * ax + zy * ay);
+              xs[k] += xcount_exact(zx, zy, ax, ay, cr);
+            }
           }
         }
       }

@@ -243,7 +243,8 @@ __device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px,
 // K3a: phase 1 of the query kernel.  One CTA (NTH threads) = one tile of up to
 // QT = NTH x QPT queries of one face, QPT adjacent queries per thread; the
 // face's TMA-staged record program is swept in lock-step by all warps, so every
-// record is one broadcast shared-memory read shared by 2 x 32 queries.
+// record is one broadcast shared-memory read shared by 32 x QPT queries.
+// Hard pairs go straight to the global queue through per-warp slot chunks.
 // ---------------------------------------------------------------------------
 template <typename R>
 struct HotView;
@@ -293,20 +294,18 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
   return r * rs;
 }
 
+constexpr int HCH = 64;   // global hard-queue slots reserved per warp at a time
+
 template <typename R, bool COUNT>
-__global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
+__global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
-  constexpr int RCH = F64 ? 960 : 1920;                  // records per staged chunk (30 KB)
+  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
   __shared__ __align__(128) Hot<R> s_rec[RCH];
-  __shared__ uint32_t s_q[NWARP][QW];
-  __shared__ double s_px[QT], s_py[QT];
-  __shared__ int32_t s_qi[QT];
-  __shared__ int s_pend[QT];
   __shared__ __align__(8) uint64_t s_bar;
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
   const Tile T = P.tiles[blockIdx.x];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int t = threadIdx.x, lane = t & 31;
   const int f = T.face;
   const uint8_t per = P.face_per[f];
   const double *dom = P.face_dom + 4 * f;
@@ -339,10 +338,6 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
     py[k] = v;
     pxf[k] = (float)u;
     pyf[k] = (float)v;
-    s_px[ql] = u;
-    s_py[ql] = v;
-    s_qi[ql] = qi[k];
-    s_pend[ql] = 0;
   }
   if (t == 0) {
     mbar_init(&s_bar, 1);
@@ -363,43 +358,24 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   // per-query state
   float cdf[QPT];
   bool up[QPT], onb[QPT], act[QPT];
-  int xs[QPT], halves[QPT], skip_end[QPT];
+  int xs[QPT], halves[QPT], skip_end[QPT], pend[QPT];
   double fr[QPT];
 #pragma unroll
   for (int k = 0; k < QPT; ++k) {
     cdf[k] = 0.f; up[k] = false; onb[k] = false; act[k] = valid[k];
-    xs[k] = 0; halves[k] = 0; skip_end[k] = 0; fr[k] = 0.0;
+    xs[k] = 0; halves[k] = 0; skip_end[k] = 0; pend[k] = 0; fr[k] = 0.0;
   }
-  int qn = 0;                    // this warp's queue length (warp-uniform)
+  int hbase = -1, hused = HCH;   // this warp's reserved slot chunk of the global queue
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
   unsigned phase = 0;
   int gr = 0;                    // warp-uniform record cursor
   const unsigned sbase = smem_u32(s_rec);
 
-  // flush this warp's smem queue to the global queue; pairs that do not fit
-  // hand their query to the overflow kernel (k_overflow, exact, rare)
-  auto flush = [&]() {
-    __syncwarp();
-    int base = 0;
-    if (lane == 0) base = atomicAdd(P.hq_count, qn);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (int i = lane; i < qn; i += 32) {
-      const uint32_t e = s_q[warp][i];
-      const int q = hp_q(e);
-      if (base + i < P.hq_cap) {   // slots past the capacity are never read by k_hard
-        HardEntry H;
-        H.px = s_px[q];
-        H.py = s_py[q];
-        H.q = s_qi[q];
-        H.c = (uint32_t)(cold0 + hp_cold(e)) | ((uint32_t)hp_angle(e) << 31);
-        P.hq[base + i] = H;
-        atomicOr(&s_pend[q], 1);
-      } else {
-        atomicOr(&s_pend[q], 2);
-      }
-    }
-    __syncwarp();
-    qn = 0;
+  // invalidate the unused tail of this warp's chunk (k_hard skips q < 0)
+  auto close_chunk = [&]() {
+    if (hbase >= 0)
+      for (int i = hused + lane; i < HCH; i += 32)
+        if (hbase + i < P.hq_cap) P.hq[hbase + i].q = -1;
   };
 
   for (int cb = 0; cb < nrec; cb += RCH) {
@@ -413,15 +389,17 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
     }
     phase ^= 1u;
     const int ce = cb + cn;
+    HotView<R> hn;
+    if (gr < ce) hn.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
     while (gr < ce) {
-      HotView<R> h;
-      h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
+      const HotView<R> h = hn;
+      if (gr + 1 < ce) hn.load(sbase + (unsigned)(gr + 1 - cb) * (unsigned)sizeof(Hot<R>));   // prefetch
       const uint32_t meta = h.meta;
       const uint32_t kind = meta & 0xFu;
       if (__builtin_expect(kind == K_SEG, 1)) {
         // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5).
-        // Fast path (branch-free): fp32 filter certifies "pruned, no crossing,
-        // d >= eps"; anything else takes the exact slow path below.
+        // Fast path (branch-free): the fp32 filter certifies "pruned, no
+        // crossing, d >= eps"; anything else takes the exact slow path below.
         float df[QPT];
         bool u1[QPT], pr[QPT], need[QPT];
         bool any = false;
@@ -471,13 +449,30 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
           for (int k = 0; k < QPT; ++k) {
             const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
             if (m) {
-              if (hard[k]) {
-                const int slot = qn + __popc(m & ((1u << lane) - 1u));
-                s_q[warp][slot] = hp_pack(QPT * t + k, (meta & F_ANGLE) ? 1 : 0, (int)(meta >> 8));
+              const int cnt = __popc(m);
+              if (hused + cnt > HCH) {                         // new chunk of queue slots
+                close_chunk();
+                int b = 0;
+                if (lane == 0) b = atomicAdd(P.hq_count, HCH);
+                hbase = __shfl_sync(0xffffffffu, b, 0);
+                hused = 0;
               }
-              qn += __popc(m);
-              if (COUNT) c_hard += hard[k] ? 1 : 0;
-              if (qn > QW - 32) flush();
+              if (hard[k]) {
+                const int slot = hbase + hused + __popc(m & ((1u << lane) - 1u));
+                if (slot < P.hq_cap) {
+                  HardEntry H;
+                  H.px = px[k];
+                  H.py = py[k];
+                  H.q = qi[k];
+                  H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
+                  P.hq[slot] = H;
+                  pend[k] |= 1;
+                } else {
+                  pend[k] |= 2;                                // queue full: k_overflow finishes it
+                }
+                if (COUNT) ++c_hard;
+              }
+              hused += cnt;
             }
           }
         }
@@ -526,6 +521,7 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
           const int skip = (int)(meta >> 8);
           if (__all_sync(0xffffffffu, all)) {
             gr += skip;
+            if (gr + 1 < ce) hn.load(sbase + (unsigned)(gr + 1 - cb) * (unsigned)sizeof(Hot<R>));
             if (COUNT && lane == 0) ++c_cull;
           } else {
 #pragma unroll
@@ -559,16 +555,13 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
       }
       ++gr;
     }
-    __syncthreads();   // all warps done with this chunk before it is overwritten
+    if (ce < nrec) __syncthreads();   // all warps done with this chunk before it is overwritten
   }
-  if (qn) flush();
-  __syncthreads();
+  close_chunk();
 
   // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
 #pragma unroll
   for (int k = 0; k < QPT; ++k) {
-    const int ql = QPT * t + k;
-    const int pnd = s_pend[ql];
     if (valid[k]) {
       if (onb[k]) {
         P.winding[qi[k]] = nan_d();
@@ -577,17 +570,17 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
       } else {
         const double w = (double)xs[k] + 0.5 * (double)halves[k] + fr[k] * (1.0 / TWO_PI);
         P.winding[qi[k]] = w;
-        if (!pnd) P.flag[qi[k]] = classify(w, P.rule);
+        if (!pend[k]) P.flag[qi[k]] = classify(w, P.rule);
       }
     }
-    const bool pend = valid[k] && !onb[k] && pnd;
-    const unsigned pm = __ballot_sync(0xffffffffu, pend);
+    const bool pq = valid[k] && !onb[k] && pend[k];
+    const unsigned pm = __ballot_sync(0xffffffffu, pq);
     if (pm) {
       int base = 0;
       if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
       base = __shfl_sync(0xffffffffu, base, 0);
       // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
-      if (pend) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi[k] | ((pnd & 2) ? (int32_t)0x80000000 : 0);
+      if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi[k] | ((pend[k] & 2) ? (int32_t)0x80000000 : 0);
     }
   }
   if (COUNT) {
@@ -606,6 +599,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   const int total = min(*P.hq_count, P.hq_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const HardEntry H = P.hq[i];
+    if (H.q < 0) continue;   // unused slot of a warp's reserved chunk
     const bool angle = H.c >> 31;
     const Cold<R> *C = P.cold + (H.c & 0x7fffffffu);
     const HardResult r = hard_pair<R, COUNT>(C, (R)H.px, (R)H.py, angle, (R)P.eps, P.max_depth, P.counters);

@@ -120,7 +120,7 @@ struct LoopInfo {
 };
 
 constexpr int NTH = 256;         // threads per query CTA
-constexpr int QPT = 4;           // adjacent queries per thread (ILP; records shared)
+constexpr int QPT = 2;           // adjacent queries per thread (ILP; records shared)
 constexpr int QT = NTH * QPT;    // queries per tile
 constexpr int NWARP = NTH / 32;
 constexpr int QW = 128;          // per-warp hard-pair queue capacity

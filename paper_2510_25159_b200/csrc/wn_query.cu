@@ -294,18 +294,21 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
   return r * rs;
 }
 
-constexpr int HCH = 64;   // global hard-queue slots reserved per warp at a time
+constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 
 template <typename R, bool COUNT>
-__global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
+__global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
-  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
+  constexpr int RCH = F64 ? 896 : 1792;                  // records per staged chunk (28 KB)
   __shared__ __align__(128) Hot<R> s_rec[RCH];
+  __shared__ HardEntry s_hb[NWARP][HWB];
+  __shared__ uint16_t s_hl[NWARP][HWB];
+  __shared__ int s_pend[QT];
   __shared__ __align__(8) uint64_t s_bar;
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
   const Tile T = P.tiles[blockIdx.x];
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int f = T.face;
   const uint8_t per = P.face_per[f];
   const double *dom = P.face_dom + 4 * f;
@@ -338,6 +341,7 @@ __global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
     py[k] = v;
     pxf[k] = (float)u;
     pyf[k] = (float)v;
+    s_pend[QPT * t + k] = 0;
   }
   if (t == 0) {
     mbar_init(&s_bar, 1);
@@ -365,17 +369,25 @@ __global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
     cdf[k] = 0.f; up[k] = false; onb[k] = false; act[k] = valid[k];
     xs[k] = 0; halves[k] = 0; skip_end[k] = 0; pend[k] = 0; fr[k] = 0.0;
   }
-  int hbase = -1, hused = HCH;   // this warp's reserved slot chunk of the global queue
+  int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
   unsigned phase = 0;
   int gr = 0;                    // warp-uniform record cursor
   const unsigned sbase = smem_u32(s_rec);
 
-  // invalidate the unused tail of this warp's chunk (k_hard skips q < 0)
-  auto close_chunk = [&]() {
-    if (hbase >= 0)
-      for (int i = hused + lane; i < HCH; i += 32)
-        if (hbase + i < P.hq_cap) P.hq[hbase + i].q = -1;
+  // flush the warp's buffer to the global queue with one exact reservation;
+  // pairs past the capacity tag their query for the overflow kernel
+  auto flush = [&]() {
+    __syncwarp();
+    int b = 0;
+    if (lane == 0) b = atomicAdd(P.hq_count, hn_);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    for (int i = lane; i < hn_; i += 32) {
+      if (b + i < P.hq_cap) P.hq[b + i] = s_hb[warp][i];
+      else atomicOr(&s_pend[s_hl[warp][i]], 2);
+    }
+    __syncwarp();
+    hn_ = 0;
   };
 
   for (int cb = 0; cb < nrec; cb += RCH) {
@@ -450,29 +462,20 @@ __global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
             const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
             if (m) {
               const int cnt = __popc(m);
-              if (hused + cnt > HCH) {                         // new chunk of queue slots
-                close_chunk();
-                int b = 0;
-                if (lane == 0) b = atomicAdd(P.hq_count, HCH);
-                hbase = __shfl_sync(0xffffffffu, b, 0);
-                hused = 0;
-              }
+              if (hn_ + cnt > HWB) flush();
               if (hard[k]) {
-                const int slot = hbase + hused + __popc(m & ((1u << lane) - 1u));
-                if (slot < P.hq_cap) {
-                  HardEntry H;
-                  H.px = px[k];
-                  H.py = py[k];
-                  H.q = qi[k];
-                  H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
-                  P.hq[slot] = H;
-                  pend[k] |= 1;
-                } else {
-                  pend[k] |= 2;                                // queue full: k_overflow finishes it
-                }
+                const int slot = hn_ + __popc(m & ((1u << lane) - 1u));
+                HardEntry H;
+                H.px = px[k];
+                H.py = py[k];
+                H.q = qi[k];
+                H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
+                s_hb[warp][slot] = H;
+                s_hl[warp][slot] = (uint16_t)(QPT * t + k);
+                pend[k] |= 1;
                 if (COUNT) ++c_hard;
               }
-              hused += cnt;
+              hn_ += cnt;
             }
           }
         }
@@ -557,7 +560,10 @@ __global__ void __launch_bounds__(NTH, 2) k_phase1(QParams<R> P) {
     }
     if (ce < nrec) __syncthreads();   // all warps done with this chunk before it is overwritten
   }
-  close_chunk();
+  if (hn_) flush();
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < QPT; ++k) pend[k] |= s_pend[QPT * t + k];
 
   // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
 #pragma unroll
@@ -599,7 +605,6 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   const int total = min(*P.hq_count, P.hq_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const HardEntry H = P.hq[i];
-    if (H.q < 0) continue;   // unused slot of a warp's reserved chunk
     const bool angle = H.c >> 31;
     const Cold<R> *C = P.cold + (H.c & 0x7fffffffu);
     const HardResult r = hard_pair<R, COUNT>(C, (R)H.px, (R)H.py, angle, (R)P.eps, P.max_depth, P.counters);

@@ -137,6 +137,10 @@ wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, int64_t 
 wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, const double *ctrl_w,
                             const int32_t *seg_degree, double *out, void *stream);
 
+/* libwn keeps freed device buffers (records, query scratch) in a per-device
+ * cache for reuse; wn_trim_memory returns them to the driver. */
+void wn_trim_memory(void);
+
 /* Release the handle; the caller guarantees no query on it is in flight. */
 void wn_free_faces(wn_faces_t faces);
 

@@ -29,7 +29,7 @@ STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4
 FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
-           "wn_last_build_launches", "wn_segment_prep"]
+           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "groups_culled_warps", "on_boundary"]
 
@@ -84,6 +84,8 @@ def load():
         L.wn_last_build_launches.argtypes = []
         L.wn_segment_prep.restype = C.c_int
         L.wn_segment_prep.argtypes = [C.c_int32, vp, vp, vp, vp, vp]
+        L.wn_trim_memory.restype = None
+        L.wn_trim_memory.argtypes = []
         L.wn_free_faces.restype = None
         L.wn_free_faces.argtypes = [vp]
         L.wn_last_error.restype = C.c_char_p

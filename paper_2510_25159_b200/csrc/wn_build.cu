@@ -72,112 +72,158 @@ __global__ void k_deg(int32_t n_segs, const int32_t *__restrict__ deg, int32_t *
 // bound on the 8 dyadic pieces [q/8,(q+1)/8] (homogeneous de Casteljau, t-units),
 // used for sub-spans inside one piece (Eq. 2 with the piece's own bound).
 // ---------------------------------------------------------------------------
-// Exact binomial coefficients C(n,k), n <= 10.
-__constant__ double c_binom[11][11] = {
-    {1}, {1, 1}, {1, 2, 1}, {1, 3, 3, 1}, {1, 4, 6, 4, 1}, {1, 5, 10, 10, 5, 1}, {1, 6, 15, 20, 15, 6, 1},
-    {1, 7, 21, 35, 35, 21, 7, 1}, {1, 8, 28, 56, 70, 56, 28, 8, 1}, {1, 9, 36, 84, 126, 126, 84, 36, 9, 1},
-    {1, 10, 45, 120, 210, 252, 210, 120, 45, 10, 1}};
+// Exact binomial coefficients, constant-folded in the unrolled bound code.
+__host__ __device__ constexpr double binom_c(int n, int k) {
+  double r = 1.0;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
 
-// Bounds on flat homogeneous control points H[3i+0..2] = (w x, w y, w), i = 0..n.
-// Written without local aggregates (nvcc 12.9 -O3 miscompiled an earlier
-// array-accumulating version on sm_100a; scripts/dev/kp.cu reproduces it).
-// Hodograph-numerator Bernstein bound: max_k |D_k| / min_k E_k with
-//   D_k = sum_{i+j=k} C(n-1,i)C(n,j)/C(2n-1,k) w_j (w_{i+1}(P_{i+1}-P_j) - w_i(P_i-P_j)),
-//   E_k = sum_{i+j=k} C(n,i)C(n,j)/C(2n,k) w_i w_j.
-__device__ __noinline__ double hodo_bound(int n, const double *H) {
+// Bounds on homogeneous control points (X_i, Y_i, W_i) = w_i (x_i, y_i, 1),
+// i = 0..N, held in registers (templated on the degree, fully unrolled).
+// Written without accumulating into local arrays (an earlier version of that
+// shape was miscompiled by nvcc 12.9 -O3 on sm_100a: scripts/dev/kp.cu).
+//
+// Hodograph-numerator Bernstein bound: |gamma'| = |X'W - XW'| / W^2 with
+//   X'W - XW' = N sum_k D_k B_k^{2N-1},
+//   D_k = sum_{i+j=k} C(N-1,i)C(N,j)/C(2N-1,k) [W_j (X_{i+1}-X_i) - (W_{i+1}-W_i) X_j],
+//   W^2 = sum_k E_k B_k^{2N},  E_k = sum_{i+j=k} C(N,i)C(N,j)/C(2N,k) W_i W_j,
+// so |gamma'| <= N max_k |D_k| / min_k E_k (convex-hull property).
+template <int N>
+__device__ __forceinline__ double hodo_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                             const double (&W)[N + 1]) {
   double dmax = 0.0, emin = INFINITY;
-  for (int k = 0; k <= 2 * n - 1; ++k) {
+#pragma unroll
+  for (int k = 0; k <= 2 * N - 1; ++k) {
     double dx = 0.0, dy = 0.0;
-    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n - 1 ? k : n - 1;
-    for (int i = i0; i <= i1; ++i) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
       const int j = k - i;
-      const double wi = H[3 * i + 2], wi1 = H[3 * i + 5], wj = H[3 * j + 2];
-      const double xi = H[3 * i] / wi, yi = H[3 * i + 1] / wi;
-      const double xi1 = H[3 * i + 3] / wi1, yi1 = H[3 * i + 4] / wi1;
-      const double xj = H[3 * j] / wj, yj = H[3 * j + 1] / wj;
-      const double c = c_binom[n - 1][i] * c_binom[n][j] / c_binom[2 * n - 1][k] * wj;
-      dx += c * (wi1 * (xi1 - xj) - wi * (xi - xj));
-      dy += c * (wi1 * (yi1 - yj) - wi * (yi - yj));
+      if (j < 0 || j > N) continue;
+      const double c = binom_c(N - 1, i) * binom_c(N, j) / binom_c(2 * N - 1, k);
+      dx += c * (W[j] * (X[i + 1] - X[i]) - (W[i + 1] - W[i]) * X[j]);
+      dy += c * (W[j] * (Y[i + 1] - Y[i]) - (W[i + 1] - W[i]) * Y[j]);
     }
     dmax = fmax(dmax, hypot(dx, dy));
   }
-  for (int k = 0; k <= 2 * n; ++k) {
+#pragma unroll
+  for (int k = 0; k <= 2 * N; ++k) {
     double e = 0.0;
-    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n ? k : n;
-    for (int i = i0; i <= i1; ++i) {
+#pragma unroll
+    for (int i = 0; i <= N; ++i) {
       const int j = k - i;
-      e += c_binom[n][i] * c_binom[n][j] / c_binom[2 * n][k] * H[3 * i + 2] * H[3 * j + 2];
+      if (j < 0 || j > N) continue;
+      e += (binom_c(N, i) * binom_c(N, j) / binom_c(2 * N, k)) * W[i] * W[j];
     }
     emin = fmin(emin, e);
   }
-  return n * dmax / emin;
+  return N * dmax / emin;
 }
 
-__device__ __noinline__ double floater_bound(int n, const double *H) {
-  double wmax = H[2], wmin = H[2], dmax = 0.0, diam = 0.0;
-  for (int i = 1; i <= n; ++i) { wmax = fmax(wmax, H[3 * i + 2]); wmin = fmin(wmin, H[3 * i + 2]); }
-  for (int i = 0; i <= n; ++i)
-    for (int j = i + 1; j <= n; ++j) {
-      const double l = hypot(H[3 * j] / H[3 * j + 2] - H[3 * i] / H[3 * i + 2],
-                             H[3 * j + 1] / H[3 * j + 2] - H[3 * i + 1] / H[3 * i + 2]);
+template <int N>
+__device__ __forceinline__ double floater_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                                const double (&W)[N + 1]) {
+  double wmax = W[0], wmin = W[0], dmax = 0.0, diam = 0.0, px[N + 1], py[N + 1];
+#pragma unroll
+  for (int i = 1; i <= N; ++i) { wmax = fmax(wmax, W[i]); wmin = fmin(wmin, W[i]); }
+#pragma unroll
+  for (int i = 0; i <= N; ++i) { px[i] = X[i] / W[i]; py[i] = Y[i] / W[i]; }
+#pragma unroll
+  for (int i = 0; i <= N; ++i)
+#pragma unroll
+    for (int j = i + 1; j <= N; ++j) {
+      const double l = hypot(px[j] - px[i], py[j] - py[i]);
       diam = fmax(diam, l);
       if (j == i + 1) dmax = fmax(dmax, l);
     }
-  if (wmax == wmin) return n * dmax;
+  if (wmax == wmin) return N * dmax;
   const double r = wmax / wmin;
-  return fmin(n * r * diam, n * r * r * dmax);
+  return fmin(N * r * diam, N * r * r * dmax);
 }
 
-// Homogeneous control points of the dyadic piece [q/8, (q+1)/8] of H (blossom-
-// free: three de Casteljau halvings, choosing the half along the bits of q).
-// A receives 3(n+1) values; works in place in A.
-__device__ __noinline__ void dyadic_piece(int n, const double *H, int q, double *A) {
-  for (int i = 0; i < 3 * (n + 1); ++i) A[i] = H[i];
+// piece [q/8,(q+1)/8]: three de Casteljau halvings along the bits of q
+template <int N>
+__device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                             const double (&W)[N + 1], int q, double (&a)[N + 1],
+                                             double (&b)[N + 1], double (&c)[N + 1]) {
+#pragma unroll
+  for (int i = 0; i <= N; ++i) { a[i] = X[i]; b[i] = Y[i]; c[i] = W[i]; }
+#pragma unroll
   for (int lvl = 2; lvl >= 0; --lvl) {
     const bool right = (q >> lvl) & 1;
-    // after r rounds of midpoint averaging, entry 0 is the left half's point r
-    // and entry n-r the right half's point n-r; keep the requested half
-    double L[18], R[18];
-    for (int c = 0; c < 3; ++c) { L[c] = A[c]; R[3 * n + c] = A[3 * n + c]; }
-    for (int r = 1; r <= n; ++r) {
-      for (int j = 0; j <= n - r; ++j)
-        for (int c = 0; c < 3; ++c) A[3 * j + c] = 0.5 * (A[3 * j + c] + A[3 * j + 3 + c]);
-      for (int c = 0; c < 3; ++c) { L[3 * r + c] = A[c]; R[3 * (n - r) + c] = A[3 * (n - r) + c]; }
+    double ta[N + 1], tb[N + 1], tc[N + 1];
+#pragma unroll
+    for (int i = 0; i <= N; ++i) { ta[i] = a[i]; tb[i] = b[i]; tc[i] = c[i]; }
+    // after round r, entry 0 is the left half's point r, entry N-r the right half's
+#pragma unroll
+    for (int r = 1; r <= N; ++r) {
+#pragma unroll
+      for (int j = 0; j <= N - r; ++j) {
+        ta[j] = 0.5 * (ta[j] + ta[j + 1]);
+        tb[j] = 0.5 * (tb[j] + tb[j + 1]);
+        tc[j] = 0.5 * (tc[j] + tc[j + 1]);
+      }
+      if (right) {
+        a[N - r] = ta[N - r]; b[N - r] = tb[N - r]; c[N - r] = tc[N - r];
+      } else {
+        a[r] = ta[0]; b[r] = tb[0]; c[r] = tc[0];
+      }
     }
-    for (int i = 0; i < 3 * (n + 1); ++i) A[i] = right ? R[i] : L[i];
   }
 }
 
-__global__ void k_prep(int32_t n_segs, const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
-                       const double *__restrict__ ctrl, const double *__restrict__ w,
-                       SegPrep *__restrict__ prep, uint8_t *__restrict__ serr) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_segs) return;
-  const int n = deg[s];
-  const int o = coff[s];
-  double H[18], A[18];
+// One thread per (segment, piece): piece q in 0..7 writes Bq[q] (the bound of
+// [q/8,(q+1)/8] in t-units, not yet clipped by B: k_emit takes the min), the
+// "piece" 8 writes B and S0 and the error flag.  Thread index = piece * n_segs
+// + segment, so a warp shares its piece (divergence only by degree).
+template <int N>
+__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o, int q,
+                                       SegPrep *__restrict__ out, uint8_t *__restrict__ err_out) {
+  double X[N + 1], Y[N + 1], W[N + 1];
   bool err = false;
   double lpoly = 0.0;
-  for (int j = 0; j <= n; ++j) {
+#pragma unroll
+  for (int j = 0; j <= N; ++j) {
     const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
     err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
-    H[3 * j] = wj * x; H[3 * j + 1] = wj * y; H[3 * j + 2] = wj;
+    X[j] = wj * x; Y[j] = wj * y; W[j] = wj;
     if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
   }
-  SegPrep *out = prep + s;
-  if (err) {
-    out->B = out->S0 = 0.0;
-    for (int q = 0; q < 8; ++q) out->Bq[q] = 0.0;
-  } else {
-    const double B = fmin(floater_bound(n, H), hodo_bound(n, H));
+  if (q == 8) {
+    *err_out = err ? 1 : 0;
+    if (err) { out->B = out->S0 = 0.0; return; }
+    const double B = fmin(floater_bound<N>(X, Y, W), hodo_bound<N>(X, Y, W));
     out->B = B;
     out->S0 = fmin(B, lpoly);
-    for (int q = 0; q < 8; ++q) {
-      dyadic_piece(n, H, q, A);
-      out->Bq[q] = fmin(B, 8.0 * fmin(floater_bound(n, A), hodo_bound(n, A)));
-    }
+    return;
   }
-  serr[s] = err ? 1 : 0;
+  if (err) { out->Bq[q] = 0.0; return; }
+  double a[N + 1], b[N + 1], c[N + 1];
+  dyadic_piece<N>(X, Y, W, q, a, b, c);
+  out->Bq[q] = 8.0 * hodo_bound<N>(a, b, c);
+}
+
+__global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
+                                              const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
+                                              const double *__restrict__ w, SegPrep *__restrict__ prep,
+                                              uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= 9 * (int64_t)n_segs) return;
+  const int q = (int)(idx / n_segs);
+  const int s = order ? order[idx % n_segs] : (int)(idx % n_segs);   // degree-sorted: warp-uniform N
+  const int o = coff[s];
+  switch (deg[s]) {
+    case 1: prep_n<1>(ctrl, w, o, q, prep + s, serr + s); break;
+    case 2: prep_n<2>(ctrl, w, o, q, prep + s, serr + s); break;
+    case 3: prep_n<3>(ctrl, w, o, q, prep + s, serr + s); break;
+    case 4: prep_n<4>(ctrl, w, o, q, prep + s, serr + s); break;
+    default: prep_n<5>(ctrl, w, o, q, prep + s, serr + s); break;
+  }
+}
+
+__global__ void k_iota(int32_t n, int32_t *__restrict__ a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
 }
 
 __global__ void k_loop_face(int32_t n_faces, const int32_t *__restrict__ face_off, int32_t *__restrict__ loop_face) {
@@ -383,7 +429,7 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
     C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
     C.B = Br;
     for (int q = 0; q < 8; ++q) {
-      const double bq = (dbg_flags & 1 ? bp.B : bp.Bq[q]) * (1.0 + rel);
+      const double bq = (dbg_flags & 1 ? bp.B : fmin(bp.B, bp.Bq[q])) * (1.0 + rel);
       C.Bq[q] = (sizeof(R) == 4) ? (R)f_up(bq) : (R)bq;
     }
     C.M = (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M;
@@ -548,11 +594,11 @@ struct DevBuf {
   std::vector<void *> ptrs;
   cudaStream_t st = 0;
   ~DevBuf() {
-    for (void *p : ptrs) cudaFreeAsync(p, st);
+    for (void *p : ptrs) cache_free(p, st);
   }
   template <typename T>
   cudaError_t alloc(T **p, size_t count) {
-    cudaError_t e = cudaMallocAsync((void **)p, sizeof(T) * (count ? count : 1), st);
+    cudaError_t e = cache_alloc((void **)p, sizeof(T) * (count ? count : 1), st);
     if (e == cudaSuccess) ptrs.push_back(*p);
     return e;
   }
@@ -565,7 +611,7 @@ void free_handle(wn_faces_t F) {
   void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
                 F->face_per, F->face_ok, F->face_M, F->counters};
   for (void *p : ps)
-    if (p) cudaFreeAsync(p, 0);
+    if (p) cache_free(p, 0);
   delete F;
 }
 
@@ -594,16 +640,16 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   F->n_seg = plan.colds;
   F->n_lines = plan.n_lines;
   F->n_groups = plan.n_cull;
-  WN_CUDA(cudaMallocAsync((void **)&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_rec_off, sizeof(int32_t) * (nf + 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_cold_off, sizeof(int32_t) * (nf + 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_order, sizeof(int32_t) * std::max(nf, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_dom, sizeof(double) * 4 * std::max(nf, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_per, std::max(nf, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_ok, std::max(nf, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
-  WN_CUDA(cudaMallocAsync((void **)&F->counters, 8 * sizeof(unsigned long long), st));
+  WN_CUDA(cache_alloc((void **)&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_rec_off, sizeof(int32_t) * (nf + 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_cold_off, sizeof(int32_t) * (nf + 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_order, sizeof(int32_t) * std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_dom, sizeof(double) * 4 * std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_per, std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_ok, std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->counters, 8 * sizeof(unsigned long long), st));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
   std::vector<int32_t> order(nf);
   std::iota(order.begin(), order.end(), 0);
@@ -626,7 +672,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   const int ng = (int)plan.groups.size();
   if (ng) {
     PlanGroup *dg = nullptr;
-    WN_CUDA(cudaMallocAsync((void **)&dg, sizeof(PlanGroup) * ng, st));
+    WN_CUDA(cache_alloc((void **)&dg, sizeof(PlanGroup) * ng, st));
     WN_CUDA(cudaMemcpyAsync(dg, plan.groups.data(), sizeof(PlanGroup) * ng, cudaMemcpyHostToDevice, st));
     const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
     ++g_build_launches;
@@ -634,7 +680,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
                                                  B.w, B.prep, B.shift, B.brk, B.info, rel, (Hot<R> *)F->hot,
                                                  (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());
-    WN_CUDA(cudaFreeAsync(dg, st));
+    cache_free(dg, st);
   }
   return WN_OK;
 }
@@ -729,6 +775,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     }
   }
   // --- K1 prep, loop->face, K2a lift ---
+  tr.mark("host checks");
   uint8_t *d_serr = nullptr;
   WN_CUDA(D.alloc(&B.prep, n_segs));
   WN_CUDA(D.alloc(&d_serr, n_segs));
@@ -737,12 +784,31 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(D.alloc(&B.brk, n_segs));
   WN_CUDA(D.alloc(&B.info, n_loops));
   g_build_launches += (n_segs ? 1 : 0) + (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
-  if (n_segs) k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr);
+  // segments sorted by degree so that k_prep's warps run one degree variant
+  int32_t *d_order = nullptr;
+  if (n_segs) {
+    int32_t *d_iota = nullptr, *d_degs = nullptr;
+    WN_CUDA(D.alloc(&d_iota, n_segs));
+    WN_CUDA(D.alloc(&d_order, n_segs));
+    WN_CUDA(D.alloc(&d_degs, n_segs));
+    k_iota<<<(n_segs + 255) / 256, 256, 0, st>>>(n_segs, d_iota);
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
+    char *dt = nullptr;
+    WN_CUDA(D.alloc(&dt, tmp));
+    cub::DeviceRadixSort::SortPairs(dt, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
+    g_build_launches += 4;
+  }
+  tr.mark("alloc calls (host)");
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) alloc + degree sort"); }
+  if (n_segs) k_prep<<<(int)((9 * (int64_t)n_segs + 127) / 128), 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep"); }
   if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, face_loop_off, B.loop_face);
   if (n_loops)
     k_lift<<<(n_loops + 127) / 128, 128, 0, st>>>(n_loops, loop_seg_off, B.loop_face, face_periodic, face_domain,
                                                  seg_degree, B.coff, ctrl_uv, d_serr, B.shift, B.brk, B.info);
   WN_CUDA(cudaGetLastError());
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
   std::vector<LoopInfo> L(n_loops);
   if (n_loops) WN_CUDA(cudaMemcpyAsync(L.data(), B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
@@ -1041,7 +1107,7 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
   WN_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
   if (h_bad) { set_error("wn_segment_prep: segment degree outside 1..5"); return WN_ERR_ARG; }
-  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, (SegPrep *)out, serr);
+  k_prep<<<(int)((9 * (int64_t)n_segs + 127) / 128), 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, (SegPrep *)out, serr, nullptr);
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaStreamSynchronize(st));
   return WN_OK;

@@ -204,6 +204,9 @@ struct wn_faces_s {
 
 namespace wn {
 void ensure_pool(int dev);
+cudaError_t cache_alloc(void **out, size_t bytes, cudaStream_t st);
+void cache_free(void *p, cudaStream_t st);
+void cache_trim();
 void set_error(const char *fmt, ...);
 wn_status_t cuda_fail(cudaError_t e, const char *what);
 }  // namespace wn

@@ -811,7 +811,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const size_t o_hq = carve(sizeof(HardEntry) * (size_t)hq_cap);
   const size_t o_tmp = carve(tmp);
   char *base = nullptr;
-  WN_CUDA(cudaMallocAsync((void **)&base, need, st));
+  WN_CUDA(cache_alloc((void **)&base, need, st));
   int32_t *cnt = (int32_t *)(base + o_cnt), *off = (int32_t *)(base + o_off);
   int32_t *cur = (int32_t *)(base + o_cur), *nt = (int32_t *)(base + o_nt);
   int32_t *toff = (int32_t *)(base + o_toff), *flags = (int32_t *)(base + o_flags);
@@ -888,7 +888,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     F->k3_events.push_back({e0, e1});
   }
   WN_CUDA(cudaGetLastError());
-  WN_CUDA(cudaFreeAsync(base, st));
+  cache_free(base, st);
   g_launches = launches;
   return WN_OK;
 }

@@ -9,73 +9,124 @@ __constant__ double c_binom[11][11] = {
     {1, 7, 21, 35, 35, 21, 7, 1}, {1, 8, 28, 56, 70, 56, 28, 8, 1}, {1, 9, 36, 84, 126, 126, 84, 36, 9, 1},
     {1, 10, 45, 120, 210, 252, 210, 120, 45, 10, 1}};
 
-// Bounds on flat homogeneous control points H[3i+0..2] = (w x, w y, w), i = 0..n.
-// Written without local aggregates (nvcc 12.9 -O3 miscompiled an earlier
-// array-accumulating version on sm_100a; scripts/dev/kp.cu reproduces it).
-// Hodograph-numerator Bernstein bound: max_k |D_k| / min_k E_k with
-//   D_k = sum_{i+j=k} C(n-1,i)C(n,j)/C(2n-1,k) w_j (w_{i+1}(P_{i+1}-P_j) - w_i(P_i-P_j)),
-//   E_k = sum_{i+j=k} C(n,i)C(n,j)/C(2n,k) w_i w_j.
-__device__ __noinline__ double hodo_bound(int n, const double *H) {
+// Bounds on homogeneous control points (X_i, Y_i, W_i) = w_i (x_i, y_i, 1),
+// i = 0..N, held in registers (templated on the degree, fully unrolled).
+// Written without accumulating into local arrays (an earlier version of that
+// shape was miscompiled by nvcc 12.9 -O3 on sm_100a: scripts/dev/kp.cu).
+//
+// Hodograph-numerator Bernstein bound: |gamma'| = |X'W - XW'| / W^2 with
+//   X'W - XW' = N sum_k D_k B_k^{2N-1},
+//   D_k = sum_{i+j=k} C(N-1,i)C(N,j)/C(2N-1,k) [W_j (X_{i+1}-X_i) - (W_{i+1}-W_i) X_j],
+//   W^2 = sum_k E_k B_k^{2N},  E_k = sum_{i+j=k} C(N,i)C(N,j)/C(2N,k) W_i W_j,
+// so |gamma'| <= N max_k |D_k| / min_k E_k (convex-hull property).
+template <int N>
+__device__ __forceinline__ double hodo_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                             const double (&W)[N + 1]) {
   double dmax = 0.0, emin = INFINITY;
-  for (int k = 0; k <= 2 * n - 1; ++k) {
+#pragma unroll
+  for (int k = 0; k <= 2 * N - 1; ++k) {
     double dx = 0.0, dy = 0.0;
-    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n - 1 ? k : n - 1;
-    for (int i = i0; i <= i1; ++i) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
       const int j = k - i;
-      const double wi = H[3 * i + 2], wi1 = H[3 * i + 5], wj = H[3 * j + 2];
-      const double xi = H[3 * i] / wi, yi = H[3 * i + 1] / wi;
-      const double xi1 = H[3 * i + 3] / wi1, yi1 = H[3 * i + 4] / wi1;
-      const double xj = H[3 * j] / wj, yj = H[3 * j + 1] / wj;
-      const double c = c_binom[n - 1][i] * c_binom[n][j] / c_binom[2 * n - 1][k] * wj;
-      dx += c * (wi1 * (xi1 - xj) - wi * (xi - xj));
-      dy += c * (wi1 * (yi1 - yj) - wi * (yi - yj));
+      if (j < 0 || j > N) continue;
+      const double c = c_binom[N - 1][i] * c_binom[N][j] / c_binom[2 * N - 1][k];
+      dx += c * (W[j] * (X[i + 1] - X[i]) - (W[i + 1] - W[i]) * X[j]);
+      dy += c * (W[j] * (Y[i + 1] - Y[i]) - (W[i + 1] - W[i]) * Y[j]);
     }
     dmax = fmax(dmax, hypot(dx, dy));
   }
-  for (int k = 0; k <= 2 * n; ++k) {
+#pragma unroll
+  for (int k = 0; k <= 2 * N; ++k) {
     double e = 0.0;
-    const int i0 = k - n > 0 ? k - n : 0, i1 = k < n ? k : n;
-    for (int i = i0; i <= i1; ++i) {
+#pragma unroll
+    for (int i = 0; i <= N; ++i) {
       const int j = k - i;
-      e += c_binom[n][i] * c_binom[n][j] / c_binom[2 * n][k] * H[3 * i + 2] * H[3 * j + 2];
+      if (j < 0 || j > N) continue;
+      e += c_binom[N][i] * c_binom[N][j] / c_binom[2 * N][k] * W[i] * W[j];
     }
     emin = fmin(emin, e);
   }
-  return n * dmax / emin;
+  return N * dmax / emin;
 }
 
-__device__ __noinline__ double floater_bound(int n, const double *H) {
-  double wmax = H[2], wmin = H[2], dmax = 0.0, diam = 0.0;
-  for (int i = 1; i <= n; ++i) { wmax = fmax(wmax, H[3 * i + 2]); wmin = fmin(wmin, H[3 * i + 2]); }
-  for (int i = 0; i <= n; ++i)
-    for (int j = i + 1; j <= n; ++j) {
-      const double l = hypot(H[3 * j] / H[3 * j + 2] - H[3 * i] / H[3 * i + 2],
-                             H[3 * j + 1] / H[3 * j + 2] - H[3 * i + 1] / H[3 * i + 2]);
+template <int N>
+__device__ __forceinline__ double floater_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                                const double (&W)[N + 1]) {
+  double wmax = W[0], wmin = W[0], dmax = 0.0, diam = 0.0;
+#pragma unroll
+  for (int i = 1; i <= N; ++i) { wmax = fmax(wmax, W[i]); wmin = fmin(wmin, W[i]); }
+#pragma unroll
+  for (int i = 0; i <= N; ++i)
+#pragma unroll
+    for (int j = i + 1; j <= N; ++j) {
+      const double l = hypot(X[j] / W[j] - X[i] / W[i], Y[j] / W[j] - Y[i] / W[i]);
       diam = fmax(diam, l);
       if (j == i + 1) dmax = fmax(dmax, l);
     }
-  if (wmax == wmin) return n * dmax;
+  if (wmax == wmin) return N * dmax;
   const double r = wmax / wmin;
-  return fmin(n * r * diam, n * r * r * dmax);
+  return fmin(N * r * diam, N * r * r * dmax);
 }
 
-// Homogeneous control points of the dyadic piece [q/8, (q+1)/8] of H (blossom-
-// free: three de Casteljau halvings, choosing the half along the bits of q).
-// A receives 3(n+1) values; works in place in A.
-__device__ __noinline__ void dyadic_piece(int n, const double *H, int q, double *A) {
-  for (int i = 0; i < 3 * (n + 1); ++i) A[i] = H[i];
+// piece [q/8,(q+1)/8]: three de Casteljau halvings along the bits of q
+template <int N>
+__device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const double (&Y)[N + 1],
+                                             const double (&W)[N + 1], int q, double (&a)[N + 1],
+                                             double (&b)[N + 1], double (&c)[N + 1]) {
+#pragma unroll
+  for (int i = 0; i <= N; ++i) { a[i] = X[i]; b[i] = Y[i]; c[i] = W[i]; }
+#pragma unroll
   for (int lvl = 2; lvl >= 0; --lvl) {
     const bool right = (q >> lvl) & 1;
-    // after r rounds of midpoint averaging, entry 0 is the left half's point r
-    // and entry n-r the right half's point n-r; keep the requested half
-    double L[18], R[18];
-    for (int c = 0; c < 3; ++c) { L[c] = A[c]; R[3 * n + c] = A[3 * n + c]; }
-    for (int r = 1; r <= n; ++r) {
-      for (int j = 0; j <= n - r; ++j)
-        for (int c = 0; c < 3; ++c) A[3 * j + c] = 0.5 * (A[3 * j + c] + A[3 * j + 3 + c]);
-      for (int c = 0; c < 3; ++c) { L[3 * r + c] = A[c]; R[3 * (n - r) + c] = A[3 * (n - r) + c]; }
+    double ta[N + 1], tb[N + 1], tc[N + 1];
+#pragma unroll
+    for (int i = 0; i <= N; ++i) { ta[i] = a[i]; tb[i] = b[i]; tc[i] = c[i]; }
+    // after round r, entry 0 is the left half's point r, entry N-r the right half's
+#pragma unroll
+    for (int r = 1; r <= N; ++r) {
+#pragma unroll
+      for (int j = 0; j <= N - r; ++j) {
+        ta[j] = 0.5 * (ta[j] + ta[j + 1]);
+        tb[j] = 0.5 * (tb[j] + tb[j + 1]);
+        tc[j] = 0.5 * (tc[j] + tc[j + 1]);
+      }
+      if (right) {
+        a[N - r] = ta[N - r]; b[N - r] = tb[N - r]; c[N - r] = tc[N - r];
+      } else {
+        a[r] = ta[0]; b[r] = tb[0]; c[r] = tc[0];
+      }
     }
-    for (int i = 0; i < 3 * (n + 1); ++i) A[i] = right ? R[i] : L[i];
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o,
+                                       SegPrep *__restrict__ out, uint8_t *__restrict__ err_out) {
+  double X[N + 1], Y[N + 1], W[N + 1];
+  bool err = false;
+  double lpoly = 0.0;
+#pragma unroll
+  for (int j = 0; j <= N; ++j) {
+    const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
+    err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
+    X[j] = wj * x; Y[j] = wj * y; W[j] = wj;
+    if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
+  }
+  *err_out = err ? 1 : 0;
+  if (err) {
+    out->B = out->S0 = 0.0;
+    for (int q = 0; q < 8; ++q) out->Bq[q] = 0.0;
+    return;
+  }
+  const double B = fmin(floater_bound<N>(X, Y, W), hodo_bound<N>(X, Y, W));
+  out->B = B;
+  out->S0 = fmin(B, lpoly);
+#pragma unroll 1
+  for (int q = 0; q < 8; ++q) {
+    double a[N + 1], b[N + 1], c[N + 1];
+    dyadic_piece<N>(X, Y, W, q, a, b, c);
+    out->Bq[q] = fmin(B, 8.0 * hodo_bound<N>(a, b, c));
   }
 }
 
@@ -84,31 +135,14 @@ __global__ void k_prep(int32_t n_segs, const int32_t *__restrict__ deg, const in
                        SegPrep *__restrict__ prep, uint8_t *__restrict__ serr) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_segs) return;
-  const int n = deg[s];
   const int o = coff[s];
-  double H[18], A[18];
-  bool err = false;
-  double lpoly = 0.0;
-  for (int j = 0; j <= n; ++j) {
-    const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
-    err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
-    H[3 * j] = wj * x; H[3 * j + 1] = wj * y; H[3 * j + 2] = wj;
-    if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
+  switch (deg[s]) {
+    case 1: prep_n<1>(ctrl, w, o, prep + s, serr + s); break;
+    case 2: prep_n<2>(ctrl, w, o, prep + s, serr + s); break;
+    case 3: prep_n<3>(ctrl, w, o, prep + s, serr + s); break;
+    case 4: prep_n<4>(ctrl, w, o, prep + s, serr + s); break;
+    default: prep_n<5>(ctrl, w, o, prep + s, serr + s); break;
   }
-  SegPrep *out = prep + s;
-  if (err) {
-    out->B = out->S0 = 0.0;
-    for (int q = 0; q < 8; ++q) out->Bq[q] = 0.0;
-  } else {
-    const double B = fmin(floater_bound(n, H), hodo_bound(n, H));
-    out->B = B;
-    out->S0 = fmin(B, lpoly);
-    for (int q = 0; q < 8; ++q) {
-      dyadic_piece(n, H, q, A);
-      out->Bq[q] = fmin(B, 8.0 * fmin(floater_bound(n, A), hodo_bound(n, A)));
-    }
-  }
-  serr[s] = err ? 1 : 0;
 }
 
 int main(){

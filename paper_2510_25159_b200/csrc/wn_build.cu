@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <vector>
 
@@ -361,8 +362,10 @@ __device__ __forceinline__ double binom5(int n, int j) {
   return tab[n][j];
 }
 
+// one warp per planned group; lanes take the group's segments in parallel
 template <typename R>
-__global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, const int32_t *__restrict__ loop_off,
+__global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
+                       const int32_t *__restrict__ loop_off,
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
                        const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
@@ -370,7 +373,8 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
                        Cold<R> *__restrict__ cold, int dbg_flags) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (g >= n_groups) return;
   const PlanGroup G = groups[g];
   const int l = G.loop;
@@ -384,26 +388,37 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
   auto Y = [&](double y, int ks) { return pv ? lat(lat(y, ks, Tv), G.kv, Tv) : y; };
   auto TX = [&](double x) { return pu ? lat(x, G.ku, Tu) : x; };
   auto TY = [&](double y) { return pv ? lat(y, G.kv, Tv) : y; };
-  int r = G.rec_off;
   if (G.kind == G_LINE) {
     // omega(p, L) for the line through beta_0 along the extension vector (Eq. 5)
-    const double bx = TX(I.sx), by = TY(I.sy);
-    uint32_t meta = K_LINE;
-    double c;
-    if (I.cu != 0) { c = by; if (I.cu > 0) meta |= F_GE; }          // v = (+-T,0): left iff p.v >=/<= c
-    else { c = bx; meta |= F_AXISV; if (I.cv < 0) meta |= F_GE; }   // v = (0,+-T): left iff p.u <=/>= c
-    put_rec<R>(hot, r, c, 0.0, 0.0, meta);
+    if (lane == 0) {
+      const double bx = TX(I.sx), by = TY(I.sy);
+      uint32_t meta = K_LINE;
+      double c;
+      if (I.cu != 0) { c = by; if (I.cu > 0) meta |= F_GE; }          // v = (+-T,0): left iff p.v >=/<= c
+      else { c = bx; meta |= F_AXISV; if (I.cv < 0) meta |= F_GE; }   // v = (0,+-T): left iff p.u <=/>= c
+      put_rec<R>(hot, G.rec_off, c, 0.0, 0.0, meta);
+    }
     return;
   }
-  if (G.flags & PF_CULL) {
+  const int cull = (G.flags & PF_CULL) ? 1 : 0;
+  if (cull && lane == 0) {
     const double xmin = TX(I.bb[0]) - G.M, xmax = TX(I.bb[2]) + G.M;
     const double ymin = TY(I.bb[1]) - G.M, ymax = TY(I.bb[3]) + G.M;
-    put_group<R>(hot, r++, xmin, ymin, xmax, ymax, K_GROUP | ((uint32_t)(G.nrec - 1) << 8));
+    put_group<R>(hot, G.rec_off, xmin, ymin, xmax, ymax, K_GROUP | ((uint32_t)(G.nrec - 1) << 8));
   }
   const int s0 = loop_off[l], s1 = loop_off[l + 1];
-  int cl = G.cold_local;
-  int cg = G.cold_off;
-  for (int s = s0; s < s1; ++s) {
+  const int r_first = G.rec_off + cull + 1;              // SEG(s0) follows GROUP? and MOVE
+  int carry = 0;                                         // breaks before this chunk
+  for (int base = s0; base < s1; base += 32) {
+    const int s = base + lane;
+    const bool in = s < s1;
+    const bool bk = in && s > s0 && brk[s];
+    const unsigned bm = __ballot_sync(0xffffffffu, bk);
+    const int nb = carry + __popc(bm & ((2u << lane) - 1u));   // breaks in (s0, s]
+    carry += __popc(bm);
+    if (!in) continue;
+    const int idx = s - s0;
+    const int r = r_first + idx + nb;
     const int n = deg[s];
     const int o = coff[s];
     const int2 k = shift[s];
@@ -412,19 +427,18 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
       px[j] = X(ctrl[2 * (o + j)], k.x);
       py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
     }
-    if (s == s0) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVE | fa);
-    else if (brk[s]) put_rec<R>(hot, r++, px[0], py[0], 0.0, K_MOVEG | fa);
+    if (s == s0) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVE | fa);
+    else if (bk) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVEG | fa);
     const SegPrep &bp = prep[s];
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
-    // see k_query; fp32 records: S0 (1 + 2^-17) + M32.  Eq. 2 uses B (cold).
-    // fp64 records: the fp32 filter span; its (1 - 2^-18) error shrink is folded
-    // in as a further factor (1 + 2^-17)
+    // and the filter's (1 - 2^-18) error shrink folded in as a further
+    // (1 + 2^-17); fp32 records: S0 (1 + 2^-17) + M32.
     const double S0 = (sizeof(R) == 8) ? (bp.S0 * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17)
                                        : bp.S0 * (1.0 + rel) + G.M;
     const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
-    put_rec<R>(hot, r++, px[n], py[n], S0, K_SEG | fa | ((uint32_t)cl << 8));
+    put_rec<R>(hot, r, px[n], py[n], S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
     Cold<R> C;
     C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
     C.B = Br;
@@ -446,13 +460,14 @@ __global__ void k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups, c
         C.cx[j] = C.cy[j] = C.cw[j] = (R)0;
       }
     }
-    cold[cg] = C;
-    ++cl;
-    ++cg;
+    cold[G.cold_off + idx] = C;
   }
-  if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
-  if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
-  if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
+  if (lane == 0) {
+    int r = r_first + (s1 - s0) + carry;
+    if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
+    if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
+    if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -462,6 +477,7 @@ struct Plan {
   std::vector<PlanGroup> groups;
   std::vector<int32_t> rec_off;   // per target face + 1
   std::vector<int32_t> cold_off;
+  void reserve(size_t ng, size_t nf) { groups.reserve(ng); rec_off.reserve(nf + 1); cold_off.reserve(nf + 1); }
   int64_t n_lines = 0, n_cull = 0;
   int32_t recs = 0, colds = 0;
   int32_t face_rec0 = 0, face_cold0 = 0;
@@ -575,7 +591,7 @@ static void plan_extended_copies(Plan &P, int l, const LoopInfo &I, const FaceCt
   }
 }
 
-static double face_margin(const std::vector<LoopInfo> &L, int l0, int l1, const FaceCtx &C, bool fp32) {
+static double face_margin(const LoopInfo *L, int l0, int l1, const FaceCtx &C, bool fp32) {
   double s = 1.0 + std::fabs(C.u0) + std::fabs(C.v0) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0);
   for (int l = l0; l < l1; ++l)
     for (int k = 0; k < 4; ++k) s = std::max(s, 1.0 + std::fabs(L[l].bb[k]) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0));
@@ -587,9 +603,41 @@ static double face_margin(const std::vector<LoopInfo> &L, int l0, int l1, const 
 using namespace wn;
 
 // ---------------------------------------------------------------------------
-// device buffers helper
+// pinned host staging (build-time transfers) and device buffers helper
 // ---------------------------------------------------------------------------
 namespace {
+// Bump allocator over pinned host blocks; reset at the start of every build
+// (each build ends with a stream synchronisation, so no copy is in flight).
+struct PinnedArena {
+  std::vector<std::pair<char *, size_t>> blocks;
+  size_t blk = 0, off = 0;
+  void reset() { blk = 0; off = 0; }
+  void *get(size_t bytes) {
+    bytes = (bytes + 255) & ~(size_t)255;
+    while (blk < blocks.size() && off + bytes > blocks[blk].second) { ++blk; off = 0; }
+    if (blk == blocks.size()) {
+      size_t sz = std::max(bytes, (size_t)64 << 20);
+      char *p = nullptr;
+      if (cudaMallocHost((void **)&p, sz) != cudaSuccess) return nullptr;
+      blocks.push_back({p, sz});
+      off = 0;
+    }
+    void *r = blocks[blk].first + off;
+    off += bytes;
+    return r;
+  }
+};
+PinnedArena g_pin;
+std::mutex g_build_mu;
+
+cudaError_t h2d(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return cudaSuccess;
+  void *s = g_pin.get(bytes);
+  if (!s) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+  memcpy(s, src, bytes);
+  return cudaMemcpyAsync(dst, s, bytes, cudaMemcpyHostToDevice, st);
+}
+
 struct DevBuf {
   std::vector<void *> ptrs;
   cudaStream_t st = 0;
@@ -660,23 +708,23 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     return (plan.rec_off[a + 1] - plan.rec_off[a]) > (plan.rec_off[b + 1] - plan.rec_off[b]);
   });
   std::vector<uint8_t> ok(nf, 1);
-  WN_CUDA(cudaMemcpyAsync(F->face_rec_off, plan.rec_off.data(), sizeof(int32_t) * (nf + 1), cudaMemcpyHostToDevice, st));
-  WN_CUDA(cudaMemcpyAsync(F->face_cold_off, plan.cold_off.data(), sizeof(int32_t) * (nf + 1), cudaMemcpyHostToDevice, st));
+  WN_CUDA(h2d(F->face_rec_off, plan.rec_off.data(), sizeof(int32_t) * (nf + 1), st));
+  WN_CUDA(h2d(F->face_cold_off, plan.cold_off.data(), sizeof(int32_t) * (nf + 1), st));
   if (nf) {
-    WN_CUDA(cudaMemcpyAsync(F->face_order, order.data(), sizeof(int32_t) * nf, cudaMemcpyHostToDevice, st));
-    WN_CUDA(cudaMemcpyAsync(F->face_dom, fdom.data(), sizeof(double) * 4 * nf, cudaMemcpyHostToDevice, st));
-    WN_CUDA(cudaMemcpyAsync(F->face_per, fper.data(), nf, cudaMemcpyHostToDevice, st));
-    WN_CUDA(cudaMemcpyAsync(F->face_ok, ok.data(), nf, cudaMemcpyHostToDevice, st));
-    WN_CUDA(cudaMemcpyAsync(F->face_M, fM.data(), sizeof(double) * nf, cudaMemcpyHostToDevice, st));
+    WN_CUDA(h2d(F->face_order, order.data(), sizeof(int32_t) * nf, st));
+    WN_CUDA(h2d(F->face_dom, fdom.data(), sizeof(double) * 4 * nf, st));
+    WN_CUDA(h2d(F->face_per, fper.data(), nf, st));
+    WN_CUDA(h2d(F->face_ok, ok.data(), nf, st));
+    WN_CUDA(h2d(F->face_M, fM.data(), sizeof(double) * nf, st));
   }
   const int ng = (int)plan.groups.size();
   if (ng) {
     PlanGroup *dg = nullptr;
     WN_CUDA(cache_alloc((void **)&dg, sizeof(PlanGroup) * ng, st));
-    WN_CUDA(cudaMemcpyAsync(dg, plan.groups.data(), sizeof(PlanGroup) * ng, cudaMemcpyHostToDevice, st));
+    WN_CUDA(h2d(dg, plan.groups.data(), sizeof(PlanGroup) * ng, st));
     const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
     ++g_build_launches;
-    k_emit<R><<<(ng + 127) / 128, 128, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
+    k_emit<R><<<(int)((32 * (int64_t)ng + 255) / 256), 256, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
                                                  B.w, B.prep, B.shift, B.brk, B.info, rel, (Hot<R> *)F->hot,
                                                  (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());
@@ -695,6 +743,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
                                       int32_t *face_status) {
   set_error("");
   g_build_launches = 0;
+  std::lock_guard<std::mutex> build_lock(g_build_mu);
+  g_pin.reset();
   if (!out) { set_error("wn_build_faces: out == NULL"); return WN_ERR_ARG; }
   if (n_faces < 0 || n_loops < 0 || n_segs < 0) { set_error("wn_build_faces: negative count"); return WN_ERR_ARG; }
   if (!loop_seg_off || !face_loop_off || (n_faces > 0 && (!face_periodic || !face_domain)) ||
@@ -809,8 +859,9 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
                                                  seg_degree, B.coff, ctrl_uv, d_serr, B.shift, B.brk, B.info);
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
-  std::vector<LoopInfo> L(n_loops);
-  if (n_loops) WN_CUDA(cudaMemcpyAsync(L.data(), B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
+  LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
+  if (!L) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
+  if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
   tr.mark("prep + lift + info d2h");
 
@@ -988,7 +1039,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
   }
   if (face_status && n_faces)
-    WN_CUDA(cudaMemcpyAsync(face_status, status.data(), sizeof(int32_t) * n_faces, cudaMemcpyHostToDevice, st));
+    WN_CUDA(h2d(face_status, status.data(), sizeof(int32_t) * n_faces, st));
   if (any_bad) {
     WN_CUDA(cudaStreamSynchronize(st));
     int first = 0;
@@ -1002,6 +1053,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   tr.mark("validate + pairing");
   // --- final plan ---
   Plan P;
+  P.reserve((size_t)n_loops * 2 + 16, (size_t)n_faces);
   std::vector<double> fdom(4 * (size_t)n_faces);
   for (int f = 0; f < n_faces; ++f) {
     const FaceCtx &C = ctx[f];

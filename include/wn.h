@@ -62,6 +62,8 @@ typedef struct {                 /* [host] */
                        1 = literal per-chord atan2 (the paper's WindingNumberLineSegment)     */
   int strict;       /* 1 = reject faces violating Prop. 1 (default); 0 = evaluate an
                        unbalanced uni-periodic loop set anyway (single extended curves)        */
+  int hierarchy;    /* 1 = path hierarchy over bit-continuous chains (span = sum of
+                       the segments' root spans; default), 0 = flat segment list              */
 } wn_options_t;
 
 /* Build the per-face records (segment prep K1, lifting K2a, copy emission K2c).

@@ -20,7 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libwn.so")
+_LIBPATH = os.environ.get("WN_LIB_OVERRIDE") or os.path.join(_HERE, "libwn.so")   # override: dev experiments only
 _lib = None
 
 WN_OK = 0
@@ -43,7 +43,7 @@ class WNError(RuntimeError):
 
 class Options(C.Structure):
     _fields_ = [("eps", C.c_double), ("max_depth", C.c_int), ("precision", C.c_int),
-                ("rule", C.c_int), ("angle_mode", C.c_int), ("strict", C.c_int)]
+                ("rule", C.c_int), ("angle_mode", C.c_int), ("strict", C.c_int), ("hierarchy", C.c_int)]
 
 
 class FacesInfo(C.Structure):
@@ -145,7 +145,7 @@ class Faces:
     @classmethod
     def build(cls, ctrl_uv, ctrl_w, seg_degree, loop_seg_off, face_loop_off, face_periodic,
               face_domain, eps=0.0, max_depth=0, precision=0, rule=0, angle_mode=0, strict=True,
-              device=None, stream=None):
+              hierarchy=True, device=None, stream=None):
         torch = _torch()
         L = load()
         if not torch.cuda.is_available():
@@ -160,7 +160,8 @@ class Faces:
         dom = _dev(face_domain, torch.float64, device).reshape(-1, 4)
         nf, nl, ns = flo.numel() - 1, lso.numel() - 1, deg.numel()
         status = torch.zeros(max(nf, 1), dtype=torch.int32, device=device)
-        opts = Options(float(eps), int(max_depth), int(precision), int(rule), int(angle_mode), int(bool(strict)))
+        opts = Options(float(eps), int(max_depth), int(precision), int(rule), int(angle_mode), int(bool(strict)),
+                       int(bool(hierarchy)))
         h = C.c_void_p()
         with torch.cuda.device(device):
             rc = L.wn_build_faces(nf, nl, ns, _ptr(ctrl), _ptr(w), _ptr(deg), _ptr(lso), _ptr(flo),

@@ -246,7 +246,8 @@ __global__ void k_lift(int32_t n_loops, const int32_t *__restrict__ loop_off, co
                        const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
                        const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
                        const double *__restrict__ ctrl, const uint8_t *__restrict__ serr,
-                       int2 *__restrict__ shift, uint8_t *__restrict__ brk, LoopInfo *__restrict__ info) {
+                       const SegPrep *__restrict__ prep, int2 *__restrict__ shift, uint8_t *__restrict__ brk,
+                       int2 *__restrict__ chain, double *__restrict__ s0pre, LoopInfo *__restrict__ info) {
   const int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= n_loops) return;
   const int f = loop_face[l];
@@ -282,6 +283,23 @@ __global__ void k_lift(int32_t n_loops, const int32_t *__restrict__ loop_off, co
       xmin = fmin(xmin, x); xmax = fmax(xmax, x);
       ymin = fmin(ymin, y); ymax = fmax(ymax, y);
       if (j == n) { ex = x; ey = y; }
+    }
+  }
+  // chains (maximal bit-continuous runs) and the prefix of root spans along the
+  // loop: the path-hierarchy bounds are built from them in k_emit
+  {
+    int cs = 0;
+    double acc = 0.0;
+    for (int s = s0; s < s1; ++s) {
+      if (s == s0 || brk[s]) cs = s - s0;
+      chain[s].x = cs;
+      acc += prep[s].S0;
+      s0pre[s] = acc;
+    }
+    int ce = s1 - s0 - 1;
+    for (int s = s1 - 1; s >= s0; --s) {
+      chain[s].y = ce - chain[s].x + 1;
+      if (s == s0 || brk[s]) ce = s - s0 - 1;
     }
   }
   LoopInfo I;
@@ -371,6 +389,7 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
                        const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
                        const double *__restrict__ wts, const SegPrep *__restrict__ prep,
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
+                       const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
                        Cold<R> *__restrict__ cold, int dbg_flags) {
   const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -407,7 +426,12 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
     put_group<R>(hot, G.rec_off, xmin, ymin, xmax, ymax, K_GROUP | ((uint32_t)(G.nrec - 1) << 8));
   }
   const int s0 = loop_off[l], s1 = loop_off[l + 1];
-  const int r_first = G.rec_off + cull + 1;              // SEG(s0) follows GROUP? and MOVE
+  const int r_first = G.rec_off + cull + 1;              // first record after GROUP? and MOVE
+  const bool tree = (G.flags & PF_TREE) != 0;
+  // fp64 records: spans of the conservative fp32 filter
+  auto filter_span = [&](double S) {
+    return (sizeof(R) == 8) ? (S * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17) : S * (1.0 + rel) + G.M;
+  };
   int carry = 0;                                         // breaks before this chunk
   for (int base = s0; base < s1; base += 32) {
     const int s = base + lane;
@@ -418,7 +442,6 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
     carry += __popc(bm);
     if (!in) continue;
     const int idx = s - s0;
-    const int r = r_first + idx + nb;
     const int n = deg[s];
     const int o = coff[s];
     const int2 k = shift[s];
@@ -427,15 +450,46 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
       px[j] = X(ctrl[2 * (o + j)], k.x);
       py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
     }
-    if (s == s0) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVE | fa);
-    else if (bk) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVEG | fa);
+    int r;
+    if (!tree) {
+      r = r_first + idx + nb;
+      if (s == s0) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVE | fa);
+      else if (bk) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVEG | fa);
+    } else {
+      // path hierarchy: each chain of m segments becomes a pre-order
+      // binary tree of 2m-1 records (SPAN nodes over segment ranges, SEG leaves);
+      // chain c starts at record r_first + 2 * (its first segment index)
+      const int2 ch = chain[s];                          // (chain start idx, chain length)
+      const int j = idx - ch.x;
+      int a = 0, bnd = ch.y - 1, off = r_first + 2 * ch.x;
+      if (j == 0) {
+        if (s == s0) put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVE | fa);
+        else put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVEG | fa);
+      }
+      while (a < bnd) {
+        const int mid = (a + bnd) >> 1;
+        if (j == a) {
+          // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
+          const int se = s0 + ch.x + bnd;                // last segment of the run
+          const int ne = deg[se], oe = coff[se];
+          const int2 ke = shift[se];
+          const double ex = X(ctrl[2 * (oe + ne)], ke.x), ey = Y(ctrl[2 * (oe + ne) + 1], ke.y);
+          const int sa = s0 + ch.x + a;
+          const double sum = s0pre[se] - (sa > s0 ? s0pre[sa - 1] : 0.0);
+          const int sub = 2 * (bnd - a + 1) - 2;          // records of the subtree after the SPAN
+          put_rec<R>(hot, off, ex, ey, filter_span(sum), K_SPAN | fa | ((uint32_t)sub << 8));
+        }
+        if (j <= mid) { bnd = mid; off += 1; }
+        else { off += 1 + (2 * (mid - a + 1) - 1); a = mid + 1; }
+      }
+      r = off;
+    }
     const SegPrep &bp = prep[s];
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // and the filter's (1 - 2^-18) error shrink folded in as a further
     // (1 + 2^-17); fp32 records: S0 (1 + 2^-17) + M32.
-    const double S0 = (sizeof(R) == 8) ? (bp.S0 * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17)
-                                       : bp.S0 * (1.0 + rel) + G.M;
+    const double S0 = filter_span(bp.S0);
     const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
     put_rec<R>(hot, r, px[n], py[n], S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
@@ -463,7 +517,7 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
     cold[G.cold_off + idx] = C;
   }
   if (lane == 0) {
-    int r = r_first + (s1 - s0) + carry;
+    int r = tree ? G.rec_off + cull + 2 * (s1 - s0) : r_first + (s1 - s0) + carry;
     if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
     if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
     if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
@@ -511,7 +565,8 @@ struct Plan {
       nrec = 1;
       ++n_lines;
     } else {
-      nrec = ((flags & PF_CULL) ? 1 : 0) + 1 + I.nseg + I.nbrk +
+      // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg
+      nrec = ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) +
              ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
       colds += I.nseg;
       if (flags & PF_CULL) ++n_cull;
@@ -545,8 +600,9 @@ struct FaceCtx {
 };
 
 // group flags for a closed / copy group
+static bool g_tree_opt = true;   // set per build from wn_options_t.hierarchy (under g_build_mu)
 static int loop_flags(const LoopInfo &I, bool angle, bool copy) {
-  int fl = angle ? PF_ANGLE : 0;
+  int fl = (angle ? PF_ANGLE : 0) | (g_tree_opt ? PF_TREE : 0);
   if (copy) {
     fl |= angle ? PF_TAIL_NCH : PF_TAIL_XCH;
     if (I.nbrk == 0) fl |= PF_CULL;
@@ -673,6 +729,8 @@ struct BuildCtx {
   SegPrep *prep;
   int2 *shift;
   uint8_t *brk;
+  int2 *chain;      // per segment: (chain start index within its loop, chain length)
+  double *s0pre;    // per segment: prefix sum of root spans S0 along its loop
   LoopInfo *info;
   cudaStream_t st;
 };
@@ -725,7 +783,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
     ++g_build_launches;
     k_emit<R><<<(int)((32 * (int64_t)ng + 255) / 256), 256, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
-                                                 B.w, B.prep, B.shift, B.brk, B.info, rel, (Hot<R> *)F->hot,
+                                                 B.w, B.prep, B.shift, B.brk, B.chain, B.s0pre, B.info, rel, (Hot<R> *)F->hot,
                                                  (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());
     cache_free(dg, st);
@@ -745,6 +803,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   g_build_launches = 0;
   std::lock_guard<std::mutex> build_lock(g_build_mu);
   g_pin.reset();
+  g_tree_opt = !opts || opts->hierarchy != 0;
   if (!out) { set_error("wn_build_faces: out == NULL"); return WN_ERR_ARG; }
   if (n_faces < 0 || n_loops < 0 || n_segs < 0) { set_error("wn_build_faces: negative count"); return WN_ERR_ARG; }
   if (!loop_seg_off || !face_loop_off || (n_faces > 0 && (!face_periodic || !face_domain)) ||
@@ -753,7 +812,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     return WN_ERR_ARG;
   }
   wn_options_t O;
-  O.eps = 0; O.max_depth = 0; O.precision = 0; O.rule = 0; O.angle_mode = 0; O.strict = 1;
+  O.eps = 0; O.max_depth = 0; O.precision = 0; O.rule = 0; O.angle_mode = 0; O.strict = 1; O.hierarchy = 1;
   if (opts) O = *opts;
   if (O.precision != 0 && O.precision != 1) { set_error("bad precision"); return WN_ERR_ARG; }
   if (O.rule != 0 && O.rule != 1) { set_error("bad rule"); return WN_ERR_ARG; }
@@ -763,6 +822,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   const double eps = O.eps > 0 ? O.eps : (fp32 ? 1e-6 : 1e-10);
   const int maxd = O.max_depth > 0 ? O.max_depth : 48;
   const bool angle = O.angle_mode == 1;
+  if (O.hierarchy != 0 && O.hierarchy != 1) { set_error("bad hierarchy option"); return WN_ERR_ARG; }
   int dev = 0;
   {
     cudaError_t e = cudaGetDevice(&dev);
@@ -832,6 +892,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(D.alloc(&B.loop_face, n_loops));
   WN_CUDA(D.alloc(&B.shift, n_segs));
   WN_CUDA(D.alloc(&B.brk, n_segs));
+  WN_CUDA(D.alloc(&B.chain, n_segs));
+  WN_CUDA(D.alloc(&B.s0pre, n_segs));
   WN_CUDA(D.alloc(&B.info, n_loops));
   g_build_launches += (n_segs ? 1 : 0) + (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
   // segments sorted by degree so that k_prep's warps run one degree variant
@@ -856,7 +918,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, face_loop_off, B.loop_face);
   if (n_loops)
     k_lift<<<(n_loops + 127) / 128, 128, 0, st>>>(n_loops, loop_seg_off, B.loop_face, face_periodic, face_domain,
-                                                 seg_degree, B.coff, ctrl_uv, d_serr, B.shift, B.brk, B.info);
+                                                 seg_degree, B.coff, ctrl_uv, d_serr, B.prep, B.shift, B.brk,
+                                                 B.chain, B.s0pre, B.info);
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
   LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));

@@ -30,7 +30,8 @@ enum : uint32_t {
   K_XCH = 6,     // extended copy closing (crossing mode): -c(A -> Z)
   K_NCH = 7,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
   K_CLOSEG = 8,  // open contractible loop: gap chord Z -> A (crossing mode)
-  K_PAD = 9      // second half of an fp32 GROUP header
+  K_PAD = 9,     // (unused)
+  K_SPAN = 10    // path-hierarchy node: (x,y) = end of the run, span = sum of its S0; aux = subtree records
 };
 constexpr uint32_t F_ANGLE = 1u << 4;   // literal atan2 chord angles (angle_mode = 1)
 constexpr uint32_t F_AXISV = 1u << 5;   // LINE parallel to v: test the u coordinate
@@ -95,7 +96,7 @@ struct HardEntry {
 
 // build-plan group (host -> device), 32 B
 enum : int32_t { G_LOOP = 0, G_COPY = 1, G_LINE = 2 };
-enum : int32_t { PF_CULL = 1, PF_ANGLE = 2, PF_TAIL_CLOSEG = 4, PF_TAIL_XCH = 8, PF_TAIL_NCH = 16 };
+enum : int32_t { PF_CULL = 1, PF_ANGLE = 2, PF_TAIL_CLOSEG = 4, PF_TAIL_XCH = 8, PF_TAIL_NCH = 16, PF_TREE = 32 };
 struct PlanGroup {
   int32_t kind, flags;
   int32_t loop;
@@ -120,8 +121,7 @@ struct LoopInfo {
 };
 
 constexpr int NTH = 256;         // threads per query CTA
-constexpr int QPT = 2;           // adjacent queries per thread (ILP; records shared)
-constexpr int QT = NTH * QPT;    // queries per tile
+constexpr int QT = NTH;          // queries per tile (one per thread)
 constexpr int NWARP = NTH / 32;
 constexpr int QW = 128;          // per-warp hard-pair queue capacity
 constexpr int MAXD = 64;         // hard cap of the explicit stack

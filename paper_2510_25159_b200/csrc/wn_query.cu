@@ -241,10 +241,12 @@ __device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px,
 
 // ---------------------------------------------------------------------------
 // K3a: phase 1 of the query kernel.  One CTA (NTH threads) = one tile of up to
-// QT = NTH x QPT queries of one face, QPT adjacent queries per thread; the
-// face's TMA-staged record program is swept in lock-step by all warps, so every
-// record is one broadcast shared-memory read shared by 32 x QPT queries.
-// Hard pairs go straight to the global queue through per-warp slot chunks.
+// QT = NTH queries of one face, one query per thread; the face's TMA-staged
+// record program is swept in lock-step by all warps, so every record is one
+// broadcast shared-memory read shared by the 32 queries of a warp.
+// Records form, per chain, the path hierarchy of P:372-380 (pre-order SPAN
+// nodes over SEG leaves): a warp skips a SPAN's subtree when every active lane
+// is outside its ellipse.  Hard (query, segment) pairs go to the global queue.
 // ---------------------------------------------------------------------------
 template <typename R>
 struct HotView;
@@ -296,14 +298,15 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 
+#ifndef WN_P1_MINB
+#define WN_P1_MINB 4
+#endif
 template <typename R, bool COUNT>
-__global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
+__global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
-  constexpr int RCH = F64 ? 896 : 1792;                  // records per staged chunk (28 KB)
+  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
   __shared__ __align__(128) Hot<R> s_rec[RCH];
   __shared__ HardEntry s_hb[NWARP][HWB];
-  __shared__ uint16_t s_hl[NWARP][HWB];
-  __shared__ int s_pend[QT];
   __shared__ __align__(8) uint64_t s_bar;
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
@@ -312,37 +315,25 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   const int f = T.face;
   const uint8_t per = P.face_per[f];
   const double *dom = P.face_dom + 4 * f;
-  bool valid[QPT];
-  int32_t qi[QPT];
-  double px[QPT], py[QPT];
-  float pxf[QPT], pyf[QPT];
-#pragma unroll
-  for (int k = 0; k < QPT; ++k) {
-    const int ql = QPT * t + k;
-    valid[k] = ql < T.qcnt;
-    const int32_t pos = (int32_t)T.qbeg + ql;
-    qi[k] = valid[k] ? (*P.unsorted ? P.perm[pos] : pos) : 0;
-    double u = 0.0, v = 0.0;
-    if (valid[k]) {
-      u = P.uv[2 * (int64_t)qi[k]];
-      v = P.uv[2 * (int64_t)qi[k] + 1];
-      if (!isfinite(u) || !isfinite(v)) {
-        P.winding[qi[k]] = nan_d();
-        P.flag[qi[k]] = 3;
-        valid[k] = false;
-        u = v = 0.0;
-      } else {
-        if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
-        if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
-        if (!F64) { u = (double)(float)u; v = (double)(float)v; }
-      }
+  bool valid = t < T.qcnt;
+  const int32_t pos = (int32_t)T.qbeg + t;
+  const int32_t qi = valid ? (*P.unsorted ? P.perm[pos] : pos) : 0;
+  double px = 0.0, py = 0.0;
+  if (valid) {
+    double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+    if (!isfinite(u) || !isfinite(v)) {
+      P.winding[qi] = nan_d();
+      P.flag[qi] = 3;
+      valid = false;
+    } else {
+      if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
+      if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
+      if (!F64) { u = (double)(float)u; v = (double)(float)v; }
+      px = u;
+      py = v;
     }
-    px[k] = u;
-    py[k] = v;
-    pxf[k] = (float)u;
-    pyf[k] = (float)v;
-    s_pend[QPT * t + k] = 0;
   }
+  const float pxf = (float)px, pyf = (float)py;
   if (t == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
@@ -357,18 +348,14 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
   // (fp64 records; margins 2^-16 scale + 2^-17 relative)
   const float eps_c = F64 ? __double2float_ru((eps + P.face_M[f] * 0x1p24) * (1.0 + 0x1p-17)) : (float)eps;
 
-  // record-stream state (warp-uniform): previous chain point, group start A
-  double prx = 0.0, pry = 0.0, gax = 0.0, gay = 0.0;
-  // per-query state
-  float cdf[QPT];
-  bool up[QPT], onb[QPT], act[QPT];
-  int xs[QPT], halves[QPT], skip_end[QPT], pend[QPT];
-  double fr[QPT];
-#pragma unroll
-  for (int k = 0; k < QPT; ++k) {
-    cdf[k] = 0.f; up[k] = false; onb[k] = false; act[k] = valid[k];
-    xs[k] = 0; halves[k] = 0; skip_end[k] = 0; pend[k] = 0; fr[k] = 0.0;
-  }
+  double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
+  // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
+  double zx = 0.0, zy = 0.0;
+  float cdf = 0.f;
+  bool up = false, onb = false;
+  int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
+  int xs = 0, halves = 0, pend = 0;
+  double fr = 0.0;
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
   unsigned phase = 0;
@@ -382,12 +369,17 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
     int b = 0;
     if (lane == 0) b = atomicAdd(P.hq_count, hn_);
     b = __shfl_sync(0xffffffffu, b, 0);
+    bool ovf = false;
     for (int i = lane; i < hn_; i += 32) {
       if (b + i < P.hq_cap) P.hq[b + i] = s_hb[warp][i];
-      else atomicOr(&s_pend[s_hl[warp][i]], 2);
+      else ovf = true;
     }
+    // an overflowing entry belongs to one of this warp's queries: tag them all
+    // that queued something in this batch (they are recomputed exactly)
+    if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
     __syncwarp();
     hn_ = 0;
+    pend &= ~4;
   };
 
   for (int cb = 0; cb < nrec; cb += RCH) {
@@ -401,158 +393,134 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
     }
     phase ^= 1u;
     const int ce = cb + cn;
-    HotView<R> hn;
-    if (gr < ce) hn.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
     while (gr < ce) {
-      const HotView<R> h = hn;
-      if (gr + 1 < ce) hn.load(sbase + (unsigned)(gr + 1 - cb) * (unsigned)sizeof(Hot<R>));   // prefetch
+      HotView<R> h;
+      h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
       const uint32_t meta = h.meta;
       const uint32_t kind = meta & 0xFu;
-      if (__builtin_expect(kind == K_SEG, 1)) {
-        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9, R5).
-        // Fast path (branch-free): the fp32 filter certifies "pruned, no
-        // crossing, d >= eps"; anything else takes the exact slow path below.
-        float df[QPT];
-        bool u1[QPT], pr[QPT], need[QPT];
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          if constexpr (F64) {
-            u1[k] = h.y >= py[k];                              // exact side of the branch cut
-            df[k] = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
-          } else {
-            u1[k] = h.fy >= pyf[k];
-            const float dx = h.fx - pxf[k], dy = h.fy - pyf[k];
-            df[k] = sqrtf(dx * dx + dy * dy);
-          }
-          pr[k] = cdf[k] + df[k] > h.fs;                       // certified pruned
-          need[k] = act[k] && (!pr[k] || !(df[k] > eps_c) || u1[k] != up[k] || (meta & F_ANGLE));
-          any |= need[k];
-          if (COUNT && act[k]) ++c_pairs;
+      const bool act = valid && gr >= skip_end;
+      if (__builtin_expect(kind == K_SEG || kind == K_SPAN, 1)) {
+        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
+        // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
+        // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
+        // ellipse, d >= eps"; a crossing / hard / uncertain lane takes the exact
+        // slow path.
+        bool u1;
+        float df;
+        if constexpr (F64) {
+          u1 = h.y >= py;                                      // exact side of the branch cut
+          df = fdist_ftz(h.fx - pxf, h.fy - pyf);
+        } else {
+          u1 = h.fy >= pyf;
+          const float dx = h.fx - pxf, dy = h.fy - pyf;
+          df = sqrtf(dx * dx + dy * dy);
         }
-        if (__any_sync(0xffffffffu, any)) {
-          bool hard[QPT];
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            hard[k] = false;
-            if (need[k]) {
-              if (!(df[k] > eps_c)) {                          // filter cannot certify d >= eps
-                if constexpr (F64) {
-                  const double dx = h.x - px[k], dy = h.y - py[k];
-                  onb[k] |= sqrt(dx * dx + dy * dy) < eps;
-                } else {
-                  onb[k] |= df[k] < (float)eps;
-                }
-              }
-              if (pr[k]) {                                     // pruned: chord (a5)
-                if (meta & F_ANGLE) {
-                  if constexpr (F64) fr[k] += chord_angle(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
-                  else fr[k] += (double)chord_angle((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
-                } else if (u1[k] != up[k]) {
-                  if constexpr (F64) xs[k] += xcount(prx - px[k], pry - py[k], h.x - px[k], h.y - py[k]);
-                  else xs[k] += xcount((float)prx - pxf[k], (float)pry - pyf[k], h.fx - pxf[k], h.fy - pyf[k]);
-                }
-              } else {
-                hard[k] = !onb[k];                             // exact recursion in phase 2
+        const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
+        if (kind == K_SPAN) {
+          // descend unless every active lane prunes the whole run
+          const bool descend = act && !pr;
+          if (!__any_sync(0xffffffffu, descend)) {
+            // every active lane substitutes the run's chord (homotopy)
+            if (__any_sync(0xffffffffu, act && (u1 != up || (meta & F_ANGLE)))) {
+              if (act) {
+                if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
               }
             }
+            if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
+            gr += (int)(meta >> 8);
+            if (COUNT && lane == 0) ++c_cull;
+          } else if (act && pr) {
+            // this lane prunes the run: chord now, inactive for the subtree
+            if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+            else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+            zx = h.x; zy = h.y; cdf = df; up = u1;
+            skip_end = gr + 1 + (int)(meta >> 8);
           }
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            const unsigned m = __ballot_sync(0xffffffffu, hard[k]);
+        } else {
+          const bool need = act && (!pr || u1 != up || (meta & F_ANGLE));
+          if (__any_sync(0xffffffffu, need)) {
+            bool hard = false;
+            if (need) {
+              if (!(df > eps_c)) {                             // filter cannot certify d >= eps
+                if constexpr (F64) {
+                  const double dx = h.x - px, dy = h.y - py;
+                  onb |= sqrt(dx * dx + dy * dy) < eps;
+                } else {
+                  onb |= df < (float)eps;
+                }
+              }
+              if (cdf + df > h.fs && !onb) {                   // pruned: chord (a5)
+                if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+              } else {
+                hard = !onb;                                   // exact recursion in phase 2
+              }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, hard);
             if (m) {
               const int cnt = __popc(m);
               if (hn_ + cnt > HWB) flush();
-              if (hard[k]) {
-                const int slot = hn_ + __popc(m & ((1u << lane) - 1u));
+              if (hard) {
                 HardEntry H;
-                H.px = px[k];
-                H.py = py[k];
-                H.q = qi[k];
+                H.px = px;
+                H.py = py;
+                H.q = qi;
                 H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
-                s_hb[warp][slot] = H;
-                s_hl[warp][slot] = (uint16_t)(QPT * t + k);
-                pend[k] |= 1;
+                s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
+                pend |= 1 | 4;
                 if (COUNT) ++c_hard;
               }
               hn_ += cnt;
             }
           }
+          if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
+          if (COUNT && act) ++c_pairs;
         }
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) {
-          cdf[k] = df[k];
-          up[k] = u1[k];
+      } else if (kind == K_MOVE || kind == K_MOVEG) {
+        const double nx = h.x - px, ny = h.y - py;
+        float nd;
+        if constexpr (F64) nd = fdist_ftz(h.fx - pxf, h.fy - pyf);
+        else nd = sqrtf((float)(nx * nx + ny * ny));
+        if (act) {
+          if (!(nd > eps_c)) onb |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
+          if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+            // gap chord Z -> A': -omega(p,Z,A') + its crossing
+            const double ax = zx - px, ay = zy - py;
+            const double cr = canon_cross(ax, ay, nx, ny);
+            fr -= atan2(cr, ax * nx + ay * ny);
+            xs += xcount_exact(ax, ay, nx, ny, cr);
+          }
         }
-        prx = h.x;
-        pry = h.y;
-      } else {
-        // group boundaries: a culled query becomes active again after its group
-#pragma unroll
-        for (int k = 0; k < QPT; ++k) act[k] = valid[k] && gr >= skip_end[k];
-        if (kind == K_MOVE || kind == K_MOVEG) {
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            const double nx = h.x - px[k], ny = h.y - py[k];
-            float nd;
-            if constexpr (F64) nd = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
-            else nd = sqrtf((float)(nx * nx + ny * ny));
-            if (act[k]) {
-              if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
-              if (kind == K_MOVEG && !(meta & F_ANGLE)) {
-                // gap chord Z -> A': -omega(p,Z,A') + its crossing
-                const double zx = prx - px[k], zy = pry - py[k];
-                const double cr = canon_cross(zx, zy, nx, ny);
-                fr[k] -= atan2(cr, zx * nx + zy * ny);
-                xs[k] += xcount_exact(zx, zy, nx, ny, cr);
-              }
-            }
-            cdf[k] = nd;
-            up[k] = F64 ? (h.y >= py[k]) : (h.fy >= pyf[k]);
-          }
-          if (kind == K_MOVE) { gax = h.x; gay = h.y; }
-          prx = h.x;
-          pry = h.y;
-        } else if (kind == K_GROUP) {
-          // copy-group / closed-loop cull: p outside the group's box => exactly 0
-          bool out[QPT], all = true;
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            out[k] = !act[k] || group_out_v(h, px[k], py[k]);
-            all &= out[k];
-          }
-          const int skip = (int)(meta >> 8);
-          if (__all_sync(0xffffffffu, all)) {
-            gr += skip;
-            if (gr + 1 < ce) hn.load(sbase + (unsigned)(gr + 1 - cb) * (unsigned)sizeof(Hot<R>));
-            if (COUNT && lane == 0) ++c_cull;
+        if (kind == K_MOVE) { gax = h.x; gay = h.y; }
+        zx = h.x; zy = h.y; cdf = nd;
+        up = F64 ? (h.y >= py) : (h.fy >= pyf);
+      } else if (kind == K_GROUP) {
+        // copy-group / closed-loop cull: p outside the group's box => exactly 0
+        const bool out = !act || group_out_v(h, px, py);
+        const int skip = (int)(meta >> 8);
+        if (__all_sync(0xffffffffu, out)) {
+          gr += skip;
+          if (COUNT && lane == 0) ++c_cull;
+        } else if (out && act) {
+          skip_end = gr + 1 + skip;
+        }
+      } else if (kind == K_LINE) {
+        // omega(p,L) = +-1/2, p on L counts as left (R11)
+        const double q = (meta & F_AXISV) ? px : py;
+        const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
+        if (act) halves += left ? 1 : -1;
+      } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
+        if (act) {
+          const double cx = zx - px, cy = zy - py, ax = gax - px, ay = gay - py;
+          if (kind == K_XCH) {
+            xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
+          } else if (kind == K_NCH) {
+            fr -= chord_angle(ax, ay, cx, cy);
           } else {
-#pragma unroll
-            for (int k = 0; k < QPT; ++k)
-              if (out[k] && act[k]) { skip_end[k] = gr + 1 + skip; act[k] = false; }
-          }
-        } else if (kind == K_LINE) {
-          // omega(p,L) = +-1/2, p on L counts as left (R11)
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            const double q = (meta & F_AXISV) ? px[k] : py[k];
-            const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
-            if (act[k]) halves[k] += left ? 1 : -1;
-          }
-        } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
-#pragma unroll
-          for (int k = 0; k < QPT; ++k) {
-            if (!act[k]) continue;
-            const double zx = prx - px[k], zy = pry - py[k], ax = gax - px[k], ay = gay - py[k];
-            if (kind == K_XCH) {
-              xs[k] -= xcount_exact(ax, ay, zx, zy, canon_cross(ax, ay, zx, zy));
-            } else if (kind == K_NCH) {
-              fr[k] -= chord_angle(ax, ay, zx, zy);
-            } else {
-              const double cr = canon_cross(zx, zy, ax, ay);
-              fr[k] -= atan2(cr, zx * ax + zy * ay);
-              xs[k] += xcount_exact(zx, zy, ax, ay, cr);
-            }
+            const double cr = canon_cross(cx, cy, ax, ay);
+            fr -= atan2(cr, cx * ax + cy * ay);
+            xs += xcount_exact(cx, cy, ax, ay, cr);
           }
         }
       }
@@ -561,33 +529,27 @@ __global__ void __launch_bounds__(NTH, 3) k_phase1(QParams<R> P) {
     if (ce < nrec) __syncthreads();   // all warps done with this chunk before it is overwritten
   }
   if (hn_) flush();
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < QPT; ++k) pend[k] |= s_pend[QPT * t + k];
 
   // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
-#pragma unroll
-  for (int k = 0; k < QPT; ++k) {
-    if (valid[k]) {
-      if (onb[k]) {
-        P.winding[qi[k]] = nan_d();
-        P.flag[qi[k]] = 2;
-        if (COUNT) atomicAdd(P.counters + 7, 1ull);
-      } else {
-        const double w = (double)xs[k] + 0.5 * (double)halves[k] + fr[k] * (1.0 / TWO_PI);
-        P.winding[qi[k]] = w;
-        if (!pend[k]) P.flag[qi[k]] = classify(w, P.rule);
-      }
+  if (valid) {
+    if (onb) {
+      P.winding[qi] = nan_d();
+      P.flag[qi] = 2;
+      if (COUNT) atomicAdd(P.counters + 7, 1ull);
+    } else {
+      const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
+      P.winding[qi] = w;
+      if (!(pend & 3)) P.flag[qi] = classify(w, P.rule);
     }
-    const bool pq = valid[k] && !onb[k] && pend[k];
-    const unsigned pm = __ballot_sync(0xffffffffu, pq);
-    if (pm) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
-      if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi[k] | ((pend[k] & 2) ? (int32_t)0x80000000 : 0);
-    }
+  }
+  const bool pq = valid && !onb && (pend & 3);
+  const unsigned pm = __ballot_sync(0xffffffffu, pq);
+  if (pm) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
+    if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((pend & 2) ? (int32_t)0x80000000 : 0);
   }
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
@@ -645,6 +607,7 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id) {
       const uint32_t meta = h.meta, kind = meta & 0xFu;
       double hx, hy, hs;
       if constexpr (sizeof(R) == 8) { hx = h.x; hy = h.y; hs = h.fs; } else { hx = h.a; hy = h.b; hs = h.c; }
+      if (kind == K_SPAN) continue;   // hierarchy node: always descend (exact, leaves only)
       if (kind == K_SEG || kind == K_MOVE || kind == K_MOVEG) {
         const double nx = hx - u, ny = hy - v, nd = sqrt(nx * nx + ny * ny);
         if (nd < P.eps) { ob = true; break; }

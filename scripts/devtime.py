@@ -32,4 +32,4 @@ for c in cfgs:
     if c == "C4":
         run("C4-fp32", G.to_fp32_inputs(wl), precision=1)
     if c in ("C2", "C5"):
-        run(c + "-angle", wl, angle_mode=1)
+        run(c + "-angle", wl, angle_mode=1); run(c + "-flat", wl, hierarchy=False)

@@ -54,10 +54,10 @@ def test_c1_full(angle_mode):
     _check(wl, w, fl, min_cmp=0.999)
 
 
-@pytest.mark.parametrize("angle_mode", [0, 1])
-def test_c2_sampled(angle_mode):
+@pytest.mark.parametrize("angle_mode,hierarchy", [(0, True), (1, True), (0, False)])
+def test_c2_sampled(angle_mode, hierarchy):
     wl = G.gen_c2(n_queries=60_000)
-    w, fl = _gpu(wl, angle_mode=angle_mode)
+    w, fl = _gpu(wl, angle_mode=angle_mode, hierarchy=hierarchy)
     _check(wl, w, fl, min_cmp=0.85)
     # the near-curve shell (1e-6) is part of the batch
     assert wl["meta"]["near_mask"].sum() > 5000
@@ -73,10 +73,10 @@ def test_c2_full_size_sampled():
     assert np.all(fl != 3)
 
 
-@pytest.mark.parametrize("angle_mode", [0, 1])
-def test_c3_torus(angle_mode):
+@pytest.mark.parametrize("angle_mode,hierarchy", [(0, True), (1, True), (0, False)])
+def test_c3_torus(angle_mode, hierarchy):
     wl = G.gen_c3(n_queries=20_000)
-    w, fl = _gpu(wl, angle_mode=angle_mode)
+    w, fl = _gpu(wl, angle_mode=angle_mode, hierarchy=hierarchy)
     _check(wl, w, fl, min_cmp=0.99)
 
 
@@ -92,10 +92,10 @@ def test_c4_fp32():
     _check(wl, w, fl, fp32=True, min_cmp=0.95)
 
 
-@pytest.mark.parametrize("angle_mode", [0, 1])
-def test_c5_reduced(angle_mode):
+@pytest.mark.parametrize("angle_mode,hierarchy", [(0, True), (1, True), (0, False), (1, False)])
+def test_c5_reduced(angle_mode, hierarchy):
     wl = G.gen_c5(n_faces=120, grid=32)
-    w, fl = _gpu(wl, angle_mode=angle_mode)
+    w, fl = _gpu(wl, angle_mode=angle_mode, hierarchy=hierarchy)
     _check(wl, w, fl, min_cmp=0.97)
 
 

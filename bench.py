@@ -115,18 +115,29 @@ def _clock_summary(proc, t0, t1):
             "reasons": reasons, "samples": len(inwin)}
 
 
+def _oracle_rate(wl, rng, cores, nq):
+    """Per-query cost of the oracle from two pilots (fixed cost = its own
+    lifting/pairing of all faces, paid once per call)."""
+    import oracle
+    ts = []
+    for m in (512, 4096):
+        idx = rng.choice(nq, size=min(nq, m), replace=False)
+        t = time.perf_counter()
+        oracle.query(wl, face_id=wl["face_id"][idx], uv=wl["uv"][idx], nthreads=cores)
+        ts.append((len(idx), time.perf_counter() - t))
+    (m0, t0), (m1, t1) = ts
+    per_q = max((t1 - t0) / max(m1 - m0, 1), 1e-9)
+    return per_q, max(t0 - per_q * m0, 0.0)
+
+
 def _cpu_baseline(wl, target_s, rank_seed=0):
     """Oracle (as it stands) on a bounded random sample of the same workload."""
     import oracle
     cores = os.cpu_count() or 1
     rng = np.random.default_rng(1234 + rank_seed)
     nq = len(wl["face_id"])
-    pilot = rng.choice(nq, size=min(nq, 256), replace=False)
-    t = time.perf_counter()
-    oracle.query(wl, face_id=wl["face_id"][pilot], uv=wl["uv"][pilot], nthreads=cores)
-    tp = time.perf_counter() - t
-    rate = len(pilot) / max(tp, 1e-6)
-    m = int(min(nq, max(512, rate * target_s)))
+    per_q, fixed = _oracle_rate(wl, rng, cores, nq)
+    m = int(min(nq, max(512, (target_s - fixed) / per_q)))
     idx = np.sort(rng.choice(nq, size=m, replace=False))
     t = time.perf_counter()
     oracle.query(wl, face_id=wl["face_id"][idx], uv=wl["uv"][idx], nthreads=cores)
@@ -146,11 +157,8 @@ def run_reference(args, rank, world):
     # size one step as a bounded sample (~ a few seconds per step)
     rng = np.random.default_rng(99)
     nq = len(wl["face_id"])
-    pilot = rng.choice(nq, size=256, replace=False)
-    t = time.perf_counter()
-    oracle.query(wl, face_id=wl["face_id"][pilot], uv=wl["uv"][pilot], nthreads=cores)
-    rate = 256 / max(time.perf_counter() - t, 1e-6)
-    per_step = int(max(512, min(nq, rate * args.ref_step_s)))
+    per_q, fixed = _oracle_rate(wl, rng, cores, nq)
+    per_step = int(max(512, min(nq, (args.ref_step_s - fixed) / per_q)))
     samples = [np.sort(rng.choice(nq, size=per_step, replace=False)) for _ in range(args.warmup + args.steps)]
     for i in range(args.warmup):
         oracle.query(wl, face_id=wl["face_id"][samples[i]], uv=wl["uv"][samples[i]], nthreads=cores)

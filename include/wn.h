@@ -119,10 +119,13 @@ wn_status_t wn_faces_info(wn_faces_t faces, wn_faces_info_t *out /* [host] */);
 
 /* Device-side event counters of the last wn_query on this handle, enabled by
  * wn_set_counters(faces, 1) (adds atomics; for diagnostics, not for timing).
- * out[host][8] = {pairs_tested, hard_pairs, nodes, evals, leaves, max_depth,
- *                 groups_culled, on_boundary}. */
+ * out[host][12] = {root (query, segment) tests, hard pairs, recursion nodes,
+ *                  split-point evaluations, leaves, max depth, warp-level skips
+ *                  (culled groups + pruned hierarchy subtrees), on-boundary,
+ *                  (query, hierarchy node) tests, phase-1 warp-record
+ *                  iterations, 0, 0}. */
 wn_status_t wn_set_counters(wn_faces_t faces, int enable);
-wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [host][8] */);
+wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [host][12] */);
 
 /* In-library timing of the query kernel K3 (CUDA events recorded on the
  * launching stream around every K3 launch while enabled).  wn_get_timing

@@ -31,7 +31,7 @@ EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
            "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
-                 "groups_culled_warps", "on_boundary"]
+                 "warp_skips", "on_boundary", "span_tests", "warp_records", "_r10", "_r11"]
 
 
 class WNError(RuntimeError):
@@ -212,7 +212,7 @@ class Faces:
         load().wn_set_counters(self._h, int(bool(enable)))
 
     def counters(self, stream=None):
-        arr = (C.c_int64 * 8)()
+        arr = (C.c_int64 * 12)()
         rc = load().wn_get_counters(self._h, _stream(stream, self.device), arr)
         if rc != WN_OK:
             raise WNError(rc, last_error())

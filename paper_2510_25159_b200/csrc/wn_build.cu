@@ -755,7 +755,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   WN_CUDA(cache_alloc((void **)&F->face_per, std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_ok, std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
-  WN_CUDA(cache_alloc((void **)&F->counters, 8 * sizeof(unsigned long long), st));
+  WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
   std::vector<int32_t> order(nf);
   std::iota(order.begin(), order.end(), 0);
@@ -1248,10 +1248,10 @@ extern "C" wn_status_t wn_set_counters(wn_faces_t F, int enable) {
 
 extern "C" wn_status_t wn_get_counters(wn_faces_t F, void *stream, int64_t *out) {
   if (!F || !out) { set_error("wn_get_counters: NULL"); return WN_ERR_ARG; }
-  unsigned long long h[8];
+  unsigned long long h[12];
   WN_CUDA(cudaMemcpyAsync(h, F->counters, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   WN_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-  for (int i = 0; i < 8; ++i) out[i] = (int64_t)h[i];
+  for (int i = 0; i < 12; ++i) out[i] = (int64_t)h[i];
   return WN_OK;
 }
 

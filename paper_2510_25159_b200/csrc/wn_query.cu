@@ -96,8 +96,10 @@ struct QParams {
   unsigned long long *counters;
 };
 
-// Counters (optional, COUNT=true): 0 pairs tested, 1 hard pairs, 2 nodes,
-// 3 evaluations, 4 leaves, 5 max depth, 6 groups culled (warp-level), 7 on-boundary
+// Counters (optional, COUNT=true): 0 (query, segment) root tests, 1 hard pairs,
+// 2 nodes, 3 evaluations, 4 leaves, 5 max depth, 6 warp-level skips (culled
+// groups + pruned hierarchy subtrees), 7 on-boundary, 8 (query, SPAN) tests,
+// 9 warp-record iterations of phase 1
 template <bool COUNT>
 __device__ __forceinline__ void cnt_add(unsigned long long *c, int i, unsigned long long v) {
   if (COUNT && v) atomicAdd(c + i, v);
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   int xs = 0, halves = 0, pend = 0;
   double fr = 0.0;
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
-  unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0;
+  unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0;
   unsigned phase = 0;
   int gr = 0;                    // warp-uniform record cursor
   const unsigned sbase = smem_u32(s_rec);
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       const uint32_t meta = h.meta;
       const uint32_t kind = meta & 0xFu;
       const bool act = valid && gr >= skip_end;
+      if (COUNT && lane == 0) ++c_rec;
       if (__builtin_expect(kind == K_SEG || kind == K_SPAN, 1)) {
         // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
         // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
@@ -417,6 +420,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         }
         const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
         if (kind == K_SPAN) {
+          if (COUNT && act) ++c_span;
           // descend unless every active lane prunes the whole run
           const bool descend = act && !pr;
           if (!__any_sync(0xffffffffu, descend)) {
@@ -555,6 +559,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
     cnt_add<COUNT>(P.counters, 1, c_hard);
     cnt_add<COUNT>(P.counters, 6, c_cull);
+    cnt_add<COUNT>(P.counters, 8, c_span);
+    cnt_add<COUNT>(P.counters, 9, c_rec);
   }
 }
 
@@ -834,7 +840,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   }
   const int hb = 148 * 8;
   if (F->counters_on) {
-    WN_CUDA(cudaMemsetAsync(F->counters, 0, 8 * sizeof(unsigned long long), st));
+    WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
     k_phase1<R, true><<<max_tiles, NTH, 0, st>>>(P);
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148, 128, 0, st>>>(P, face_id);

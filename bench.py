@@ -40,16 +40,17 @@ WORKLOAD = ("C5 synthetic B-Rep batch / tessellation: 20000 faces, loops 1-8 (ge
             "segments/loop 4-128 (log-uniform), degree 1-5 rational Bezier, 30% periodic in u, "
             "64x64 uv grid per face (81,920,000 queries), fp64")
 
-# FP64 roofline: B200 = 148 SMs x 64 FP64 lanes/clk,
-# FMA = 2 flops, at the 1965 MHz max SM clock (MEASURED_PEAKS.json sm_max_mhz).
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-# Algorithmic FP64 flops per unit of K3 work, this implementation (crossing
-# mode), counted from the SASS of k_query<double> (DESIGN.md "K3 work per
-# unit"; ncu cross-check in profiles/): per (query, segment) pair tested in
-# phase 1, per recursion node, per midpoint evaluation (degree-weighted mean).
-FLOPS_PER_PAIR = 14.0
-FLOPS_PER_NODE = 13.0
-FLOPS_PER_EVAL = 40.0
+# Roofline of the dominant kernel, k_phase1 (DESIGN.md 6 "Roofline"): after the
+# fp32 filter, the telescoped crossings and the path hierarchy it is bound by
+# SM instruction issue (ncu: issue-active ~59%, FP64 pipe ~8%, FMA pipe ~11%),
+# so the roofline is the issue rate: 148 SMs x 4 schedulers x 1 warp-instruction
+# per clock at the 1965 MHz max SM clock (MEASURED_PEAKS.json sm_max_mhz).
+ISSUE_PEAK = 148 * 4 * 1.965e9 / 1e9          # G warp-instructions / s
+# Work per unit of k_phase1, this implementation (profiles/round1: ncu
+# smsp__inst_executed.sum / the counters of the same launch): warp instructions
+# per warp-record iteration (record read, tests of 32 queries, hierarchy
+# decisions, hard-pair pushes amortised).
+INSTR_PER_WARP_RECORD = 74.8
 
 
 def _env_int(k, d):
@@ -255,11 +256,12 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     tw0 = time.time()
     e0.record(st)
-    k3_ms, k3_n = 0.0, 0
+    k3_ms, p1_ms, k3_n = 0.0, 0.0, 0
     for _ in range(args.steps):
         h = step(timing=True)
-        ms, n = h.timing()        # waits on the K3 events of this step (build already synced)
+        ms, p1, n = h.timing()    # waits on the K3 events of this step (build already synced)
         k3_ms += ms
+        p1_ms += p1
         k3_n += n
         h.close()
     e1.record(st)
@@ -336,16 +338,20 @@ def main():
         e2e = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
-    # ---- roofline of the dominant kernel (K3, k_query) ----
+    # ---- roofline of the dominant kernel (k_phase1) ----
     k3_avg = k3_ms / max(k3_n, 1)
-    flops = (FLOPS_PER_PAIR * cnt["pairs_tested"] + FLOPS_PER_NODE * cnt["nodes"] +
-             FLOPS_PER_EVAL * cnt["evals"])
-    achieved = flops / (k3_avg / 1e3) / 1e12
-    roofline = {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "wn::k_query<double>", "k3_ms": k3_avg, "k3_share_of_step": k3_avg / ms_step,
-                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 2 x 1.965 GHz (max clock)",
-                "units": {"pairs_tested": cnt["pairs_tested"], "nodes": cnt["nodes"], "evals": cnt["evals"]}}
+    p1_avg = p1_ms / max(k3_n, 1)
+    work = INSTR_PER_WARP_RECORD * cnt["warp_records"] / 1e9          # G warp-instructions per launch
+    achieved = work / (p1_avg / 1e3)
+    # dram traffic of k_phase1 per launch from the committed ncu --set full capture
+    roofline = {"bound": "alu", "achieved": achieved, "peak": ISSUE_PEAK, "unit": "Gwarp-inst/s",
+                "frac": achieved / ISSUE_PEAK, "traffic": 2.278e9,
+                "kernel": "wn::k_phase1<double>", "kernel_ms": p1_avg, "kernel_share_of_step": p1_avg / ms_step,
+                "k3_ms": k3_avg,
+                "peak_source": "derived: 148 SMs x 4 schedulers x 1 warp-inst/clk x 1.965 GHz (max SM clock)",
+                "units": {"warp_records": cnt["warp_records"], "instr_per_warp_record": INSTR_PER_WARP_RECORD},
+                "pipes_ncu": {"fp64_pct": 7.6, "fma_pct": 11.2, "alu_pct": 46.3, "xu_pct": 11.8,
+                              "issue_active_pct": 58.9, "src": "profiles/round1/ncu_full_k3_raw.csv"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

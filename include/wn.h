@@ -128,11 +128,13 @@ wn_status_t wn_set_counters(wn_faces_t faces, int enable);
 wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [host][12] */);
 
 /* In-library timing of the query kernel K3 (CUDA events recorded on the
- * launching stream around every K3 launch while enabled).  wn_get_timing
- * waits for the recorded events, returns the summed K3 milliseconds and the
- * number of K3 launches since the last wn_get_timing, and resets them. */
+ * launching stream around every K3 launch -- phase 1, hard pairs, overflow,
+ * finish -- and after its phase 1, while enabled).  wn_get_timing waits for the
+ * recorded events, returns the summed K3 and phase-1 milliseconds and the
+ * number of timed queries since the last call, and resets them. */
 wn_status_t wn_set_timing(wn_faces_t faces, int enable);
-wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, int64_t *k3_launches /* [host] */);
+wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, double *phase1_ms /* [host] or NULL */,
+                          int64_t *k3_launches /* [host] */);
 
 /* K1 segment prep on its own (diagnostics / tests): for every segment writes
  * out[s][10] = {B, S0, Bq[0..7]}: the derivative bound of Lemma 1 (P:335-345,

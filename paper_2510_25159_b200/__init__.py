@@ -79,7 +79,7 @@ def load():
         L.wn_set_timing.restype = C.c_int
         L.wn_set_timing.argtypes = [vp, C.c_int]
         L.wn_get_timing.restype = C.c_int
-        L.wn_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
+        L.wn_get_timing.argtypes = [vp, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]
         L.wn_last_build_launches.restype = C.c_int32
         L.wn_last_build_launches.argtypes = []
         L.wn_segment_prep.restype = C.c_int
@@ -222,13 +222,14 @@ class Faces:
         load().wn_set_timing(self._h, int(bool(enable)))
 
     def timing(self):
-        """(summed K3 milliseconds, K3 launches) since the last call (waits on events)."""
+        """(summed K3 ms, summed phase-1 ms, timed queries) since the last call (waits on events)."""
         ms = C.c_double()
+        p1 = C.c_double()
         n = C.c_int64()
-        rc = load().wn_get_timing(self._h, C.byref(ms), C.byref(n))
+        rc = load().wn_get_timing(self._h, C.byref(ms), C.byref(p1), C.byref(n))
         if rc != WN_OK:
             raise WNError(rc, last_error())
-        return ms.value, n.value
+        return ms.value, p1.value, n.value
 
     def close(self):
         if self._h:

@@ -711,6 +711,7 @@ struct DevBuf {
 void free_handle(wn_faces_t F) {
   if (!F) return;
   for (auto &pr : F->k3_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto &e : F->k3_mid) cudaEventDestroy(e);
   // stream-ordered frees on the legacy stream (caller guarantees no query in flight)
   void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
                 F->face_per, F->face_ok, F->face_M, F->counters};

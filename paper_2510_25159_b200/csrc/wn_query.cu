@@ -832,9 +832,10 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.max_depth = F->max_depth;
   P.rule = F->opt.rule;
   P.counters = F->counters;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
   if (F->timing_on) {
     WN_CUDA(cudaEventCreate(&e0));
+    WN_CUDA(cudaEventCreate(&em));
     WN_CUDA(cudaEventCreate(&e1));
     WN_CUDA(cudaEventRecord(e0, st));
   }
@@ -842,11 +843,13 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   if (F->counters_on) {
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
     k_phase1<R, true><<<max_tiles, NTH, 0, st>>>(P);
+    if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, F->counters);
   } else {
     k_phase1<R, false><<<max_tiles, NTH, 0, st>>>(P);
+    if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
     k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, nullptr);
@@ -855,6 +858,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   if (F->timing_on) {
     WN_CUDA(cudaEventRecord(e1, st));
     F->k3_events.push_back({e0, e1});
+    F->k3_mid.push_back(em);
   }
   WN_CUDA(cudaGetLastError());
   cache_free(base, st);
@@ -904,19 +908,25 @@ extern "C" wn_status_t wn_set_timing(wn_faces_t F, int enable) {
   return WN_OK;
 }
 
-extern "C" wn_status_t wn_get_timing(wn_faces_t F, double *ms, int64_t *launches) {
+extern "C" wn_status_t wn_get_timing(wn_faces_t F, double *ms, double *phase1_ms, int64_t *launches) {
   if (!F || !ms || !launches) { wn::set_error("wn_get_timing: NULL"); return WN_ERR_ARG; }
-  double tot = 0.0;
-  for (auto &pr : F->k3_events) {
+  double tot = 0.0, p1 = 0.0;
+  for (size_t i = 0; i < F->k3_events.size(); ++i) {
+    auto &pr = F->k3_events[i];
     WN_CUDA(cudaEventSynchronize(pr.second));
-    float t = 0.f;
+    float t = 0.f, tm = 0.f;
     WN_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
+    WN_CUDA(cudaEventElapsedTime(&tm, pr.first, F->k3_mid[i]));
     tot += t;
+    p1 += tm;
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
+    cudaEventDestroy(F->k3_mid[i]);
   }
   *ms = tot;
+  if (phase1_ms) *phase1_ms = p1;
   *launches = (int64_t)F->k3_events.size();
   F->k3_events.clear();
+  F->k3_mid.clear();
   return WN_OK;
 }

@@ -9,7 +9,7 @@ SOURCES = ["wn_build.cu", "wn_query.cu", "wn_alloc.cu"]
 HEADERS = ["wn_common.cuh", os.path.join("..", "..", "include", "wn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-shared", "-Xptxas", "-v", "-lgomp"]
 
 
 def _stale():

@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <omp.h>
 #include <numeric>
 #include <vector>
 
@@ -532,6 +533,11 @@ struct Plan {
   std::vector<int32_t> rec_off;   // per target face + 1
   std::vector<int32_t> cold_off;
   void reserve(size_t ng, size_t nf) { groups.reserve(ng); rec_off.reserve(nf + 1); cold_off.reserve(nf + 1); }
+  // keep capacity (pages stay mapped across builds: page faults dominated the host plan)
+  void clear() {
+    groups.clear(); rec_off.clear(); cold_off.clear();
+    n_lines = n_cull = 0; recs = colds = 0; face_rec0 = face_cold0 = 0; cur_face = -1;
+  }
   int64_t n_lines = 0, n_cull = 0;
   int32_t recs = 0, colds = 0;
   int32_t face_rec0 = 0, face_cold0 = 0;
@@ -758,15 +764,26 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
-  std::vector<int32_t> order(nf);
-  std::iota(order.begin(), order.end(), 0);
   int32_t maxr = 0;
   for (int f = 0; f < nf; ++f) maxr = std::max(maxr, plan.rec_off[f + 1] - plan.rec_off[f]);
   F->max_face_records = maxr;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    return (plan.rec_off[a + 1] - plan.rec_off[a]) > (plan.rec_off[b + 1] - plan.rec_off[b]);
-  });
-  std::vector<uint8_t> ok(nf, 1);
+  // face_order: faces by decreasing record count, ties by index (stable counting sort)
+  static std::vector<int32_t> order, bucket;
+  order.resize(nf);
+  if ((int64_t)maxr <= 4 * (int64_t)nf + 4096) {
+    bucket.assign((size_t)maxr + 2, 0);
+    for (int f = 0; f < nf; ++f) ++bucket[maxr - (plan.rec_off[f + 1] - plan.rec_off[f]) + 1];
+    for (int32_t c = 0; c <= maxr; ++c) bucket[c + 1] += bucket[c];
+    for (int f = 0; f < nf; ++f) order[bucket[maxr - (plan.rec_off[f + 1] - plan.rec_off[f])]++] = f;
+  } else {
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {
+      const int ca = plan.rec_off[a + 1] - plan.rec_off[a], cb = plan.rec_off[b + 1] - plan.rec_off[b];
+      return ca != cb ? ca > cb : a < b;
+    });
+  }
+  static std::vector<uint8_t> ok;
+  ok.assign(nf, 1);
   WN_CUDA(h2d(F->face_rec_off, plan.rec_off.data(), sizeof(int32_t) * (nf + 1), st));
   WN_CUDA(h2d(F->face_cold_off, plan.cold_off.data(), sizeof(int32_t) * (nf + 1), st));
   if (nf) {
@@ -836,9 +853,10 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   Trace tr;
 
   // --- host copies of the small CSR / face arrays ---
-  std::vector<int32_t> h_lso(n_loops + 1), h_flo(n_faces + 1);
-  std::vector<uint8_t> h_per(n_faces);
-  std::vector<double> h_dom(4 * (size_t)n_faces);
+  static std::vector<int32_t> h_lso, h_flo;
+  static std::vector<uint8_t> h_per;
+  static std::vector<double> h_dom;
+  h_lso.resize(n_loops + 1); h_flo.resize(n_faces + 1); h_per.resize(n_faces); h_dom.resize(4 * (size_t)n_faces);
   WN_CUDA(cudaMemcpyAsync(h_lso.data(), loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaMemcpyAsync(h_flo.data(), face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st));
   if (n_faces) {
@@ -930,11 +948,16 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   tr.mark("prep + lift + info d2h");
 
   // --- K2b: validation + planning (host) ---
-  std::vector<int32_t> status(n_faces, WN_FACE_OK);
-  std::vector<FaceCtx> ctx(n_faces);
+  static std::vector<int32_t> status;
+  static std::vector<FaceCtx> ctx;
+  status.assign(n_faces, WN_FACE_OK);
+  ctx.resize(n_faces);
   // pairing requests for bi-periodic faces
   struct Cand { int face, alpha, beta, s; double px, py; };
   std::vector<int> need_pair;
+  static std::vector<uint8_t> needp;
+  needp.assign(n_faces, 0);
+#pragma omp parallel for schedule(static, 256)
   for (int f = 0; f < n_faces; ++f) {
     FaceCtx &C = ctx[f];
     C.per = h_per[f] & 3;
@@ -960,15 +983,19 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     if (nA != nB && (O.strict || C.per == 3)) { status[f] = WN_FACE_UNBALANCED; continue; }
     if (C.per == 3 && nA > 0) {
       if (cp != 0 && cq != 0) { status[f] = WN_FACE_GENERAL_PQ; continue; }
-      need_pair.push_back(f);
+      needp[f] = 1;
     }
   }
+  for (int f = 0; f < n_faces; ++f)
+    if (needp[f]) need_pair.push_back(f);
   bool any_bad = false;
   for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
 
   // --- pairing (Algs. 7-9) for bi-periodic faces via probe queries ---
   // pair_beta[alpha] = beta, pair_s[alpha] = transverse translate of beta
-  std::vector<int> pair_beta(n_loops, -1), pair_s(n_loops, 0);
+  static std::vector<int> pair_beta, pair_s;
+  pair_beta.assign(n_loops, -1);
+  pair_s.assign(n_loops, 0);
   if (!any_bad && !need_pair.empty()) {
     // virtual faces: one uni-periodic extended curve per non-contractible loop
     std::vector<int> vface(n_loops, -1);
@@ -1115,14 +1142,17 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   }
 
   tr.mark("validate + pairing");
-  // --- final plan ---
-  Plan P;
-  P.reserve((size_t)n_loops * 2 + 16, (size_t)n_faces);
-  std::vector<double> fdom(4 * (size_t)n_faces);
+  // --- final plan: faces planned in parallel (contiguous face ranges per
+  // thread, concatenated in face order with offset fix-ups) ---
+  static std::vector<double> fdom;
+  fdom.resize(4 * (size_t)n_faces);
   for (int f = 0; f < n_faces; ++f) {
     const FaceCtx &C = ctx[f];
     fdom[4 * f] = C.u0; fdom[4 * f + 1] = C.Tu; fdom[4 * f + 2] = C.v0; fdom[4 * f + 3] = C.Tv;
-    P.begin_face(f);
+  }
+  tr.mark("plan: fdom");
+  auto plan_face = [&](Plan &P, int f) {
+    const FaceCtx &C = ctx[f];
     for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
       const LoopInfo &I = L[l];
       if (I.nseg == 0) continue;
@@ -1162,6 +1192,58 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
         plan_extended_copies(P, lb, Ib, C, axis, sb + j, true);
       }
     }
+  };
+  const int nth = std::max(1, std::min(omp_get_max_threads(), std::max(1, n_faces / 256)));
+  static std::vector<Plan> TP;
+  if ((int)TP.size() < nth) TP.resize(nth);
+  for (int i = 0; i < nth; ++i) TP[i].clear();
+#pragma omp parallel for num_threads(nth) schedule(static, 1)
+  for (int tid = 0; tid < nth; ++tid) {
+    const int f0 = (int)((int64_t)n_faces * tid / nth), f1 = (int)((int64_t)n_faces * (tid + 1) / nth);
+    Plan &Q = TP[tid];
+    Q.reserve((size_t)(h_flo[f1] - h_flo[f0]) * 2 + 16, (size_t)(f1 - f0));
+    for (int f = f0; f < f1; ++f) {
+      Q.begin_face(f);
+      plan_face(Q, f);
+    }
+  }
+  tr.mark("plan: parallel faces");
+  static Plan P;
+  P.clear();
+  {
+    // per-thread group / record / cold bases, then a parallel copy with offset fix-ups
+    static std::vector<size_t> gb, fb;
+    static std::vector<int32_t> rb, cb;
+    gb.assign(nth + 1, 0); fb.assign(nth + 1, 0); rb.assign(nth + 1, 0); cb.assign(nth + 1, 0);
+    for (int t = 0; t < nth; ++t) {
+      const Plan &Q = TP[t];
+      gb[t + 1] = gb[t] + Q.groups.size();
+      fb[t + 1] = fb[t] + Q.rec_off.size();
+      rb[t + 1] = rb[t] + Q.recs;
+      cb[t + 1] = cb[t] + Q.colds;
+      P.n_lines += Q.n_lines;
+      P.n_cull += Q.n_cull;
+    }
+    P.groups.resize(gb[nth]);
+    P.rec_off.resize(fb[nth]);
+    P.cold_off.resize(fb[nth]);
+#pragma omp parallel for num_threads(nth) schedule(static, 1)
+    for (int t = 0; t < nth; ++t) {
+      const Plan &Q = TP[t];
+      PlanGroup *dg = P.groups.data() + gb[t];
+      for (size_t i = 0; i < Q.groups.size(); ++i) {
+        PlanGroup G = Q.groups[i];
+        G.rec_off += rb[t];
+        G.cold_off += cb[t];
+        dg[i] = G;
+      }
+      for (size_t i = 0; i < Q.rec_off.size(); ++i) {
+        P.rec_off[fb[t] + i] = Q.rec_off[i] + rb[t];
+        P.cold_off[fb[t] + i] = Q.cold_off[i] + cb[t];
+      }
+    }
+    P.recs = rb[nth];
+    P.colds = cb[nth];
   }
   P.end();
   if (P.recs < 0 || P.colds >= (1 << 23) * 64) { set_error("too many records"); return WN_ERR_ARG; }
@@ -1171,16 +1253,18 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       return WN_ERR_ARG;
     }
 
-  tr.mark("plan");
+  tr.mark("plan: concat + checks");
   wn_faces_t F = new wn_faces_s();
   F->precision = fp32 ? 1 : 0;
   F->opt = O;
   F->eps = eps;
   F->max_depth = maxd;
   F->device = dev;
-  std::vector<uint8_t> fper(n_faces);
+  static std::vector<uint8_t> fper;
+  fper.resize(n_faces);
   for (int f = 0; f < n_faces; ++f) fper[f] = ctx[f].per;
-  std::vector<double> fM(n_faces);
+  static std::vector<double> fM;
+  fM.resize(n_faces);
   for (int f = 0; f < n_faces; ++f) fM[f] = ctx[f].M;
   wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, fM, F) : materialise<double>(B, P, fper, fdom, fM, F);
   if (rc != WN_OK) { free_handle(F); return rc; }

@@ -23,16 +23,17 @@ namespace wn {
 // ---------------------------------------------------------------------------
 enum : uint32_t {
   K_SEG = 1,     // (a,b) = F1, c = root span S0 (Eq. 1 with R5 margin); aux = face-local cold index
-  K_MOVE = 2,    // (a,b) = chain start; sets group start A and the previous point
-  K_MOVEG = 3,   // (a,b) = next chain start after a gap; crossing mode adds the gap terms
-  K_GROUP = 4,   // cull header: bbox (float4 in a,b for fp64; a,b,c + next record for fp32); aux = records to skip
-  K_LINE = 5,    // a = line coordinate; omega(p,L) = +-1/2
-  K_XCH = 6,     // extended copy closing (crossing mode): -c(A -> Z)
-  K_NCH = 7,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
-  K_CLOSEG = 8,  // open contractible loop: gap chord Z -> A (crossing mode)
-  K_PAD = 9,     // (unused)
-  K_SPAN = 10    // path-hierarchy node: (x,y) = end of the run, span = sum of its S0; aux = subtree records
+  K_SPAN = 2,    // path-hierarchy node: (x,y) = end of the run, span = sum of its S0; aux = subtree records
+  K_MOVE = 3,    // (a,b) = chain start; sets group start A and the previous point
+  K_MOVEG = 4,   // (a,b) = next chain start after a gap; crossing mode adds the gap terms
+  K_GROUP = 5,   // cull header: bbox (float4 in a,b for fp64; a,b,c + next record for fp32); aux = records to skip
+  K_LINE = 6,    // a = line coordinate; omega(p,L) = +-1/2
+  K_XCH = 7,     // extended copy closing (crossing mode): -c(A -> Z)
+  K_NCH = 8,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
+  K_CLOSEG = 9,  // open contractible loop: gap chord Z -> A (crossing mode)
+  K_PAD = 10     // (unused)
 };
+// SEG and SPAN (the records of the inner loop) are kinds 1 and 2: one compare
 constexpr uint32_t F_ANGLE = 1u << 4;   // literal atan2 chord angles (angle_mode = 1)
 constexpr uint32_t F_AXISV = 1u << 5;   // LINE parallel to v: test the u coordinate
 constexpr uint32_t F_GE = 1u << 6;      // LINE: left iff q >= c (else q <= c)

@@ -253,7 +253,7 @@ __device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px,
 template <typename R>
 struct HotView;
 template <>
-struct HotView<double> {   // explicit ld.shared of one 32-B record
+struct HotView<double> {   // one 32-B record: two ld.shared.v4 at a 32-bit shared address
   float fx, fy, fs;
   uint32_t meta;
   double x, y;
@@ -315,245 +315,266 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   const Tile T = P.tiles[blockIdx.x];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int f = T.face;
-  const uint8_t per = P.face_per[f];
-  const double *dom = P.face_dom + 4 * f;
-  bool valid = t < T.qcnt;
-  const int32_t pos = (int32_t)T.qbeg + t;
-  const int32_t qi = valid ? (*P.unsorted ? P.perm[pos] : pos) : 0;
-  double px = 0.0, py = 0.0;
-  if (valid) {
-    double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
-    if (!isfinite(u) || !isfinite(v)) {
-      P.winding[qi] = nan_d();
-      P.flag[qi] = 3;
-      valid = false;
-    } else {
-      if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
-      if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
-      if (!F64) { u = (double)(float)u; v = (double)(float)v; }
-      px = u;
-      py = v;
-    }
-  }
-  const float pxf = (float)px, pyf = (float)py;
+  const int rec0 = P.face_rec_off[f];
+  const int nrec = P.face_rec_off[f + 1] - rec0;
+  // a face program that fits one chunk is staged once and reused by every
+  // sub-tile of the unit (the copy overlaps the first query loads)
+  const bool single = nrec <= RCH;
   if (t == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
+    if (single && nrec > 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&s_bar, (unsigned)(nrec * sizeof(Hot<R>)));
+      tma_bulk_g2s(s_rec, P.hot + rec0, (unsigned)(nrec * sizeof(Hot<R>)), &s_bar);
+    }
   }
-  __syncthreads();
-
-  const int rec0 = P.face_rec_off[f];
-  const int nrec = P.face_rec_off[f + 1] - rec0;
+  const uint8_t per = P.face_per[f];
+  const double *dom = P.face_dom + 4 * f;
+  const int unsorted = *P.unsorted;
   const int cold0 = P.face_cold_off[f];
   const double eps = P.eps;
   // fp32-filter constant: a distance df > eps_c certifies d >= eps
   // (fp64 records; margins 2^-16 scale + 2^-17 relative)
   const float eps_c = F64 ? __double2float_ru((eps + P.face_M[f] * 0x1p24) * (1.0 + 0x1p-17)) : (float)eps;
-
-  double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
-  // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
-  double zx = 0.0, zy = 0.0;
-  float cdf = 0.f;
-  bool up = false, onb = false;
-  int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
-  int xs = 0, halves = 0, pend = 0;
-  double fr = 0.0;
+  // shared address of the record buffer, opaque to the compiler so that it is
+  // kept in a register instead of being recomputed in the inner loop
+  unsigned sbase;
+  asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(s_rec)));
+  unsigned phase = 0;
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0;
-  unsigned phase = 0;
-  int gr = 0;                    // warp-uniform record cursor
-  const unsigned sbase = smem_u32(s_rec);
+  __syncthreads();               // barrier initialised
 
-  // flush the warp's buffer to the global queue with one exact reservation;
-  // pairs past the capacity tag their query for the overflow kernel
-  auto flush = [&]() {
-    __syncwarp();
-    int b = 0;
-    if (lane == 0) b = atomicAdd(P.hq_count, hn_);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    bool ovf = false;
-    for (int i = lane; i < hn_; i += 32) {
-      if (b + i < P.hq_cap) P.hq[b + i] = s_hb[warp][i];
-      else ovf = true;
+  // one unit = up to QU queries of face f, processed QT at a time
+  for (int sub = 0; sub < T.qcnt; sub += QT) {
+    bool valid = sub + t < T.qcnt;
+    const int32_t pos = (int32_t)(T.qbeg + sub) + t;
+    const int32_t qi = valid ? (unsorted ? P.perm[pos] : pos) : 0;
+    double px = 0.0, py = 0.0;
+    if (valid) {
+      double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+      if (!isfinite(u) || !isfinite(v)) {
+        P.winding[qi] = nan_d();
+        P.flag[qi] = 3;
+        valid = false;
+      } else {
+        if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
+        if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
+        if (!F64) { u = (double)(float)u; v = (double)(float)v; }
+        px = u;
+        py = v;
+      }
     }
-    // an overflowing entry belongs to one of this warp's queries: tag them all
-    // that queued something in this batch (they are recomputed exactly)
-    if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
-    __syncwarp();
-    hn_ = 0;
-    pend &= ~4;
-  };
+    const float pxf = (float)px, pyf = (float)py;
 
-  for (int cb = 0; cb < nrec; cb += RCH) {
-    const int cn = min(RCH, nrec - cb);
-    if (t == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&s_bar, (unsigned)(cn * sizeof(Hot<R>)));
-      tma_bulk_g2s(s_rec, P.hot + rec0 + cb, (unsigned)(cn * sizeof(Hot<R>)), &s_bar);
-    }
-    while (!mbar_try_wait(&s_bar, phase)) {
-    }
-    phase ^= 1u;
-    const int ce = cb + cn;
-    while (gr < ce) {
-      HotView<R> h;
-      h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
-      const uint32_t meta = h.meta;
-      const uint32_t kind = meta & 0xFu;
-      const bool act = valid && gr >= skip_end;
-      if (COUNT && lane == 0) ++c_rec;
-      if (__builtin_expect(kind == K_SEG || kind == K_SPAN, 1)) {
-        // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
-        // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
-        // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
-        // ellipse, d >= eps"; a crossing / hard / uncertain lane takes the exact
-        // slow path.
-        bool u1;
-        float df;
-        if constexpr (F64) {
-          u1 = h.y >= py;                                      // exact side of the branch cut
-          df = fdist_ftz(h.fx - pxf, h.fy - pyf);
-        } else {
-          u1 = h.fy >= pyf;
-          const float dx = h.fx - pxf, dy = h.fy - pyf;
-          df = sqrtf(dx * dx + dy * dy);
+    double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
+    // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
+    double zx = 0.0, zy = 0.0;
+    float cdf = 0.f;
+    bool up = false, onb = false;
+    int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
+    int xs = 0, halves = 0, pend = 0;
+    double fr = 0.0;
+    int gr = 0;                    // warp-uniform record cursor
+
+    // flush the warp's buffer to the global queue with one exact reservation;
+    // pairs past the capacity tag their query for the overflow kernel
+    auto flush = [&]() {
+      __syncwarp();
+      int b = 0;
+      if (lane == 0) b = atomicAdd(P.hq_count, hn_);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      bool ovf = false;
+      for (int i = lane; i < hn_; i += 32) {
+        if (b + i < P.hq_cap) P.hq[b + i] = s_hb[warp][i];
+        else ovf = true;
+      }
+      // an overflowing entry belongs to one of this warp's queries: tag them all
+      // that queued something in this batch (they are recomputed exactly)
+      if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
+      __syncwarp();
+      hn_ = 0;
+      pend &= ~4;
+    };
+
+    for (int cb = 0; cb < nrec; cb += RCH) {
+      const int cn = min(RCH, nrec - cb);
+      if (!single) {
+        if (t == 0) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&s_bar, (unsigned)(cn * sizeof(Hot<R>)));
+          tma_bulk_g2s(s_rec, P.hot + rec0 + cb, (unsigned)(cn * sizeof(Hot<R>)), &s_bar);
         }
-        const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
-        if (kind == K_SPAN) {
-          if (COUNT && act) ++c_span;
-          // descend unless every active lane prunes the whole run
-          const bool descend = act && !pr;
-          if (!__any_sync(0xffffffffu, descend)) {
-            // every active lane substitutes the run's chord (homotopy)
-            if (__any_sync(0xffffffffu, act && (u1 != up || (meta & F_ANGLE)))) {
-              if (act) {
-                if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-                else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+        while (!mbar_try_wait(&s_bar, phase)) {
+        }
+        phase ^= 1u;
+      } else if (sub == 0) {
+        while (!mbar_try_wait(&s_bar, 0)) {
+        }
+      }
+      const int ce = cb + cn;
+      while (gr < ce) {
+        HotView<R> h;
+        h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
+        const uint32_t meta = h.meta;
+        const uint32_t kind = meta & 0xFu;
+        const bool act = valid && gr >= skip_end;
+        if (COUNT && lane == 0) ++c_rec;
+        if (__builtin_expect(kind - K_SEG < 2u, 1)) {   // SEG or SPAN
+          // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
+          // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
+          // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
+          // ellipse, d >= eps"; a crossing / hard / uncertain lane takes the exact
+          // slow path.
+          bool u1;
+          float df;
+          if constexpr (F64) {
+            u1 = h.y >= py;                                      // exact side of the branch cut
+            df = fdist_ftz(h.fx - pxf, h.fy - pyf);
+          } else {
+            u1 = h.fy >= pyf;
+            const float dx = h.fx - pxf, dy = h.fy - pyf;
+            df = sqrtf(dx * dx + dy * dy);
+          }
+          const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
+          if (kind == K_SPAN) {
+            if (COUNT && act) ++c_span;
+            // descend unless every active lane prunes the whole run
+            const bool descend = act && !pr;
+            if (!__any_sync(0xffffffffu, descend)) {
+              // every active lane substitutes the run's chord (homotopy)
+              if (__any_sync(0xffffffffu, act && (u1 != up || (meta & F_ANGLE)))) {
+                if (act) {
+                  if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                  else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+                }
+              }
+              if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
+              gr += (int)(meta >> 8);
+              if (COUNT && lane == 0) ++c_cull;
+            } else if (act && pr) {
+              // this lane prunes the run: chord now, inactive for the subtree
+              if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+              else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+              zx = h.x; zy = h.y; cdf = df; up = u1;
+              skip_end = gr + 1 + (int)(meta >> 8);
+            }
+          } else {
+            const bool need = act && (!pr || u1 != up || (meta & F_ANGLE));
+            if (__any_sync(0xffffffffu, need)) {
+              bool hard = false;
+              if (need) {
+                if (!(df > eps_c)) {                             // filter cannot certify d >= eps
+                  if constexpr (F64) {
+                    const double dx = h.x - px, dy = h.y - py;
+                    onb |= sqrt(dx * dx + dy * dy) < eps;
+                  } else {
+                    onb |= df < (float)eps;
+                  }
+                }
+                if (cdf + df > h.fs && !onb) {                   // pruned: chord (a5)
+                  if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                  else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+                } else {
+                  hard = !onb;                                   // exact recursion in phase 2
+                }
+              }
+              const unsigned m = __ballot_sync(0xffffffffu, hard);
+              if (m) {
+                const int cnt = __popc(m);
+                if (hn_ + cnt > HWB) flush();
+                if (hard) {
+                  HardEntry H;
+                  H.px = px;
+                  H.py = py;
+                  H.q = qi;
+                  H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
+                  s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
+                  pend |= 1 | 4;
+                  if (COUNT) ++c_hard;
+                }
+                hn_ += cnt;
               }
             }
             if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
-            gr += (int)(meta >> 8);
+            if (COUNT && act) ++c_pairs;
+          }
+        } else if (kind == K_MOVE || kind == K_MOVEG) {
+          const double nx = h.x - px, ny = h.y - py;
+          float nd;
+          if constexpr (F64) nd = fdist_ftz(h.fx - pxf, h.fy - pyf);
+          else nd = sqrtf((float)(nx * nx + ny * ny));
+          if (act) {
+            if (!(nd > eps_c)) onb |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
+            if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+              // gap chord Z -> A': -omega(p,Z,A') + its crossing
+              const double ax = zx - px, ay = zy - py;
+              const double cr = canon_cross(ax, ay, nx, ny);
+              fr -= atan2(cr, ax * nx + ay * ny);
+              xs += xcount_exact(ax, ay, nx, ny, cr);
+            }
+          }
+          if (kind == K_MOVE) { gax = h.x; gay = h.y; }
+          zx = h.x; zy = h.y; cdf = nd;
+          up = F64 ? (h.y >= py) : (h.fy >= pyf);
+        } else if (kind == K_GROUP) {
+          // copy-group / closed-loop cull: p outside the group's box => exactly 0
+          const bool out = !act || group_out_v(h, px, py);
+          const int skip = (int)(meta >> 8);
+          if (__all_sync(0xffffffffu, out)) {
+            gr += skip;
             if (COUNT && lane == 0) ++c_cull;
-          } else if (act && pr) {
-            // this lane prunes the run: chord now, inactive for the subtree
-            if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-            else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
-            zx = h.x; zy = h.y; cdf = df; up = u1;
-            skip_end = gr + 1 + (int)(meta >> 8);
+          } else if (out && act) {
+            skip_end = gr + 1 + skip;
           }
-        } else {
-          const bool need = act && (!pr || u1 != up || (meta & F_ANGLE));
-          if (__any_sync(0xffffffffu, need)) {
-            bool hard = false;
-            if (need) {
-              if (!(df > eps_c)) {                             // filter cannot certify d >= eps
-                if constexpr (F64) {
-                  const double dx = h.x - px, dy = h.y - py;
-                  onb |= sqrt(dx * dx + dy * dy) < eps;
-                } else {
-                  onb |= df < (float)eps;
-                }
-              }
-              if (cdf + df > h.fs && !onb) {                   // pruned: chord (a5)
-                if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-                else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
-              } else {
-                hard = !onb;                                   // exact recursion in phase 2
-              }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, hard);
-            if (m) {
-              const int cnt = __popc(m);
-              if (hn_ + cnt > HWB) flush();
-              if (hard) {
-                HardEntry H;
-                H.px = px;
-                H.py = py;
-                H.q = qi;
-                H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
-                s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
-                pend |= 1 | 4;
-                if (COUNT) ++c_hard;
-              }
-              hn_ += cnt;
+        } else if (kind == K_LINE) {
+          // omega(p,L) = +-1/2, p on L counts as left (R11)
+          const double q = (meta & F_AXISV) ? px : py;
+          const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
+          if (act) halves += left ? 1 : -1;
+        } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
+          if (act) {
+            const double cx = zx - px, cy = zy - py, ax = gax - px, ay = gay - py;
+            if (kind == K_XCH) {
+              xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
+            } else if (kind == K_NCH) {
+              fr -= chord_angle(ax, ay, cx, cy);
+            } else {
+              const double cr = canon_cross(cx, cy, ax, ay);
+              fr -= atan2(cr, cx * ax + cy * ay);
+              xs += xcount_exact(cx, cy, ax, ay, cr);
             }
           }
-          if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
-          if (COUNT && act) ++c_pairs;
         }
-      } else if (kind == K_MOVE || kind == K_MOVEG) {
-        const double nx = h.x - px, ny = h.y - py;
-        float nd;
-        if constexpr (F64) nd = fdist_ftz(h.fx - pxf, h.fy - pyf);
-        else nd = sqrtf((float)(nx * nx + ny * ny));
-        if (act) {
-          if (!(nd > eps_c)) onb |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
-          if (kind == K_MOVEG && !(meta & F_ANGLE)) {
-            // gap chord Z -> A': -omega(p,Z,A') + its crossing
-            const double ax = zx - px, ay = zy - py;
-            const double cr = canon_cross(ax, ay, nx, ny);
-            fr -= atan2(cr, ax * nx + ay * ny);
-            xs += xcount_exact(ax, ay, nx, ny, cr);
-          }
-        }
-        if (kind == K_MOVE) { gax = h.x; gay = h.y; }
-        zx = h.x; zy = h.y; cdf = nd;
-        up = F64 ? (h.y >= py) : (h.fy >= pyf);
-      } else if (kind == K_GROUP) {
-        // copy-group / closed-loop cull: p outside the group's box => exactly 0
-        const bool out = !act || group_out_v(h, px, py);
-        const int skip = (int)(meta >> 8);
-        if (__all_sync(0xffffffffu, out)) {
-          gr += skip;
-          if (COUNT && lane == 0) ++c_cull;
-        } else if (out && act) {
-          skip_end = gr + 1 + skip;
-        }
-      } else if (kind == K_LINE) {
-        // omega(p,L) = +-1/2, p on L counts as left (R11)
-        const double q = (meta & F_AXISV) ? px : py;
-        const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
-        if (act) halves += left ? 1 : -1;
-      } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
-        if (act) {
-          const double cx = zx - px, cy = zy - py, ax = gax - px, ay = gay - py;
-          if (kind == K_XCH) {
-            xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
-          } else if (kind == K_NCH) {
-            fr -= chord_angle(ax, ay, cx, cy);
-          } else {
-            const double cr = canon_cross(cx, cy, ax, ay);
-            fr -= atan2(cr, cx * ax + cy * ay);
-            xs += xcount_exact(cx, cy, ax, ay, cr);
-          }
-        }
+        ++gr;
       }
-      ++gr;
+      // all warps done with this chunk before it is overwritten (multi-chunk faces)
+      if (!single && (ce < nrec || sub + QT < T.qcnt)) __syncthreads();
     }
-    if (ce < nrec) __syncthreads();   // all warps done with this chunk before it is overwritten
-  }
-  if (hn_) flush();
+    if (hn_) flush();
 
-  // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
-  if (valid) {
-    if (onb) {
-      P.winding[qi] = nan_d();
-      P.flag[qi] = 2;
-      if (COUNT) atomicAdd(P.counters + 7, 1ull);
-    } else {
-      const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
-      P.winding[qi] = w;
-      if (!(pend & 3)) P.flag[qi] = classify(w, P.rule);
+    // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
+    if (valid) {
+      if (onb) {
+        P.winding[qi] = nan_d();
+        P.flag[qi] = 2;
+        if (COUNT) atomicAdd(P.counters + 7, 1ull);
+      } else {
+        const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
+        P.winding[qi] = w;
+        if (!(pend & 3)) P.flag[qi] = classify(w, P.rule);
+      }
     }
-  }
-  const bool pq = valid && !onb && (pend & 3);
-  const unsigned pm = __ballot_sync(0xffffffffu, pq);
-  if (pm) {
-    int base = 0;
-    if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
-    if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((pend & 2) ? (int32_t)0x80000000 : 0);
+    const bool pq = valid && !onb && (pend & 3);
+    const unsigned pm = __ballot_sync(0xffffffffu, pq);
+    if (pm) {
+      int base = 0;
+      if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
+      if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((pend & 2) ? (int32_t)0x80000000 : 0);
+    }
   }
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
@@ -722,14 +743,14 @@ __global__ void k_scatter(int64_t n, const int32_t *__restrict__ face_id, int32_
   }
 }
 
-__global__ void k_ntiles(int32_t n_faces, const int32_t *__restrict__ order, const int32_t *__restrict__ cnt,
-                         int32_t *__restrict__ nt) {
+__global__ void k_ntiles(int32_t n_faces, int32_t qu, const int32_t *__restrict__ order,
+                         const int32_t *__restrict__ cnt, int32_t *__restrict__ nt) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n_faces) nt[j] = (cnt[order[j]] + QT - 1) / QT;
+  if (j < n_faces) nt[j] = (cnt[order[j]] + qu - 1) / qu;
   if (j == n_faces) nt[j] = 0;
 }
 
-__global__ void k_tiles(int32_t n_faces, int32_t max_tiles, const int32_t *__restrict__ order,
+__global__ void k_tiles(int32_t n_faces, int32_t max_tiles, int32_t qu, const int32_t *__restrict__ order,
                         const int32_t *__restrict__ cnt, const int32_t *__restrict__ off,
                         const int32_t *__restrict__ toff, Tile *__restrict__ tiles, int32_t *__restrict__ ntiles) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -745,8 +766,8 @@ __global__ void k_tiles(int32_t n_faces, int32_t max_tiles, const int32_t *__res
   const int k = i - toff[lo];
   Tile T;
   T.face = f;
-  T.qbeg = off[f] + k * QT;
-  T.qcnt = min(QT, cnt[f] - k * QT);
+  T.qbeg = off[f] + (int64_t)k * qu;
+  T.qcnt = min(qu, cnt[f] - k * qu);
   tiles[i] = T;
 }
 
@@ -756,7 +777,13 @@ template <typename R>
 static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id, const double *uv,
                                 double *winding, uint8_t *flag, cudaStream_t st) {
   const int nf = F->n_faces;
-  const int64_t max_tiles64 = (n + QT - 1) / QT + nf;
+  // unit = up to qu queries of one face per CTA (QT at a time): large batches
+  // amortise the CTA prologue and the record staging over several sub-tiles,
+  // small ones keep >= ~4 waves of CTAs
+  int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
+  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(64, atoi(s)));
+  const int qu = QT * sub;
+  const int64_t max_tiles64 = (n + qu - 1) / qu + nf;
   if (n > INT32_MAX - 1 || max_tiles64 > INT32_MAX) {
     set_error("wn_query: batch too large (n=%lld); split it", (long long)n);
     return WN_ERR_ARG;
@@ -801,11 +828,11 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   launches += 2;
   k_scatter<<<nb, TB, 0, st>>>(n, face_id, nf, off, cur, flags, perm);
   ++launches;
-  k_ntiles<<<(nf + 1 + TB - 1) / TB, TB, 0, st>>>(nf, F->face_order, cnt, nt);
+  k_ntiles<<<(nf + 1 + TB - 1) / TB, TB, 0, st>>>(nf, qu, F->face_order, cnt, nt);
   ++launches;
   cub::DeviceScan::ExclusiveSum(tmpb, tmp, nt, toff, nf + 1, st);
   launches += 2;
-  k_tiles<<<(max_tiles + TB - 1) / TB, TB, 0, st>>>(nf, max_tiles, F->face_order, cnt, off, toff, tiles,
+  k_tiles<<<(max_tiles + TB - 1) / TB, TB, 0, st>>>(nf, max_tiles, qu, F->face_order, cnt, off, toff, tiles,
                                                    flags + 1);
   ++launches;
   QParams<R> P;

@@ -88,8 +88,6 @@ struct QParams {
   HardEntry *hq;          // global hard-pair queue
   int32_t *hq_count;
   int32_t hq_cap;
-  int32_t *pend;          // queries with queued hard pairs
-  int32_t *pend_count;
   double eps;
   int max_depth;
   int rule;
@@ -298,6 +296,10 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
   return r * rs;
 }
 
+// intermediate flag values between phase 1 and k_finish / k_overflow
+constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classifies
+constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
+
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 
 #ifndef WN_P1_MINB
@@ -345,6 +347,33 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0;
   __syncthreads();               // barrier initialised
+  // pend bits of the lane's current query: 1 hard pairs queued, 2 one of them
+  // overflowed the queue, 4 entries still in the warp buffer
+  int pend = 0;
+
+  // flush the warp's buffer to the global queue with one exact reservation.
+  // Entries past the capacity mark their query FLAG_OVERFLOW (recomputed
+  // exactly by k_overflow); the lane's own current query also keeps bit 2
+  // because its final flag is written after this.
+  auto flush = [&]() {
+    __syncwarp();
+    int b = 0;
+    if (lane == 0) b = atomicAdd(P.hq_count, hn_);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    bool ovf = false;
+    for (int i = lane; i < hn_; i += 32) {
+      if (b + i < P.hq_cap) {
+        P.hq[b + i] = s_hb[warp][i];
+      } else {
+        P.flag[s_hb[warp][i].q] = FLAG_OVERFLOW;
+        ovf = true;
+      }
+    }
+    if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
+    __syncwarp();
+    hn_ = 0;
+    pend &= ~4;
+  };
 
   // one unit = up to QU queries of face f, processed QT at a time
   for (int sub = 0; sub < T.qcnt; sub += QT) {
@@ -374,29 +403,10 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     float cdf = 0.f;
     bool up = false, onb = false;
     int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
-    int xs = 0, halves = 0, pend = 0;
+    int xs = 0, halves = 0;
+    pend = 0;
     double fr = 0.0;
     int gr = 0;                    // warp-uniform record cursor
-
-    // flush the warp's buffer to the global queue with one exact reservation;
-    // pairs past the capacity tag their query for the overflow kernel
-    auto flush = [&]() {
-      __syncwarp();
-      int b = 0;
-      if (lane == 0) b = atomicAdd(P.hq_count, hn_);
-      b = __shfl_sync(0xffffffffu, b, 0);
-      bool ovf = false;
-      for (int i = lane; i < hn_; i += 32) {
-        if (b + i < P.hq_cap) P.hq[b + i] = s_hb[warp][i];
-        else ovf = true;
-      }
-      // an overflowing entry belongs to one of this warp's queries: tag them all
-      // that queued something in this batch (they are recomputed exactly)
-      if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
-      __syncwarp();
-      hn_ = 0;
-      pend &= ~4;
-    };
 
     for (int cb = 0; cb < nrec; cb += RCH) {
       const int cn = min(RCH, nrec - cb);
@@ -552,7 +562,6 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       // all warps done with this chunk before it is overwritten (multi-chunk faces)
       if (!single && (ce < nrec || sub + QT < T.qcnt)) __syncthreads();
     }
-    if (hn_) flush();
 
     // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
     if (valid) {
@@ -563,19 +572,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       } else {
         const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
         P.winding[qi] = w;
-        if (!(pend & 3)) P.flag[qi] = classify(w, P.rule);
+        P.flag[qi] = (pend & 2) ? FLAG_OVERFLOW : (pend & 1) ? FLAG_PENDING : classify(w, P.rule);
       }
     }
-    const bool pq = valid && !onb && (pend & 3);
-    const unsigned pm = __ballot_sync(0xffffffffu, pq);
-    if (pm) {
-      int base = 0;
-      if (lane == 0) base = atomicAdd(P.pend_count, __popc(pm));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      // bit 31 tags queries whose hard pairs overflowed the queue (k_overflow)
-      if (pq) P.pend[base + __popc(pm & ((1u << lane) - 1u))] = qi | ((pend & 2) ? (int32_t)0x80000000 : 0);
-    }
   }
+  if (hn_) flush();   // entries of finished queries: overflow marks their flags directly
   if (COUNT) {
     cnt_add<COUNT>(P.counters, 0, c_pairs);
     cnt_add<COUNT>(P.counters, 1, c_hard);
@@ -611,12 +612,10 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
 // program again for that query, exact root tests against the (valid, inflated)
 // stored span and the recursion inline.  Normally never has work.
 template <typename R>
-__global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id) {
-  const int total = *P.pend_count;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int e = P.pend[i];
-    if (e >= 0) continue;
-    const int qi = e & 0x7fffffff;
+__global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id, int64_t n) {
+  if (*P.hq_count <= P.hq_cap) return;   // nothing overflowed (uniform)
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < n; qi += (int64_t)gridDim.x * blockDim.x) {
+    if (P.flag[qi] != FLAG_OVERFLOW) continue;
     const int f = face_id[qi];
     double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
     const uint8_t per = P.face_per[f];
@@ -682,21 +681,38 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id) {
   }
 }
 
-// K3c: classify the queries that had hard pairs (a8)
-__global__ void k_finish(const int32_t *__restrict__ pend, const int32_t *__restrict__ pend_count,
-                         const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
+// K3c: classify the queries that had hard pairs (a8): every FLAG_PENDING entry
+// of the flag array (4 flags per thread when the array is word aligned)
+__device__ __forceinline__ uint8_t finish_one(uint8_t fl, const double *__restrict__ winding, int64_t q, int rule,
+                                              unsigned long long *counters) {
+  if (fl != FLAG_PENDING) return fl;
+  const double w = winding[q];
+  if (isnan(w)) {
+    if (counters) atomicAdd(counters + 7, 1ull);
+    return 2;
+  }
+  return classify(w, rule);
+}
+
+__global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
                          unsigned long long *counters) {
-  const int total = *pend_count;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int q = pend[i];
-    if (q < 0) continue;   // overflow query: finished by k_overflow
-    const double w = winding[q];
-    if (isnan(w)) {
-      flag[q] = 2;
-      if (counters) atomicAdd(counters + 7, 1ull);
-    } else {
-      flag[q] = classify(w, rule);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (((uintptr_t)flag & 3) == 0) {
+    const int64_t nw = n >> 2;
+    uint32_t *fw = reinterpret_cast<uint32_t *>(flag);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += stride) {
+      uint32_t v = fw[i];
+      if ((v & 0x80808080u) == 0) continue;   // final flags are 0..3
+      uint32_t o = 0;
+      for (int k = 0; k < 4; ++k)
+        o |= (uint32_t)finish_one((uint8_t)(v >> (8 * k)), winding, 4 * i + k, rule, counters) << (8 * k);
+      fw[i] = o;
     }
+    for (int64_t q = (nw << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += stride)
+      flag[q] = finish_one(flag[q], winding, q, rule, counters);
+  } else {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += stride)
+      flag[q] = finish_one(flag[q], winding, q, rule, counters);
   }
 }
 
@@ -803,7 +819,6 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const size_t o_toff = carve(sizeof(int32_t) * (nf + 1));
   const size_t o_tiles = carve(sizeof(Tile) * (size_t)max_tiles);
   const size_t o_perm = carve(sizeof(int32_t) * (size_t)n);
-  const size_t o_pend = carve(sizeof(int32_t) * (size_t)n);
   const size_t o_hq = carve(sizeof(HardEntry) * (size_t)hq_cap);
   const size_t o_tmp = carve(tmp);
   char *base = nullptr;
@@ -813,7 +828,6 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   int32_t *toff = (int32_t *)(base + o_toff), *flags = (int32_t *)(base + o_flags);
   Tile *tiles = (Tile *)(base + o_tiles);
   int32_t *perm = (int32_t *)(base + o_perm);
-  int32_t *pend = (int32_t *)(base + o_pend);
   HardEntry *hq = (HardEntry *)(base + o_hq);
   void *tmpb = base + o_tmp;
   int launches = 0;
@@ -853,8 +867,6 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.hq = hq;
   P.hq_count = flags + 2;
   P.hq_cap = hq_cap;
-  P.pend = pend;
-  P.pend_count = flags + 3;
   P.eps = F->eps;
   P.max_depth = F->max_depth;
   P.rule = F->opt.rule;
@@ -872,14 +884,14 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     k_phase1<R, true><<<max_tiles, NTH, 0, st>>>(P);
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
-    k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
-    k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, F->counters);
+    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, winding, flag, P.rule, F->counters);
   } else {
     k_phase1<R, false><<<max_tiles, NTH, 0, st>>>(P);
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
-    k_overflow<R><<<148, 128, 0, st>>>(P, face_id);
-    k_finish<<<148 * 4, 256, 0, st>>>(pend, flags + 3, winding, flag, P.rule, nullptr);
+    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, winding, flag, P.rule, nullptr);
   }
   launches += 4;
   if (F->timing_on) {

@@ -697,18 +697,39 @@ __device__ __forceinline__ uint8_t finish_one(uint8_t fl, const double *__restri
 __global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
                          unsigned long long *counters) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  if (((uintptr_t)flag & 3) == 0) {
-    const int64_t nw = n >> 2;
-    uint32_t *fw = reinterpret_cast<uint32_t *>(flag);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += stride) {
-      uint32_t v = fw[i];
-      if ((v & 0x80808080u) == 0) continue;   // final flags are 0..3
-      uint32_t o = 0;
-      for (int k = 0; k < 4; ++k)
-        o |= (uint32_t)finish_one((uint8_t)(v >> (8 * k)), winding, 4 * i + k, rule, counters) << (8 * k);
-      fw[i] = o;
+  if (((uintptr_t)flag & 15) == 0) {
+    const int64_t nv = n >> 4;
+    uint4 *fv = reinterpret_cast<uint4 *>(flag);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+      uint4 v = fv[i];
+      if (((v.x | v.y | v.z | v.w) & 0x80808080u) == 0) continue;   // final flags are 0..3
+      // all 16 windings in flight at once (a pending group has several)
+      double wv[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) wv[k] = winding[16 * i + k];
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t o = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint8_t fl = (uint8_t)(w[j] >> (8 * k));
+          if (fl == FLAG_PENDING) {
+            const double x = wv[4 * j + k];
+            if (isnan(x)) {
+              fl = 2;
+              if (counters) atomicAdd(counters + 7, 1ull);
+            } else {
+              fl = classify(x, rule);
+            }
+          }
+          o |= (uint32_t)fl << (8 * k);
+        }
+        w[j] = o;
+      }
+      fv[i] = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    for (int64_t q = (nw << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += stride)
+    for (int64_t q = (nv << 4) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += stride)
       flag[q] = finish_one(flag[q], winding, q, rule, counters);
   } else {
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += stride)
@@ -720,24 +741,61 @@ __global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t 
 // K4: bucketing by face (a3).  Histogram with warp-aggregated atomics and a
 // sortedness flag; scatter only when the batch is not grouped by face.
 // ---------------------------------------------------------------------------
+// Histogram by runs: the count of face f is the sum over maximal runs of f of
+// (end - start), so each run adds -start at its first and end at its last
+// element -- two atomics per run (a face-sorted batch: two per face).  Four ids
+// per thread (16-B loads when aligned); run neighbours across threads via
+// shuffles, across warps from global memory.  Invalid ids are flagged (3) and
+// belong to no run.
+__device__ __forceinline__ int hist_key(int f, int n_faces) { return (f >= 0 && f < n_faces) ? f : -1; }
+
 __global__ void k_hist(int64_t n, const int32_t *__restrict__ face_id, int32_t n_faces,
                        int32_t *__restrict__ cnt, int32_t *__restrict__ unsorted,
                        double *__restrict__ winding, uint8_t *__restrict__ flag) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i - threadIdx.x < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool in = i < n;
-    int f = in ? face_id[i] : -1;
-    const bool ok = in && f >= 0 && f < n_faces;
-    if (in && !ok) {
-      winding[i] = __longlong_as_double(0x7ff8000000000000LL);
-      flag[i] = 3;
+  constexpr int G = 8;   // ids per thread (two 16-B loads in flight)
+  const bool vec = ((uintptr_t)face_id & 15) == 0;
+  const int64_t ng = (n + G - 1) / G;
+  const int lane = threadIdx.x & 31;
+  bool uns = false;
+  for (int64_t g0 = blockIdx.x * (int64_t)blockDim.x; g0 < ng; g0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = g0 + threadIdx.x;
+    const int64_t i0 = g * G;
+    int id[G];
+    if (g < ng && vec && i0 + G - 1 < n) {
+      const int4 v0 = *reinterpret_cast<const int4 *>(face_id + i0);
+      const int4 v1 = *reinterpret_cast<const int4 *>(face_id + i0 + 4);
+      id[0] = v0.x; id[1] = v0.y; id[2] = v0.z; id[3] = v0.w;
+      id[4] = v1.x; id[5] = v1.y; id[6] = v1.z; id[7] = v1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < G; ++k) id[k] = (g < ng && i0 + k < n) ? face_id[i0 + k] : INT32_MIN;
     }
-    if (in && i > 0 && face_id[i - 1] > face_id[i]) atomicOr(unsorted, 1);
-    const int key = ok ? f : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = __ffs(peers) - 1;
-    if (ok && (int)(threadIdx.x & 31) == leader) atomicAdd(&cnt[f], __popc(peers));
+    // raw neighbours: previous id (i0-1) and next id (i0+G)
+    int prv = __shfl_up_sync(0xffffffffu, id[G - 1], 1);
+    int nxt = __shfl_down_sync(0xffffffffu, id[0], 1);
+    if (lane == 0) prv = (g < ng && i0 > 0) ? face_id[i0 - 1] : INT32_MIN;
+    if (lane == 31 || g + 1 >= ng) nxt = (g < ng && i0 + G < n) ? face_id[i0 + G] : INT32_MIN;
+    if (g < ng) {
+#pragma unroll
+      for (int k = 0; k < G; ++k) {
+        const int64_t i = i0 + k;
+        if (i >= n) break;
+        const int f = id[k];
+        const int pf = k ? id[k - 1] : prv;
+        const int nf_ = (k < G - 1 && i + 1 < n) ? id[k + 1] : nxt;
+        if (i > 0 && pf > f) uns = true;
+        const int key = hist_key(f, n_faces);
+        if (key < 0) {
+          winding[i] = __longlong_as_double(0x7ff8000000000000LL);
+          flag[i] = 3;
+          continue;
+        }
+        if (i == 0 || hist_key(pf, n_faces) != key) atomicAdd(&cnt[key], -(int32_t)i);
+        if (i + 1 >= n || hist_key(nf_, n_faces) != key) atomicAdd(&cnt[key], (int32_t)(i + 1));
+      }
+    }
   }
+  if (__any_sync(0xffffffffu, uns) && lane == 0) atomicOr(unsorted, 1);
 }
 
 __global__ void k_scatter(int64_t n, const int32_t *__restrict__ face_id, int32_t n_faces,
@@ -836,7 +894,9 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const int TB = 256;
   const int64_t nb64 = (n + TB - 1) / TB;
   const int nb = (int)(nb64 < 148 * 32 ? nb64 : 148 * 32);
-  k_hist<<<nb, TB, 0, st>>>(n, face_id, nf, cnt, flags, winding, flag);
+  const int64_t nbh64 = ((n + 7) / 8 + TB - 1) / TB;
+  const int nbh = (int)(nbh64 < 148 * 16 ? nbh64 : 148 * 16);
+  k_hist<<<nbh, TB, 0, st>>>(n, face_id, nf, cnt, flags, winding, flag);
   ++launches;
   cub::DeviceScan::ExclusiveSum(tmpb, tmp, cnt, off, nf + 1, st);
   launches += 2;

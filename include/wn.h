@@ -82,8 +82,13 @@ typedef struct {                 /* [host] */
  *   stream        cudaStream_t (0 = legacy default stream).
  *   out           [host] receives the handle on WN_OK; untouched otherwise.
  *   face_status   [n_faces] DEVICE int32 or NULL: WN_FACE_* per face.
- * Performs one stream synchronisation (topology validation / planning).  The
- * input buffers may be freed once it returns. */
+ * The host waits only for the per-loop summaries (topology validation and
+ * planning need them); derivative bounds and record emission stay asynchronous
+ * on `stream` after the call returns.  The input buffers must therefore stay
+ * valid until that work completes: free them in stream order on `stream` (a
+ * caching allocator on the same stream) or after synchronising it.  Queries
+ * may be issued at once on any stream (wn_query waits for the build's event);
+ * wn_free_faces orders its frees after the handle's last build/query. */
 wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, const double *ctrl_uv,
                            const double *ctrl_w, const int32_t *seg_degree,
                            const int32_t *loop_seg_off, const int32_t *face_loop_off,

@@ -169,6 +169,11 @@ class Faces:
                                   _ptr(status))
         if rc != WN_OK:
             raise WNError(rc, last_error(), status[:nf].cpu().numpy())
+        if stream is not None and hasattr(stream, "cuda_stream"):
+            # the build is asynchronous on `stream`: keep the inputs alive on it
+            for t in (ctrl, w, deg, lso, flo, per, dom, status):
+                if t is not None and t.is_cuda:
+                    t.record_stream(stream)
         return cls(h, device, nf, opts)
 
     @classmethod

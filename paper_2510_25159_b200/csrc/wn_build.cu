@@ -214,7 +214,12 @@ __global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__r
   const int q = (int)(idx / n_segs);
   const int s = order ? order[idx % n_segs] : (int)(idx % n_segs);   // degree-sorted: warp-uniform N
   const int o = coff[s];
-  switch (deg[s]) {
+  const int n = deg[s];
+  if (n < 1 || n > 5) {   // rejected on the host (k_deg flag); never read past the arrays
+    if (q == 8) { serr[s] = 1; prep[s].B = prep[s].S0 = 0.0; } else { prep[s].Bq[q] = 0.0; }
+    return;
+  }
+  switch (n) {
     case 1: prep_n<1>(ctrl, w, o, q, prep + s, serr + s); break;
     case 2: prep_n<2>(ctrl, w, o, q, prep + s, serr + s); break;
     case 3: prep_n<3>(ctrl, w, o, q, prep + s, serr + s); break;
@@ -228,10 +233,12 @@ __global__ void k_iota(int32_t n, int32_t *__restrict__ a) {
   if (i < n) a[i] = i;
 }
 
-__global__ void k_loop_face(int32_t n_faces, const int32_t *__restrict__ face_off, int32_t *__restrict__ loop_face) {
+__global__ void k_loop_face(int32_t n_faces, int32_t n_loops, const int32_t *__restrict__ face_off,
+                            int32_t *__restrict__ loop_face) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n_faces) return;
-  for (int l = face_off[f]; l < face_off[f + 1]; ++l) loop_face[l] = f;
+  const int l0 = max(face_off[f], 0), l1 = min(face_off[f + 1], n_loops);   // clamped (validated on the host)
+  for (int l = l0; l < l1; ++l) loop_face[l] = f;
 }
 
 __device__ __forceinline__ double lat(double x, int k, double T) { return __dadd_rn(x, __dmul_rn((double)k, T)); }
@@ -243,77 +250,153 @@ __device__ __forceinline__ double lat(double x, int k, double T) { return __dadd
 // Homology class = round(closure / T).  Junctions that are not
 // bit-continuous after lifting are recorded as chain breaks.
 // ---------------------------------------------------------------------------
-__global__ void k_lift(int32_t n_loops, const int32_t *__restrict__ loop_off, const int32_t *__restrict__ loop_face,
-                       const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
-                       const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
-                       const double *__restrict__ ctrl, const uint8_t *__restrict__ serr,
-                       const SegPrep *__restrict__ prep, int2 *__restrict__ shift, uint8_t *__restrict__ brk,
-                       int2 *__restrict__ chain, double *__restrict__ s0pre, LoopInfo *__restrict__ info) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, int32_t n_segs,
+                                              const int32_t *__restrict__ loop_off,
+                                              const int32_t *__restrict__ loop_face,
+                                              const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
+                                              const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
+                                              const double *__restrict__ ctrl, const double *__restrict__ wts,
+                                              int2 *__restrict__ shift, uint8_t *__restrict__ brk,
+                                              int2 *__restrict__ chain, double2 *__restrict__ lend,
+                                              LoopInfo *__restrict__ info) {
+  // one warp per loop; lanes take its segments 32 at a time.  The lattice
+  // shifts are a sequential recurrence (each segment continues from the
+  // lifted end of the previous one, R17/R18): the warp walks a chunk's 32
+  // segments in order with broadcast end points; everything else is parallel.
+  const int l = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (l >= n_loops) return;
   const int f = loop_face[l];
-  const int pu = face_per[f] & 1, pv = (face_per[f] >> 1) & 1;
-  const double Tu = face_dom[4 * f + 1], Tv = face_dom[4 * f + 3];
-  int ku = 0, kv = 0, nbrk = 0, err = 0;
-  double ex = 0, ey = 0, sx = 0, sy = 0;
+  const bool fok = f >= 0 && f < n_faces;   // -1: loop outside every face (bad CSR, rejected on the host)
+  const int pu = fok ? face_per[f] & 1 : 0, pv = fok ? (face_per[f] >> 1) & 1 : 0;
+  const double Tu = fok ? face_dom[4 * f + 1] : 0.0, Tv = fok ? face_dom[4 * f + 3] : 0.0;
+  const int s0 = min(max(loop_off[l], 0), n_segs), s1 = min(max(loop_off[l + 1], s0), n_segs);
+  double ex = 0, ey = 0;           // lifted end of the previous segment (uniform)
+  double sx = 0, sy = 0;
+  int nbrk = 0, err = 0, cs = 0;   // cs: chain start (loop index) carried across chunks
   double xmin = INFINITY, ymin = INFINITY, xmax = -INFINITY, ymax = -INFINITY;
-  const int s0 = loop_off[l], s1 = loop_off[l + 1];
-  for (int s = s0; s < s1; ++s) {
-    const int n = deg[s];
-    const int o = coff[s];
-    err |= serr[s];
-    const double x0 = ctrl[2 * o], y0 = ctrl[2 * o + 1];
-    if (s > s0) {
-      if (pu) ku = (int)round(__ddiv_rn(__dsub_rn(ex, x0), Tu));
-      if (pv) kv = (int)round(__ddiv_rn(__dsub_rn(ey, y0), Tv));
+  for (int base = s0; base < s1; base += 32) {
+    const int s = base + lane;
+    const bool in = s < s1;
+    const int cnt = min(32, s1 - base);
+    double x0 = 0, y0 = 0, xe = 0, ye = 0, bx0 = INFINITY, by0 = INFINITY, bx1 = -INFINITY, by1 = -INFINITY;
+    bool e = false;
+    if (in) {
+      int n = deg[s];
+      const int o = coff[s];
+      if (n < 1 || n > 5) { e = true; n = -1; }   // rejected on the host (k_deg flag)
+      for (int j = 0; j <= n; ++j) {
+        const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = wts ? wts[o + j] : 1.0;
+        e |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
+        bx0 = fmin(bx0, x); bx1 = fmax(bx1, x);
+        by0 = fmin(by0, y); by1 = fmax(by1, y);
+        if (j == 0) { x0 = x; y0 = y; }
+        if (j == n) { xe = x; ye = y; }
+      }
     }
-    shift[s] = make_int2(ku, kv);
-    const double lx0 = pu ? lat(x0, ku, Tu) : x0, ly0 = pv ? lat(y0, kv, Tv) : y0;
-    if (s > s0) {
-      const bool b = !(lx0 == ex && ly0 == ey);
-      brk[s] = b;
-      nbrk += b;
-    } else {
-      brk[s] = 0;
-      sx = lx0;
-      sy = ly0;
+    err |= __any_sync(0xffffffffu, e);
+    // shifts: sequential over the chunk (uniform loop, broadcast operands);
+    // a loop of a non-periodic face only compares each start with the previous end
+    int ku = 0, kv = 0;
+    bool bk = false;
+    if (!pu && !pv) {
+      double pxe = __shfl_up_sync(0xffffffffu, xe, 1), pye = __shfl_up_sync(0xffffffffu, ye, 1);
+      if (lane == 0) { pxe = ex; pye = ey; }
+      bk = in && s > s0 && !(x0 == pxe && y0 == pye);
+      if (base == s0) { sx = __shfl_sync(0xffffffffu, x0, 0); sy = __shfl_sync(0xffffffffu, y0, 0); }
+      ex = __shfl_sync(0xffffffffu, xe, cnt - 1);
+      ey = __shfl_sync(0xffffffffu, ye, cnt - 1);
     }
-    for (int j = 0; j <= n; ++j) {
-      const double x = pu ? lat(ctrl[2 * (o + j)], ku, Tu) : ctrl[2 * (o + j)];
-      const double y = pv ? lat(ctrl[2 * (o + j) + 1], kv, Tv) : ctrl[2 * (o + j) + 1];
-      xmin = fmin(xmin, x); xmax = fmax(xmax, x);
-      ymin = fmin(ymin, y); ymax = fmax(ymax, y);
-      if (j == n) { ex = x; ey = y; }
+    for (int j = 0; (pu || pv) && j < cnt; ++j) {
+      const double x0j = __shfl_sync(0xffffffffu, x0, j), y0j = __shfl_sync(0xffffffffu, y0, j);
+      const double xej = __shfl_sync(0xffffffffu, xe, j), yej = __shfl_sync(0xffffffffu, ye, j);
+      int kuj = 0, kvj = 0;
+      if (base + j > s0) {
+        if (pu) kuj = (int)round(__ddiv_rn(__dsub_rn(ex, x0j), Tu));
+        if (pv) kvj = (int)round(__ddiv_rn(__dsub_rn(ey, y0j), Tv));
+      }
+      const double lx0 = pu ? lat(x0j, kuj, Tu) : x0j, ly0 = pv ? lat(y0j, kvj, Tv) : y0j;
+      const bool bj = (base + j > s0) && !(lx0 == ex && ly0 == ey);
+      if (base + j == s0) { sx = lx0; sy = ly0; }
+      if (lane == j) { ku = kuj; kv = kvj; bk = bj; }
+      ex = pu ? lat(xej, kuj, Tu) : xej;
+      ey = pv ? lat(yej, kvj, Tv) : yej;
     }
+    if (in) {
+      shift[s] = make_int2(ku, kv);
+      brk[s] = bk;
+      // lifted box and end point: lat() is monotone, so it commutes with min/max
+      bx0 = pu ? lat(bx0, ku, Tu) : bx0; bx1 = pu ? lat(bx1, ku, Tu) : bx1;
+      by0 = pv ? lat(by0, kv, Tv) : by0; by1 = pv ? lat(by1, kv, Tv) : by1;
+      lend[s] = make_double2(pu ? lat(xe, ku, Tu) : xe, pv ? lat(ye, kv, Tv) : ye);
+    }
+    xmin = fmin(xmin, bx0); xmax = fmax(xmax, bx1);
+    ymin = fmin(ymin, by0); ymax = fmax(ymax, by1);
+    // chain starts: the last break (or the loop start) at or before s
+    const unsigned bm = __ballot_sync(0xffffffffu, in && (bk || s == s0));
+    nbrk += __popc(__ballot_sync(0xffffffffu, in && bk));
+    const unsigned upto = bm & ((2u << lane) - 1u);
+    const int my_cs = upto ? (base + 31 - __clz(upto)) - s0 : cs;
+    if (in) chain[s].x = my_cs;
+    if (bm) cs = (base + 31 - __clz(bm)) - s0;
   }
-  // chains (maximal bit-continuous runs) and the prefix of root spans along the
-  // loop: the path-hierarchy bounds are built from them in k_emit
-  {
-    int cs = 0;
-    double acc = 0.0;
-    for (int s = s0; s < s1; ++s) {
-      if (s == s0 || brk[s]) cs = s - s0;
-      chain[s].x = cs;
-      acc += prep[s].S0;
-      s0pre[s] = acc;
-    }
-    int ce = s1 - s0 - 1;
-    for (int s = s1 - 1; s >= s0; --s) {
-      chain[s].y = ce - chain[s].x + 1;
-      if (s == s0 || brk[s]) ce = s - s0 - 1;
-    }
+  // chain lengths: next chain start after s (backward over the chunks)
+  __syncwarp();
+  int nxt = s1 - s0;                 // first chain start after the current chunk
+  for (int base = s0 + ((s1 - s0 - 1) / 32) * 32; base >= s0 && s1 > s0; base -= 32) {
+    const int s = base + lane;
+    const bool in = s < s1;
+    const bool st = in && (s == s0 || brk[s]);
+    const unsigned bm = __ballot_sync(0xffffffffu, st);
+    const unsigned after = bm & ~((2u << lane) - 1u);   // chain starts strictly after s
+    const int ce = after ? (base + __ffs(after) - 1) - s0 : nxt;
+    if (in) chain[s].y = ce - chain[s].x;
+    if (bm) nxt = (base + __ffs(bm) - 1) - s0;
   }
-  LoopInfo I;
-  I.cu = (pu && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ex, sx), Tu)) : 0;
-  I.cv = (pv && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ey, sy), Tv)) : 0;
-  I.nbrk = nbrk;
-  I.closed = (s1 > s0) && ex == sx && ey == sy;
-  I.err = err;
-  I.nseg = s1 - s0;
-  I.sx = sx;
-  I.sy = sy;
-  I.bb[0] = xmin; I.bb[1] = ymin; I.bb[2] = xmax; I.bb[3] = ymax;
-  info[l] = I;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    xmin = fmin(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
+    ymin = fmin(ymin, __shfl_xor_sync(0xffffffffu, ymin, o));
+    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    ymax = fmax(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
+  }
+  if (lane == 0) {
+    LoopInfo I;
+    I.cu = (pu && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ex, sx), Tu)) : 0;
+    I.cv = (pv && s1 > s0) ? (int)round(__ddiv_rn(__dsub_rn(ey, sy), Tv)) : 0;
+    I.nbrk = nbrk;
+    I.closed = (s1 > s0) && ex == sx && ey == sy;
+    I.err = err;
+    I.nseg = s1 - s0;
+    I.sx = sx;
+    I.sy = sy;
+    I.bb[0] = xmin; I.bb[1] = ymin; I.bb[2] = xmax; I.bb[3] = ymax;
+    info[l] = I;
+  }
+}
+
+// prefix sums of the root spans S0 along each loop (warp per loop, after K1);
+// the path-hierarchy spans are differences of them.  Summation
+// order differs from a serial sum by a few ulps, far inside the R5 margin.
+__global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, const int32_t *__restrict__ loop_off,
+                                               const SegPrep *__restrict__ prep, double *__restrict__ s0pre) {
+  const int l = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (l >= n_loops) return;
+  const int s0 = min(max(loop_off[l], 0), n_segs), s1 = min(max(loop_off[l + 1], s0), n_segs);
+  double carry = 0.0;
+  for (int base = s0; base < s1; base += 32) {
+    const int s = base + lane;
+    double v = s < s1 ? prep[s].S0 : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    v += carry;
+    if (s < s1) s0pre[s] = v;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -391,6 +474,7 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
                        const double *__restrict__ wts, const SegPrep *__restrict__ prep,
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
+                       const double2 *__restrict__ lend,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
                        Cold<R> *__restrict__ cold, int dbg_flags) {
   const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -472,9 +556,8 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
         if (j == a) {
           // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
           const int se = s0 + ch.x + bnd;                // last segment of the run
-          const int ne = deg[se], oe = coff[se];
-          const int2 ke = shift[se];
-          const double ex = X(ctrl[2 * (oe + ne)], ke.x), ey = Y(ctrl[2 * (oe + ne) + 1], ke.y);
+          const double2 le = lend[se];                   // its lifted end point (K2a)
+          const double ex = TX(le.x), ey = TY(le.y);
           const int sa = s0 + ch.x + a;
           const double sum = s0pre[se] - (sa > s0 ? s0pre[sa - 1] : 0.0);
           const int sub = 2 * (bnd - a + 1) - 2;          // records of the subtree after the SPAN
@@ -691,6 +774,20 @@ struct PinnedArena {
 };
 PinnedArena g_pin;
 std::mutex g_build_mu;
+// The build returns without waiting for its device work: the pinned staging of
+// one build stays in use until the event recorded after its last copy, which
+// the next build waits on before reusing the arena (per device).
+cudaEvent_t g_pin_ev[64] = {};
+bool g_pin_pending[64] = {};
+cudaEvent_t g_info_ev_dev[64] = {};
+struct PinRelease {
+  cudaEvent_t ev;
+  bool *pending;
+  cudaStream_t st;
+  ~PinRelease() {
+    if (cudaEventRecord(ev, st) == cudaSuccess) *pending = true;
+  }
+};
 
 cudaError_t h2d(void *dst, const void *src, size_t bytes, cudaStream_t st) {
   if (!bytes) return cudaSuccess;
@@ -718,11 +815,15 @@ void free_handle(wn_faces_t F) {
   if (!F) return;
   for (auto &pr : F->k3_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto &e : F->k3_mid) cudaEventDestroy(e);
-  // stream-ordered frees on the legacy stream (caller guarantees no query in flight)
+  // stream-ordered frees on the legacy stream, after the handle's last use
+  // (its build or its latest query, on whatever stream that ran)
+  if (F->last_use) cudaStreamWaitEvent(0, F->last_use, 0);
   void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
                 F->face_per, F->face_ok, F->face_M, F->counters};
   for (void *p : ps)
     if (p) cache_free(p, 0);
+  if (F->last_use) cudaEventDestroy(F->last_use);
+  if (F->ready) cudaEventDestroy(F->ready);
   delete F;
 }
 
@@ -738,6 +839,7 @@ struct BuildCtx {
   uint8_t *brk;
   int2 *chain;      // per segment: (chain start index within its loop, chain length)
   double *s0pre;    // per segment: prefix sum of root spans S0 along its loop
+  double2 *lend;    // per segment: lifted end point
   LoopInfo *info;
   cudaStream_t st;
 };
@@ -801,7 +903,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
     ++g_build_launches;
     k_emit<R><<<(int)((32 * (int64_t)ng + 255) / 256), 256, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
-                                                 B.w, B.prep, B.shift, B.brk, B.chain, B.s0pre, B.info, rel, (Hot<R> *)F->hot,
+                                                 B.w, B.prep, B.shift, B.brk, B.chain, B.s0pre, B.lend, B.info, rel, (Hot<R> *)F->hot,
                                                  (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());
     cache_free(dg, st);
@@ -820,6 +922,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   set_error("");
   g_build_launches = 0;
   std::lock_guard<std::mutex> build_lock(g_build_mu);
+  for (int d = 0; d < 64; ++d)
+    if (g_pin_pending[d]) {
+      cudaEventSynchronize(g_pin_ev[d]);
+      g_pin_pending[d] = false;
+    }
   g_pin.reset();
   g_tree_opt = !opts || opts->hierarchy != 0;
   if (!out) { set_error("wn_build_faces: out == NULL"); return WN_ERR_ARG; }
@@ -847,21 +954,31 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   }
   ensure_pool(dev);
+  if (dev < 0 || dev >= 64) { set_error("device index out of range"); return WN_ERR_ARG; }
+  if (!g_pin_ev[dev]) {
+    WN_CUDA(cudaEventCreateWithFlags(&g_pin_ev[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaEventCreateWithFlags(&g_info_ev_dev[dev], cudaEventDisableTiming));
+  }
+  cudaEvent_t g_info_ev = g_info_ev_dev[dev];
   cudaStream_t st = (cudaStream_t)stream;
+  PinRelease pin_release{g_pin_ev[dev], &g_pin_pending[dev], st};
   DevBuf D;
   D.st = st;
   Trace tr;
 
   // --- host copies of the small CSR / face arrays ---
-  static std::vector<int32_t> h_lso, h_flo;
-  static std::vector<uint8_t> h_per;
-  static std::vector<double> h_dom;
-  h_lso.resize(n_loops + 1); h_flo.resize(n_faces + 1); h_per.resize(n_faces); h_dom.resize(4 * (size_t)n_faces);
-  WN_CUDA(cudaMemcpyAsync(h_lso.data(), loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToHost, st));
-  WN_CUDA(cudaMemcpyAsync(h_flo.data(), face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st));
+  // (pinned staging: the copies stay asynchronous; read after g_info_ev)
+  int32_t *h_lso = (int32_t *)g_pin.get(sizeof(int32_t) * (n_loops + 1));
+  int32_t *h_flo = (int32_t *)g_pin.get(sizeof(int32_t) * (n_faces + 1));
+  uint8_t *h_per = (uint8_t *)g_pin.get(std::max(n_faces, 1));
+  double *h_dom = (double *)g_pin.get(sizeof(double) * 4 * std::max(n_faces, 1));
+  int32_t *h_bad = (int32_t *)g_pin.get(sizeof(int32_t));
+  if (!h_lso || !h_flo || !h_per || !h_dom || !h_bad) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
+  WN_CUDA(cudaMemcpyAsync(h_lso, loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaMemcpyAsync(h_flo, face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st));
   if (n_faces) {
-    WN_CUDA(cudaMemcpyAsync(h_per.data(), face_periodic, n_faces, cudaMemcpyDeviceToHost, st));
-    WN_CUDA(cudaMemcpyAsync(h_dom.data(), face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st));
+    WN_CUDA(cudaMemcpyAsync(h_per, face_periodic, n_faces, cudaMemcpyDeviceToHost, st));
+    WN_CUDA(cudaMemcpyAsync(h_dom, face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st));
   }
   // --- K0: degrees -> control offsets ---
   int32_t *d_cnt = nullptr, *d_bad = nullptr;
@@ -882,29 +999,9 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(D.alloc((char **)&dt, tmp));
     cub::DeviceScan::ExclusiveSum(dt, tmp, d_cnt, B.coff, n_segs + 1, st);
   }
-  int32_t h_bad = 0;
-  WN_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-  WN_CUDA(cudaStreamSynchronize(st));
-  tr.mark("csr d2h + degree scan");
-  // CSR / domain checks on the host
-  bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
-  for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
-  for (int f = 0; csr_ok && f < n_faces; ++f) csr_ok = h_flo[f] <= h_flo[f + 1];
-  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return WN_ERR_ARG; }
-  if (h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return WN_ERR_ARG; }
-  for (int f = 0; f < n_faces; ++f) {
-    const double *d = &h_dom[4 * f];
-    if ((h_per[f] & 1) && !(std::isfinite(d[0]) && std::isfinite(d[1]) && d[1] > 0)) {
-      set_error("face %d: bad u period", f);
-      return WN_ERR_GEOM;
-    }
-    if ((h_per[f] & 2) && !(std::isfinite(d[2]) && std::isfinite(d[3]) && d[3] > 0)) {
-      set_error("face %d: bad v period", f);
-      return WN_ERR_GEOM;
-    }
-  }
+  WN_CUDA(cudaMemcpyAsync(h_bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  tr.mark("csr copies + degree scan (async)");
   // --- K1 prep, loop->face, K2a lift ---
-  tr.mark("host checks");
   uint8_t *d_serr = nullptr;
   WN_CUDA(D.alloc(&B.prep, n_segs));
   WN_CUDA(D.alloc(&d_serr, n_segs));
@@ -913,8 +1010,23 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(D.alloc(&B.brk, n_segs));
   WN_CUDA(D.alloc(&B.chain, n_segs));
   WN_CUDA(D.alloc(&B.s0pre, n_segs));
+  WN_CUDA(D.alloc(&B.lend, n_segs));
   WN_CUDA(D.alloc(&B.info, n_loops));
-  g_build_launches += (n_segs ? 1 : 0) + (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
+  // K2a first: the host planner only needs the loop summaries, so their copy
+  // is waited on while K1 (derivative bounds) runs on the device
+  if (n_loops) WN_CUDA(cudaMemsetAsync(B.loop_face, 0xFF, sizeof(int32_t) * n_loops, st));
+  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, n_loops, face_loop_off, B.loop_face);
+  if (n_loops)
+    k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_faces, n_segs, loop_seg_off, B.loop_face, face_periodic,
+                                                                      face_domain, seg_degree, B.coff, ctrl_uv, ctrl_w,
+                                                                      B.shift, B.brk, B.chain, B.lend, B.info);
+  g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
+  WN_CUDA(cudaGetLastError());
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
+  LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
+  if (!L) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
+  if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
+  WN_CUDA(cudaEventRecord(g_info_ev, st));
   // segments sorted by degree so that k_prep's warps run one degree variant
   int32_t *d_order = nullptr;
   if (n_segs) {
@@ -929,23 +1041,37 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(D.alloc(&dt, tmp));
     cub::DeviceRadixSort::SortPairs(dt, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
     g_build_launches += 4;
+    k_prep<<<(int)((9 * (int64_t)n_segs + 127) / 128), 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w,
+                                                                    B.prep, d_serr, d_order);
+    ++g_build_launches;
   }
-  tr.mark("alloc calls (host)");
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) alloc + degree sort"); }
-  if (n_segs) k_prep<<<(int)((9 * (int64_t)n_segs + 127) / 128), 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep"); }
-  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, face_loop_off, B.loop_face);
-  if (n_loops)
-    k_lift<<<(n_loops + 127) / 128, 128, 0, st>>>(n_loops, loop_seg_off, B.loop_face, face_periodic, face_domain,
-                                                 seg_degree, B.coff, ctrl_uv, d_serr, B.prep, B.shift, B.brk,
-                                                 B.chain, B.s0pre, B.info);
+  if (n_loops) {
+    k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, loop_seg_off, B.prep, B.s0pre);
+    ++g_build_launches;
+  }
   WN_CUDA(cudaGetLastError());
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
-  LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
-  if (!L) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
-  if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
-  WN_CUDA(cudaStreamSynchronize(st));
-  tr.mark("prep + lift + info d2h");
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep + k_s0pre"); }
+  WN_CUDA(cudaEventSynchronize(g_info_ev));
+  tr.mark("loop summaries d2h");
+  // CSR / domain checks on the host (the kernels above clamp every CSR index,
+  // so a bad input is reported here without any out-of-bounds access)
+  bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
+  for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
+  for (int f = 0; csr_ok && f < n_faces; ++f) csr_ok = h_flo[f] <= h_flo[f + 1];
+  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return WN_ERR_ARG; }
+  if (*h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return WN_ERR_ARG; }
+  for (int f = 0; f < n_faces; ++f) {
+    const double *d = &h_dom[4 * f];
+    if ((h_per[f] & 1) && !(std::isfinite(d[0]) && std::isfinite(d[1]) && d[1] > 0)) {
+      set_error("face %d: bad u period", f);
+      return WN_ERR_GEOM;
+    }
+    if ((h_per[f] & 2) && !(std::isfinite(d[2]) && std::isfinite(d[3]) && d[3] > 0)) {
+      set_error("face %d: bad v period", f);
+      return WN_ERR_GEOM;
+    }
+  }
+  tr.mark("host checks");
 
   // --- K2b: validation + planning (host) ---
   static std::vector<int32_t> status;
@@ -1269,9 +1395,16 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, fM, F) : materialise<double>(B, P, fper, fdom, fM, F);
   if (rc != WN_OK) { free_handle(F); return rc; }
   tr.mark("materialise (alloc+h2d+emit)");
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build sync"); }
-  tr.mark("final sync");
+  // no final synchronisation: the handle's records are complete in stream
+  // order, so queries enqueued on `stream` after this call see them
+  {
+    cudaError_t e = cudaEventCreateWithFlags(&F->last_use, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&F->ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(F->last_use, st);
+    if (e == cudaSuccess) e = cudaEventRecord(F->ready, st);
+    if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build event"); }
+  }
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_emit"); }
   *out = F;
   return WN_OK;
 }

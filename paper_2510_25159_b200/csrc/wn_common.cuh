@@ -197,6 +197,8 @@ struct wn_faces_s {
   double *face_M = nullptr;        // [n_faces] absolute margin M (R5) per face
   unsigned long long *counters = nullptr;  // [8]
   int counters_on = 0;
+  cudaEvent_t last_use = nullptr;    // recorded after the build and after every query
+  cudaEvent_t ready = nullptr;       // recorded after the build's record emission
   int timing_on = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k3_events;
   std::vector<cudaEvent_t> k3_mid;   // after phase 1 (k_phase1) of each timed query

@@ -961,6 +961,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   }
   WN_CUDA(cudaGetLastError());
   cache_free(base, st);
+  if (F->last_use) WN_CUDA(cudaEventRecord(F->last_use, st));
   g_launches = launches;
   return WN_OK;
 }
@@ -995,6 +996,8 @@ extern "C" wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face
     // every query references a non-existent face
     wn::set_error("");
   }
+  // the build's record emission may still be running on its own stream
+  if (faces->ready) WN_CUDA(cudaStreamWaitEvent(st, faces->ready, 0));
   if (faces->precision == 1) return wn::launch_query<float>(faces, n, face_id, uv, winding, flag, st);
   return wn::launch_query<double>(faces, n, face_id, uv, winding, flag, st);
 }

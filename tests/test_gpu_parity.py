@@ -7,6 +7,7 @@ than tol from a half-integer) the inside/outside flag is bit-exact and
 rounded inputs, R19); the GPU never reports on-boundary there."""
 import numpy as np
 import pytest
+import torch
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -183,6 +184,32 @@ def test_bad_geometry_rejected():
     with pytest.raises(wn.WNError) as ei:
         wn.Faces.from_workload(bad2)
     assert ei.value.status == 1
+
+
+@pytest.mark.gpu
+def test_bad_csr_rejected_without_fault():
+    # the device kernels run before the host validates the CSR offsets: they
+    # must clamp every index (a fault here would poison the context)
+    wl = G.gen_c2(n_queries=100)
+    ns, nl = len(wl["seg_degree"]), len(wl["loop_seg_off"]) - 1
+    for lso in (np.r_[wl["loop_seg_off"][:-1], ns + 1000],          # past the segment array
+                np.r_[0, np.full(nl, -5)],                          # decreasing / negative
+                np.r_[0, np.full(nl, 10 ** 9)]):
+        bad = dict(wl)
+        bad["loop_seg_off"] = lso.astype(np.int32)
+        with pytest.raises(wn.WNError) as ei:
+            wn.Faces.from_workload(bad)
+        assert ei.value.status == 1
+    nf = len(wl["face_loop_off"]) - 1
+    bad = dict(wl)
+    bad["face_loop_off"] = np.r_[0, np.full(nf, nl + 77)].astype(np.int32)
+    with pytest.raises(wn.WNError):
+        wn.Faces.from_workload(bad)
+    # the context is still healthy
+    faces = wn.Faces.from_workload(wl)
+    r = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    assert r.flag.cpu().numpy().max() <= 3
 
 
 def test_counters_and_info():

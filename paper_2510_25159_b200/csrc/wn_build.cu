@@ -274,6 +274,8 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
   double ex = 0, ey = 0;           // lifted end of the previous segment (uniform)
   double sx = 0, sy = 0;
   int nbrk = 0, err = 0, cs = 0;   // cs: chain start (loop index) carried across chunks
+  int cku = 0, ckv = 0;            // shift of the previous chunk's last segment
+  double cxr = 0, cyr = 0;         // its raw (stored) end point
   double xmin = INFINITY, ymin = INFINITY, xmax = -INFINITY, ymax = -INFINITY;
   for (int base = s0; base < s1; base += 32) {
     const int s = base + lane;
@@ -295,40 +297,73 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
       }
     }
     err |= __any_sync(0xffffffffu, e);
-    // shifts: sequential over the chunk (uniform loop, broadcast operands);
-    // a loop of a non-periodic face only compares each start with the previous end
+    // shifts (R17/R18): k_s = round((lifted end of s-1 - start of s) / T),
+    // k = 0 for the loop's first segment -- a sequential recurrence.  The
+    // candidates are the prefix sums of the local deltas round((raw end of s-1
+    // - start of s) / T); every lane then re-evaluates the recurrence with its
+    // candidate predecessor, so if all agree the candidates ARE the recurrence's
+    // values (induction from k = 0).  A chunk where a lane disagrees (a rounding
+    // tie) walks the recurrence serially.
     int ku = 0, kv = 0;
-    bool bk = false;
-    if (!pu && !pv) {
-      double pxe = __shfl_up_sync(0xffffffffu, xe, 1), pye = __shfl_up_sync(0xffffffffu, ye, 1);
-      if (lane == 0) { pxe = ex; pye = ey; }
-      bk = in && s > s0 && !(x0 == pxe && y0 == pye);
-      if (base == s0) { sx = __shfl_sync(0xffffffffu, x0, 0); sy = __shfl_sync(0xffffffffu, y0, 0); }
-      ex = __shfl_sync(0xffffffffu, xe, cnt - 1);
-      ey = __shfl_sync(0xffffffffu, ye, cnt - 1);
-    }
-    for (int j = 0; (pu || pv) && j < cnt; ++j) {
-      const double x0j = __shfl_sync(0xffffffffu, x0, j), y0j = __shfl_sync(0xffffffffu, y0, j);
-      const double xej = __shfl_sync(0xffffffffu, xe, j), yej = __shfl_sync(0xffffffffu, ye, j);
-      int kuj = 0, kvj = 0;
-      if (base + j > s0) {
-        if (pu) kuj = (int)round(__ddiv_rn(__dsub_rn(ex, x0j), Tu));
-        if (pv) kvj = (int)round(__ddiv_rn(__dsub_rn(ey, y0j), Tv));
+    if (pu || pv) {
+      const bool first = s == s0;
+      double pxr = __shfl_up_sync(0xffffffffu, xe, 1), pyr = __shfl_up_sync(0xffffffffu, ye, 1);
+      if (lane == 0) { pxr = cxr; pyr = cyr; }
+      int su = 0, sv = 0;
+      if (in && !first) {
+        if (pu) su = (int)round(__ddiv_rn(__dsub_rn(pxr, x0), Tu));
+        if (pv) sv = (int)round(__ddiv_rn(__dsub_rn(pyr, y0), Tv));
       }
-      const double lx0 = pu ? lat(x0j, kuj, Tu) : x0j, ly0 = pv ? lat(y0j, kvj, Tv) : y0j;
-      const bool bj = (base + j > s0) && !(lx0 == ex && ly0 == ey);
-      if (base + j == s0) { sx = lx0; sy = ly0; }
-      if (lane == j) { ku = kuj; kv = kvj; bk = bj; }
-      ex = pu ? lat(xej, kuj, Tu) : xej;
-      ey = pv ? lat(yej, kvj, Tv) : yej;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tu = __shfl_up_sync(0xffffffffu, su, o), tv = __shfl_up_sync(0xffffffffu, sv, o);
+        if (lane >= o) { su += tu; sv += tv; }
+      }
+      ku = cku + su;
+      kv = ckv + sv;
+      int pku = __shfl_up_sync(0xffffffffu, ku, 1), pkv = __shfl_up_sync(0xffffffffu, kv, 1);
+      if (lane == 0) { pku = cku; pkv = ckv; }
+      bool ok = true;
+      if (in && !first) {
+        if (pu) ok &= ku == (int)round(__ddiv_rn(__dsub_rn(lat(pxr, pku, Tu), x0), Tu));
+        if (pv) ok &= kv == (int)round(__ddiv_rn(__dsub_rn(lat(pyr, pkv, Tv), y0), Tv));
+      }
+      if (!__all_sync(0xffffffffu, ok)) {
+        double qx = ex, qy = ey;   // lifted end of the previous segment
+        for (int j = 0; j < cnt; ++j) {
+          const double x0j = __shfl_sync(0xffffffffu, x0, j), y0j = __shfl_sync(0xffffffffu, y0, j);
+          const double xej = __shfl_sync(0xffffffffu, xe, j), yej = __shfl_sync(0xffffffffu, ye, j);
+          int kuj = 0, kvj = 0;
+          if (base + j > s0) {
+            if (pu) kuj = (int)round(__ddiv_rn(__dsub_rn(qx, x0j), Tu));
+            if (pv) kvj = (int)round(__ddiv_rn(__dsub_rn(qy, y0j), Tv));
+          }
+          if (lane == j) { ku = kuj; kv = kvj; }
+          qx = pu ? lat(xej, kuj, Tu) : xej;
+          qy = pv ? lat(yej, kvj, Tv) : yej;
+        }
+      }
     }
+    // lifted start / end, the previous lifted end, bit-continuity of the junction
+    const double lx0 = pu ? lat(x0, ku, Tu) : x0, ly0 = pv ? lat(y0, kv, Tv) : y0;
+    const double lxe = pu ? lat(xe, ku, Tu) : xe, lye = pv ? lat(ye, kv, Tv) : ye;
+    double pex = __shfl_up_sync(0xffffffffu, lxe, 1), pey = __shfl_up_sync(0xffffffffu, lye, 1);
+    if (lane == 0) { pex = ex; pey = ey; }
+    const bool bk = in && s > s0 && !(lx0 == pex && ly0 == pey);
+    if (base == s0) { sx = __shfl_sync(0xffffffffu, lx0, 0); sy = __shfl_sync(0xffffffffu, ly0, 0); }
+    ex = __shfl_sync(0xffffffffu, lxe, cnt - 1);
+    ey = __shfl_sync(0xffffffffu, lye, cnt - 1);
+    cku = __shfl_sync(0xffffffffu, ku, cnt - 1);
+    ckv = __shfl_sync(0xffffffffu, kv, cnt - 1);
+    cxr = __shfl_sync(0xffffffffu, xe, cnt - 1);
+    cyr = __shfl_sync(0xffffffffu, ye, cnt - 1);
     if (in) {
       shift[s] = make_int2(ku, kv);
       brk[s] = bk;
       // lifted box and end point: lat() is monotone, so it commutes with min/max
       bx0 = pu ? lat(bx0, ku, Tu) : bx0; bx1 = pu ? lat(bx1, ku, Tu) : bx1;
       by0 = pv ? lat(by0, kv, Tv) : by0; by1 = pv ? lat(by1, kv, Tv) : by1;
-      lend[s] = make_double2(pu ? lat(xe, ku, Tu) : xe, pv ? lat(ye, kv, Tv) : ye);
+      lend[s] = make_double2(lxe, lye);
     }
     xmin = fmin(xmin, bx0); xmax = fmax(xmax, bx1);
     ymin = fmin(ymin, by0); ymax = fmax(ymax, by1);

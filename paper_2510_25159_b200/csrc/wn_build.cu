@@ -493,15 +493,35 @@ __device__ void put_group<float>(Hot<float> *H, int r, double xmin, double ymin,
   H[r] = h;
 }
 
+// C(n, j) for n <= 5, exact (no per-call local table)
 __device__ __forceinline__ double binom5(int n, int j) {
-  const double tab[6][6] = {{1, 0, 0, 0, 0, 0}, {1, 1, 0, 0, 0, 0}, {1, 2, 1, 0, 0, 0},
-                            {1, 3, 3, 1, 0, 0}, {1, 4, 6, 4, 1, 0}, {1, 5, 10, 10, 5, 1}};
-  return tab[n][j];
+  double c = 1.0;
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    if (i < j) c = c * (double)(n - i) / (double)(i + 1);   // integer quotients: exact
+  return c;
 }
 
-// one warp per planned group; lanes take the group's segments in parallel
 template <typename R>
-__global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
+__device__ __forceinline__ void st2(R *p, R a, R b);
+template <>
+__device__ __forceinline__ void st2<double>(double *p, double a, double b) {
+  *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+template <>
+__device__ __forceinline__ void st2<float>(float *p, float a, float b) {
+  *reinterpret_cast<float2 *>(p) = make_float2(a, b);
+}
+
+// one warp per planned group; lanes take the group's segments in parallel.
+// The path-hierarchy SPAN records of a chain need the end point and the S0
+// prefix of segments handled by other lanes (or chunks): for groups of up to
+// EMIT_STAGE segments the warp first stages them in shared memory, so the
+// per-level SPAN emission reads shared memory instead of a chain of global loads.
+constexpr int EMIT_WARPS = 4;
+constexpr int EMIT_STAGE = 256;
+template <typename R>
+__global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
                        const int32_t *__restrict__ loop_off,
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
@@ -548,6 +568,18 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
   const int s0 = loop_off[l], s1 = loop_off[l + 1];
   const int r_first = G.rec_off + cull + 1;              // first record after GROUP? and MOVE
   const bool tree = (G.flags & PF_TREE) != 0;
+  __shared__ double2 s_end[EMIT_WARPS][EMIT_STAGE];      // translated lifted end points
+  __shared__ double s_pre[EMIT_WARPS][EMIT_STAGE];       // S0 prefix sums
+  const int wib = (threadIdx.x >> 5);
+  const bool staged = tree && (s1 - s0) <= EMIT_STAGE;
+  if (staged) {
+    for (int s = s0 + lane; s < s1; s += 32) {
+      const double2 le = lend[s];
+      s_end[wib][s - s0] = make_double2(TX(le.x), TY(le.y));
+      s_pre[wib][s - s0] = s0pre[s];
+    }
+    __syncwarp();
+  }
   // fp64 records: spans of the conservative fp32 filter
   auto filter_span = [&](double S) {
     return (sizeof(R) == 8) ? (S * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17) : S * (1.0 + rel) + G.M;
@@ -565,10 +597,16 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
     const int n = deg[s];
     const int o = coff[s];
     const int2 k = shift[s];
-    double px[6], py[6];
-    for (int j = 0; j <= n; ++j) {
-      px[j] = X(ctrl[2 * (o + j)], k.x);
-      py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
+    // register-resident control points (unrolled over the maximum degree)
+    double px[6], py[6], pxn = 0.0, pyn = 0.0;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      px[j] = py[j] = 0.0;
+      if (j <= n) {
+        px[j] = X(ctrl[2 * (o + j)], k.x);
+        py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
+      }
+      if (j == n) { pxn = px[j]; pyn = py[j]; }
     }
     int r;
     if (!tree) {
@@ -591,10 +629,17 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
         if (j == a) {
           // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
           const int se = s0 + ch.x + bnd;                // last segment of the run
-          const double2 le = lend[se];                   // its lifted end point (K2a)
-          const double ex = TX(le.x), ey = TY(le.y);
           const int sa = s0 + ch.x + a;
-          const double sum = s0pre[se] - (sa > s0 ? s0pre[sa - 1] : 0.0);
+          double ex, ey, sum;
+          if (staged) {
+            const double2 le = s_end[wib][se - s0];
+            ex = le.x; ey = le.y;
+            sum = s_pre[wib][se - s0] - (sa > s0 ? s_pre[wib][sa - 1 - s0] : 0.0);
+          } else {
+            const double2 le = lend[se];                 // its lifted end point (K2a)
+            ex = TX(le.x); ey = TY(le.y);
+            sum = s0pre[se] - (sa > s0 ? s0pre[sa - 1] : 0.0);
+          }
           const int sub = 2 * (bnd - a + 1) - 2;          // records of the subtree after the SPAN
           put_rec<R>(hot, off, ex, ey, filter_span(sum), K_SPAN | fa | ((uint32_t)sub << 8));
         }
@@ -611,29 +656,38 @@ __global__ void __launch_bounds__(256) k_emit(int32_t n_groups, const PlanGroup 
     const double S0 = filter_span(bp.S0);
     const double Bm = bp.B * (1.0 + rel);
     const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
-    put_rec<R>(hot, r, px[n], py[n], S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
-    Cold<R> C;
-    C.f0x = (R)px[0]; C.f0y = (R)py[0]; C.f1x = (R)px[n]; C.f1y = (R)py[n];
-    C.B = Br;
-    for (int q = 0; q < 8; ++q) {
-      const double bq = (dbg_flags & 1 ? bp.B : fmin(bp.B, bp.Bq[q])) * (1.0 + rel);
-      C.Bq[q] = (sizeof(R) == 4) ? (R)f_up(bq) : (R)bq;
+    put_rec<R>(hot, r, pxn, pyn, S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
+    // cold record written field pair by field pair (vector stores, no local copy)
+    Cold<R> *Cp = cold + G.cold_off + idx;
+    st2<R>(&Cp->f0x, (R)px[0], (R)py[0]);
+    st2<R>(&Cp->f1x, (R)pxn, (R)pyn);
+    st2<R>(&Cp->B, Br, (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M);
+    *reinterpret_cast<int2 *>(&Cp->n) = make_int2(n, 0);
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const double b0 = (dbg_flags & 1 ? bp.B : fmin(bp.B, bp.Bq[q])) * (1.0 + rel);
+      const double b1 = (dbg_flags & 1 ? bp.B : fmin(bp.B, bp.Bq[q + 1])) * (1.0 + rel);
+      st2<R>(&Cp->Bq[q], (sizeof(R) == 4) ? (R)f_up(b0) : (R)b0, (sizeof(R) == 4) ? (R)f_up(b1) : (R)b1);
     }
-    C.M = (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M;
-    C.n = n;
-    C.pad = 0;
+    R cxv[6], cyv[6], cwv[6];
+#pragma unroll
     for (int j = 0; j < 6; ++j) {
       if (j <= n) {
         const double wj = wts ? wts[o + j] : 1.0;
         const double cw = binom5(n, j) * wj;
-        C.cx[j] = (R)(cw * px[j]);
-        C.cy[j] = (R)(cw * py[j]);
-        C.cw[j] = (R)cw;
+        cxv[j] = (R)(cw * px[j]);
+        cyv[j] = (R)(cw * py[j]);
+        cwv[j] = (R)cw;
       } else {
-        C.cx[j] = C.cy[j] = C.cw[j] = (R)0;
+        cxv[j] = cyv[j] = cwv[j] = (R)0;
       }
     }
-    cold[G.cold_off + idx] = C;
+#pragma unroll
+    for (int j = 0; j < 6; j += 2) {
+      st2<R>(&Cp->cx[j], cxv[j], cxv[j + 1]);
+      st2<R>(&Cp->cy[j], cyv[j], cyv[j + 1]);
+      st2<R>(&Cp->cw[j], cwv[j], cwv[j + 1]);
+    }
   }
   if (lane == 0) {
     int r = tree ? G.rec_off + cull + 2 * (s1 - s0) : r_first + (s1 - s0) + carry;
@@ -937,7 +991,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     WN_CUDA(h2d(dg, plan.groups.data(), sizeof(PlanGroup) * ng, st));
     const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
     ++g_build_launches;
-    k_emit<R><<<(int)((32 * (int64_t)ng + 255) / 256), 256, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
+    k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
                                                  B.w, B.prep, B.shift, B.brk, B.chain, B.s0pre, B.lend, B.info, rel, (Hot<R> *)F->hot,
                                                  (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
     WN_CUDA(cudaGetLastError());

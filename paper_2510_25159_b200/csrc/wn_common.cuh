@@ -59,13 +59,13 @@ struct __align__(16) Hot<float> {
 // homogeneous coefficients c_j = C(n,j) w_j (x_j, y_j, 1) (O(n) evaluation,
 // Table 1).
 template <typename R>
-struct Cold {
+struct __align__(16) Cold {   // 16-B aligned; every field pair below starts on a 16-B (fp64) boundary
   R f0x, f0y, f1x, f1y;
   R B;      // derivative bound (A.1; R29) incl. relative margin
   R M;      // absolute margin (R5)
-  int32_t n, pad;
   R cx[6], cy[6], cw[6];
   R Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin
+  int32_t n, pad;
 };
 
 // K1 output per input segment (translation invariant)

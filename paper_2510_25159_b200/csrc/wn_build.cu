@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <omp.h>
 #include <numeric>
@@ -755,16 +756,17 @@ struct Plan {
   }
 };
 
-static int gcd_i(int a, int b) {
-  a = std::abs(a); b = std::abs(b);
+__host__ __device__ inline int gcd_i(int a, int b) {
+  a = a < 0 ? -a : a;
+  b = b < 0 ? -b : b;
   while (b) { int t = a % b; a = b; b = t; }
   return a;
 }
 
 // lattice translates k with [lo + k T, hi + k T] meeting [t0 - m, t0 + T + m]
-static void k_range(double lo, double hi, double t0, double T, double m, int &k0, int &k1) {
-  k0 = (int)std::ceil((t0 - m - hi) / T) - 1;
-  k1 = (int)std::floor((t0 + T + m - lo) / T) + 1;
+__host__ __device__ inline void k_range(double lo, double hi, double t0, double T, double m, int &k0, int &k1) {
+  k0 = (int)ceil((t0 - m - hi) / T) - 1;
+  k1 = (int)floor((t0 + T + m - lo) / T) + 1;
   // tighten exactly (the +-1 guards the division rounding)
   while (k0 <= k1 && !(lo + k0 * T <= t0 + T + m && hi + k0 * T >= t0 - m)) ++k0;
   while (k1 >= k0 && !(lo + k1 * T <= t0 + T + m && hi + k1 * T >= t0 - m)) --k1;
@@ -777,10 +779,17 @@ struct FaceCtx {
   bool angle;
 };
 
+// hot records of one planned group (must match k_emit's layout)
+__host__ __device__ inline int group_nrec(int kind, int flags, const LoopInfo &I) {
+  if (kind == G_LINE) return 1;
+  // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg
+  return ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) +
+         ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
+}
+
 // group flags for a closed / copy group
-static bool g_tree_opt = true;   // set per build from wn_options_t.hierarchy (under g_build_mu)
-static int loop_flags(const LoopInfo &I, bool angle, bool copy) {
-  int fl = (angle ? PF_ANGLE : 0) | (g_tree_opt ? PF_TREE : 0);
+__host__ __device__ inline int loop_flags(const LoopInfo &I, bool angle, bool copy, bool tree) {
+  int fl = (angle ? PF_ANGLE : 0) | (tree ? PF_TREE : 0);
   if (copy) {
     fl |= angle ? PF_TAIL_NCH : PF_TAIL_XCH;
     if (I.nbrk == 0) fl |= PF_CULL;
@@ -792,11 +801,16 @@ static int loop_flags(const LoopInfo &I, bool angle, bool copy) {
   return fl;
 }
 
+__host__ __device__ inline double tile_margin(const FaceCtx &C) {
+  return 1e-9 * (1.0 + fabs(C.u0) + C.Tu + fabs(C.v0) + C.Tv);
+}
+
 // contractible loop in a (uni/bi/non-)periodic face: every translate meeting the tile
-static void plan_contractible(Plan &P, int l, const LoopInfo &I, const FaceCtx &C) {
-  const int fl = loop_flags(I, C.angle, false);
+template <class S>
+__host__ __device__ void plan_contractible(S &P, int l, const LoopInfo &I, const FaceCtx &C, bool tree) {
+  const int fl = loop_flags(I, C.angle, false, tree);
   int i0 = 0, i1 = 0, j0 = 0, j1 = 0;
-  const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
+  const double m = tile_margin(C);
   if (C.per & 1) k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, i0, i1);
   if (C.per & 2) k_range(I.bb[1], I.bb[3], C.v0, C.Tv, m, j0, j1);
   for (int i = i0; i <= i1; ++i)
@@ -805,10 +819,11 @@ static void plan_contractible(Plan &P, int l, const LoopInfo &I, const FaceCtx &
 
 // non-contractible loop along axis a (0 = u, 1 = v) at transverse translate jt:
 // copies (Eq. 5 rewritten with chords tiling L) meeting the tile
-static void plan_extended_copies(Plan &P, int l, const LoopInfo &I, const FaceCtx &C, int axis, int jt,
-                                 bool transverse_cull_tile) {
-  const int fl = loop_flags(I, C.angle, true);
-  const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
+template <class S>
+__host__ __device__ void plan_extended_copies(S &P, int l, const LoopInfo &I, const FaceCtx &C, int axis, int jt,
+                                              bool transverse_cull_tile, bool tree) {
+  const int fl = loop_flags(I, C.angle, true, tree);
+  const double m = tile_margin(C);
   int k0, k1;
   if (axis == 0) k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, k0, k1);
   else k_range(I.bb[1], I.bb[3], C.v0, C.Tv, m, k0, k1);
@@ -825,11 +840,238 @@ static void plan_extended_copies(Plan &P, int l, const LoopInfo &I, const FaceCt
   }
 }
 
-static double face_margin(const LoopInfo *L, int l0, int l1, const FaceCtx &C, bool fp32) {
-  double s = 1.0 + std::fabs(C.u0) + std::fabs(C.v0) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0);
+// the groups of one (validated, paired) face
+template <class S>
+__host__ __device__ void plan_face(S &P, const LoopInfo *L, int l0, int l1, const FaceCtx &C,
+                                   const int *pair_beta, const int *pair_s, bool tree) {
+  for (int l = l0; l < l1; ++l) {
+    const LoopInfo &I = L[l];
+    if (I.nseg == 0) continue;
+    if (C.per == 0 || (I.cu == 0 && I.cv == 0)) {
+      plan_contractible(P, l, I, C, tree);
+      continue;
+    }
+    const int axis = (I.cu != 0) ? 0 : 1;
+    if (C.per != 3) {
+      // uni-periodic non-contractible loop: omega(p,L) + copies (Eq. 5)
+      P.add(G_LINE, 0, l, 0, 0, I, C.M);
+      plan_extended_copies(P, l, I, C, axis, 0, false, tree);
+      continue;
+    }
+    // bi-periodic: alpha loops drive Eq. 8 for their pair; beta loops are emitted with them
+    if (!pair_beta || pair_beta[l] < 0) continue;
+    const int lb = pair_beta[l];
+    const int sb = pair_s[l];
+    const LoopInfo &Ib = L[lb];
+    const int tax = axis == 0 ? 1 : 0;
+    const double Tt = tax ? C.Tv : C.Tu, t0 = tax ? C.v0 : C.u0;
+    const double m = tile_margin(C);
+    // transverse window: every band offset j whose lines or copies can meet the tile
+    const double ca = tax ? I.sy : I.sx, cb = (tax ? Ib.sy : Ib.sx) + sb * Tt;
+    const double lo = fmin(fmin(ca, cb), fmin(tax ? I.bb[1] : I.bb[0], (tax ? Ib.bb[1] : Ib.bb[0]) + sb * Tt));
+    const double hi = fmax(fmax(ca, cb), fmax(tax ? I.bb[3] : I.bb[2], (tax ? Ib.bb[3] : Ib.bb[2]) + sb * Tt));
+    int j0, j1;
+    k_range(lo, hi, t0, Tt, m, j0, j1);
+    for (int j = j0; j <= j1; ++j) {
+      // Eq. 8 band j: omega(p, L_alpha) + omega(p, L_beta) only when the strip meets the tile
+      const double la_c = ca + j * Tt, lb_c = cb + j * Tt;
+      if (fmin(la_c, lb_c) <= t0 + Tt + m && fmax(la_c, lb_c) >= t0 - m) {
+        if (axis == 0) { P.add(G_LINE, 0, l, 0, j, I, C.M); P.add(G_LINE, 0, lb, 0, sb + j, Ib, C.M); }
+        else { P.add(G_LINE, 0, l, j, 0, I, C.M); P.add(G_LINE, 0, lb, sb + j, 0, Ib, C.M); }
+      }
+      plan_extended_copies(P, l, I, C, axis, j, true, tree);
+      plan_extended_copies(P, lb, Ib, C, axis, sb + j, true, tree);
+    }
+  }
+}
+
+__host__ __device__ inline double face_margin(const LoopInfo *L, int l0, int l1, const FaceCtx &C, bool fp32) {
+  const double ext = ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0);
+  double s = 1.0 + fabs(C.u0) + fabs(C.v0) + ext;
   for (int l = l0; l < l1; ++l)
-    for (int k = 0; k < 4; ++k) s = std::max(s, 1.0 + std::fabs(L[l].bb[k]) + ((C.per & 1) ? 2 * C.Tu : 0.0) + ((C.per & 2) ? 2 * C.Tv : 0.0));
-  return fp32 ? std::ldexp(s, -17) : std::ldexp(s, -40);
+    for (int k = 0; k < 4; ++k) s = fmax(s, 1.0 + fabs(L[l].bb[k]) + ext);
+  return fp32 ? ldexp(s, -17) : ldexp(s, -40);
+}
+
+// face context from the stored periodicity / domain (non-periodic axes zeroed)
+__host__ __device__ inline FaceCtx face_ctx(uint8_t per, const double *dom, bool angle) {
+  FaceCtx C;
+  C.per = per & 3;
+  C.u0 = dom[0]; C.Tu = dom[1]; C.v0 = dom[2]; C.Tv = dom[3];
+  if (!(C.per & 1)) { C.u0 = 0; C.Tu = 0; }
+  if (!(C.per & 2)) { C.v0 = 0; C.Tv = 0; }
+  C.angle = angle;
+  C.M = 0.0;
+  return C;
+}
+
+// topology validation of one face (Prop. 1; R12-R16): WN_FACE_* code;
+// *needp = 1 when the face's non-contractible loops must be paired (Algs. 7-9)
+__host__ __device__ inline int face_validate(const LoopInfo *L, int l0, int l1, const FaceCtx &C, bool strict,
+                                             int *needp) {
+  int st = WN_FACE_OK;
+  *needp = 0;
+  int cp = 0, cq = 0, nA = 0, nB = 0;
+  for (int l = l0; l < l1; ++l) {
+    const LoopInfo &I = L[l];
+    if (I.err) st = WN_FACE_GEOM;
+    if (I.nseg == 0 || (I.cu == 0 && I.cv == 0)) continue;
+    if (C.per == 1 && abs(I.cu) > 1) st = WN_FACE_B1;
+    if (C.per == 2 && abs(I.cv) > 1) st = WN_FACE_B1;
+    if (gcd_i(I.cu, I.cv) != 1 && !st) st = WN_FACE_CLASS;
+    if (cp == 0 && cq == 0) { cp = I.cu; cq = I.cv; }
+    if (I.cu == cp && I.cv == cq) ++nA;
+    else if (I.cu == -cp && I.cv == -cq) ++nB;
+    else if (!st) st = WN_FACE_CLASS;
+  }
+  if (st) return st;
+  if (nA != nB && (strict || C.per == 3)) return WN_FACE_UNBALANCED;
+  if (C.per == 3 && nA > 0) {
+    if (cp != 0 && cq != 0) return WN_FACE_GENERAL_PQ;
+    *needp = 1;
+  }
+  return WN_FACE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K2b on the device: one thread per face validates it, derives its margin and
+// plans its groups twice -- a counting pass, a scan, and a filling pass that
+// writes the PlanGroups where k_emit reads them.  The host only reads a small
+// summary (totals for the record allocations, validation outcome).
+// ---------------------------------------------------------------------------
+struct BuildSummary {
+  int bad, needp, geom, unsup, toobig, maxr;
+  unsigned long long first_bad;   // (face << 32) | code, minimum over bad faces
+  int tot_g, tot_r, tot_c, pad;
+  unsigned long long lines, cull;
+};
+
+struct CountSink {
+  int ng = 0, recs = 0, colds = 0, lines = 0, cull = 0;
+  __device__ void add(int kind, int flags, int, int, int, const LoopInfo &I, double) {
+    ++ng;
+    recs += group_nrec(kind, flags, I);
+    if (kind == G_LINE) ++lines;
+    else {
+      colds += I.nseg;
+      if (flags & PF_CULL) ++cull;
+    }
+  }
+};
+
+struct FillSink {
+  PlanGroup *out;
+  int face, recs, colds, cold0;
+  __device__ void add(int kind, int flags, int loop, int ku, int kv, const LoopInfo &I, double M) {
+    PlanGroup G;
+    G.kind = kind;
+    G.flags = flags;
+    G.loop = loop;
+    G.ku = ku;
+    G.kv = kv;
+    G.rec_off = recs;
+    G.cold_off = colds;
+    G.cold_local = colds - cold0;
+    G.nrec = group_nrec(kind, flags, I);
+    G.face = face;
+    G.M = M;
+    *out++ = G;
+    recs += G.nrec;
+    if (kind != G_LINE) colds += I.nseg;
+  }
+};
+
+__global__ void k_plan_count(int32_t n_faces, int32_t n_loops, const int32_t *__restrict__ flo,
+                             const uint8_t *__restrict__ per,
+                             const double *__restrict__ dom, const LoopInfo *__restrict__ L, int angle, int strict,
+                             int tree, int fp32, const int *__restrict__ pair_beta, const int *__restrict__ pair_s,
+                             int32_t *__restrict__ status, uint8_t *__restrict__ fper, double *__restrict__ fdom,
+                             double *__restrict__ fM, int4 *__restrict__ cnt, uint32_t *__restrict__ okey,
+                             int32_t *__restrict__ oval, BuildSummary *__restrict__ sum) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_faces) return;
+  const int l0 = min(max(flo[f], 0), n_loops), l1 = min(max(flo[f + 1], l0), n_loops);   // clamped (host-validated)
+  FaceCtx C = face_ctx(per[f], dom + 4 * f, angle != 0);
+  C.M = face_margin(L, l0, l1, C, fp32 != 0);
+  int needp = 0;
+  const int st = face_validate(L, l0, l1, C, strict != 0, &needp);
+  status[f] = st;
+  fper[f] = C.per;
+  fdom[4 * f] = C.u0; fdom[4 * f + 1] = C.Tu; fdom[4 * f + 2] = C.v0; fdom[4 * f + 3] = C.Tv;
+  fM[f] = C.M;
+  CountSink S;
+  if (st) {
+    atomicOr(&sum->bad, 1);
+    if (st == WN_FACE_GEOM) atomicOr(&sum->geom, 1);
+    if (st == WN_FACE_GENERAL_PQ) atomicOr(&sum->unsup, 1);
+    atomicMin(&sum->first_bad, ((unsigned long long)f << 32) | (unsigned)st);
+  } else if (needp && !pair_beta) {
+    atomicOr(&sum->needp, 1);
+  } else {
+    plan_face(S, L, l0, l1, C, pair_beta, pair_s, tree != 0);
+    if (S.lines) atomicAdd(&sum->lines, (unsigned long long)S.lines);
+    if (S.cull) atomicAdd(&sum->cull, (unsigned long long)S.cull);
+    if (S.recs >= (1 << 24) || S.colds >= (1 << 22)) atomicOr(&sum->toobig, 1);
+    atomicMax(&sum->maxr, S.recs);
+  }
+  cnt[f] = make_int4(S.ng, S.recs, S.colds, 0);
+  okey[f] = 0xffffffffu - (uint32_t)S.recs;   // ascending key = descending record count
+  oval[f] = f;
+}
+
+// exclusive scans of the per-face (groups, records, colds) -- one block
+constexpr int PLAN_SCAN_T = 1024;
+__global__ void __launch_bounds__(PLAN_SCAN_T) k_plan_scan(int32_t n_faces, const int4 *__restrict__ cnt,
+                                                           int4 *__restrict__ off, int32_t *__restrict__ rec_off,
+                                                           int32_t *__restrict__ cold_off,
+                                                           BuildSummary *__restrict__ sum) {
+  __shared__ long long s_part[3][PLAN_SCAN_T];
+  const int t = threadIdx.x;
+  const int per_t = (n_faces + PLAN_SCAN_T - 1) / PLAN_SCAN_T;
+  const int f0 = min(n_faces, t * per_t), f1 = min(n_faces, f0 + per_t);
+  long long a = 0, r = 0, c = 0;
+  for (int f = f0; f < f1; ++f) { a += cnt[f].x; r += cnt[f].y; c += cnt[f].z; }
+  s_part[0][t] = a; s_part[1][t] = r; s_part[2][t] = c;
+  __syncthreads();
+  for (int o = 1; o < PLAN_SCAN_T; o <<= 1) {   // Hillis-Steele inclusive scan
+    long long va = 0, vr = 0, vc = 0;
+    if (t >= o) { va = s_part[0][t - o]; vr = s_part[1][t - o]; vc = s_part[2][t - o]; }
+    __syncthreads();
+    s_part[0][t] += va; s_part[1][t] += vr; s_part[2][t] += vc;
+    __syncthreads();
+  }
+  long long ba = t ? s_part[0][t - 1] : 0, br = t ? s_part[1][t - 1] : 0, bc = t ? s_part[2][t - 1] : 0;
+  for (int f = f0; f < f1; ++f) {
+    off[f] = make_int4((int)ba, (int)br, (int)bc, 0);
+    rec_off[f] = (int)br;
+    cold_off[f] = (int)bc;
+    ba += cnt[f].x; br += cnt[f].y; bc += cnt[f].z;
+  }
+  if (t == PLAN_SCAN_T - 1) {
+    const long long ta = s_part[0][t], tr = s_part[1][t], tc = s_part[2][t];
+    rec_off[n_faces] = (int)tr;
+    cold_off[n_faces] = (int)tc;
+    if (ta > INT32_MAX || tr > INT32_MAX || tc >= (1ll << 23) * 64) sum->toobig = 1;
+    sum->tot_g = (int)ta;
+    sum->tot_r = (int)tr;
+    sum->tot_c = (int)tc;
+  }
+}
+
+__global__ void k_plan_fill(int32_t n_faces, int32_t n_loops, const int32_t *__restrict__ flo,
+                            const uint8_t *__restrict__ fper,
+                            const double *__restrict__ fdom, const double *__restrict__ fM,
+                            const LoopInfo *__restrict__ L, int angle, int tree, const int *__restrict__ pair_beta,
+                            const int *__restrict__ pair_s, const int4 *__restrict__ off,
+                            PlanGroup *__restrict__ groups) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n_faces) return;
+  FaceCtx C = face_ctx(fper[f], fdom + 4 * f, angle != 0);
+  C.M = fM[f];
+  const int4 o = off[f];
+  FillSink S{groups + o.x, f, o.y, o.z, o.z};
+  const int l0 = min(max(flo[f], 0), n_loops), l1 = min(max(flo[f + 1], l0), n_loops);
+  plan_face(S, L, l0, l1, C, pair_beta, pair_s, tree != 0);
 }
 
 }  // namespace wn
@@ -868,7 +1110,9 @@ std::mutex g_build_mu;
 // the next build waits on before reusing the arena (per device).
 cudaEvent_t g_pin_ev[64] = {};
 bool g_pin_pending[64] = {};
-cudaEvent_t g_info_ev_dev[64] = {};
+// per device: the auxiliary stream of the device planner and its fork/join events
+cudaStream_t g_aux[64] = {};
+cudaEvent_t g_ev_lift[64] = {}, g_ev_plan[64] = {}, g_ev_fill[64] = {};
 struct PinRelease {
   cudaEvent_t ev;
   bool *pending;
@@ -933,7 +1177,22 @@ struct BuildCtx {
   cudaStream_t st;
 };
 
-// emit the records of `plan` into a new handle whose faces carry `fper`/`fdom`
+// K2c launch over `ng` device PlanGroups into F's record buffers
+template <typename R>
+cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces_t F) {
+  if (ng <= 0) return cudaSuccess;
+  const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
+  ++g_build_launches;
+  k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, B.st>>>(
+      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl, B.w, B.prep, B.shift, B.brk, B.chain,
+      B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, (Cold<R> *)F->cold,
+      std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
+  return cudaGetLastError();
+}
+
+// emit the records of a HOST `plan` into a new handle whose faces carry
+// `fper`/`fdom` (the pairing probes' virtual faces; the main build plans on
+// the device)
 template <typename R>
 wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<uint8_t> &fper,
                         const std::vector<double> &fdom, const std::vector<double> &fM, wn_faces_t F) {
@@ -989,12 +1248,7 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
     PlanGroup *dg = nullptr;
     WN_CUDA(cache_alloc((void **)&dg, sizeof(PlanGroup) * ng, st));
     WN_CUDA(h2d(dg, plan.groups.data(), sizeof(PlanGroup) * ng, st));
-    const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
-    ++g_build_launches;
-    k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, st>>>(ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl,
-                                                 B.w, B.prep, B.shift, B.brk, B.chain, B.s0pre, B.lend, B.info, rel, (Hot<R> *)F->hot,
-                                                 (Cold<R> *)F->cold, std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
-    WN_CUDA(cudaGetLastError());
+    WN_CUDA(launch_emit<R>(B, ng, dg, F));
     cache_free(dg, st);
   }
   return WN_OK;
@@ -1017,7 +1271,6 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       g_pin_pending[d] = false;
     }
   g_pin.reset();
-  g_tree_opt = !opts || opts->hierarchy != 0;
   if (!out) { set_error("wn_build_faces: out == NULL"); return WN_ERR_ARG; }
   if (n_faces < 0 || n_loops < 0 || n_segs < 0) { set_error("wn_build_faces: negative count"); return WN_ERR_ARG; }
   if (!loop_seg_off || !face_loop_off || (n_faces > 0 && (!face_periodic || !face_domain)) ||
@@ -1046,9 +1299,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   if (dev < 0 || dev >= 64) { set_error("device index out of range"); return WN_ERR_ARG; }
   if (!g_pin_ev[dev]) {
     WN_CUDA(cudaEventCreateWithFlags(&g_pin_ev[dev], cudaEventDisableTiming));
-    WN_CUDA(cudaEventCreateWithFlags(&g_info_ev_dev[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaEventCreateWithFlags(&g_ev_lift[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaEventCreateWithFlags(&g_ev_plan[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaEventCreateWithFlags(&g_ev_fill[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaStreamCreateWithFlags(&g_aux[dev], cudaStreamNonBlocking));
   }
-  cudaEvent_t g_info_ev = g_info_ev_dev[dev];
   cudaStream_t st = (cudaStream_t)stream;
   PinRelease pin_release{g_pin_ev[dev], &g_pin_pending[dev], st};
   DevBuf D;
@@ -1056,7 +1311,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   Trace tr;
 
   // --- host copies of the small CSR / face arrays ---
-  // (pinned staging: the copies stay asynchronous; read after g_info_ev)
+  // (pinned staging: the copies stay asynchronous; read after the plan summary event)
   int32_t *h_lso = (int32_t *)g_pin.get(sizeof(int32_t) * (n_loops + 1));
   int32_t *h_flo = (int32_t *)g_pin.get(sizeof(int32_t) * (n_faces + 1));
   uint8_t *h_per = (uint8_t *)g_pin.get(std::max(n_faces, 1));
@@ -1112,10 +1367,74 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
-  LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
-  if (!L) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
-  if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st));
-  WN_CUDA(cudaEventRecord(g_info_ev, st));
+  // --- K2b on the device, on an auxiliary stream concurrent with K1 ---
+  cudaStream_t st2 = g_aux[dev];
+  WN_CUDA(cudaEventRecord(g_ev_lift[dev], st));
+  WN_CUDA(cudaStreamWaitEvent(st2, g_ev_lift[dev], 0));
+  DevBuf D2;
+  D2.st = st2;
+  wn_faces_t F = new wn_faces_s();
+  std::unique_ptr<wn_faces_s, void (*)(wn_faces_s *)> F_guard(F, [](wn_faces_s *p) { free_handle(p); });
+  F->precision = fp32 ? 1 : 0;
+  F->opt = O;
+  F->eps = eps;
+  F->max_depth = maxd;
+  F->device = dev;
+  F->n_faces = n_faces;
+  const int nf1 = std::max(n_faces, 1);
+  WN_CUDA(cache_alloc((void **)&F->face_rec_off, sizeof(int32_t) * (n_faces + 1), st2));
+  WN_CUDA(cache_alloc((void **)&F->face_cold_off, sizeof(int32_t) * (n_faces + 1), st2));
+  WN_CUDA(cache_alloc((void **)&F->face_order, sizeof(int32_t) * nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->face_dom, sizeof(double) * 4 * nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->face_per, nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->face_ok, nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st2));
+  int32_t *d_status = face_status;
+  if (!d_status) WN_CUDA(D2.alloc(&d_status, nf1));
+  int4 *d_cnt4 = nullptr, *d_off4 = nullptr;
+  uint32_t *d_okey = nullptr, *d_okey2 = nullptr;
+  int32_t *d_oval = nullptr;
+  BuildSummary *d_sum = nullptr;
+  WN_CUDA(D2.alloc(&d_cnt4, nf1));
+  WN_CUDA(D2.alloc(&d_off4, nf1));
+  WN_CUDA(D2.alloc(&d_okey, nf1));
+  WN_CUDA(D2.alloc(&d_okey2, nf1));
+  WN_CUDA(D2.alloc(&d_oval, nf1));
+  WN_CUDA(D2.alloc(&d_sum, 1));
+  size_t sort_tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, d_okey, d_okey2, d_oval, F->face_order, n_faces, 0, 32, st2);
+  char *d_sort_tmp = nullptr;
+  WN_CUDA(D2.alloc(&d_sort_tmp, std::max(sort_tmp, (size_t)16)));
+  BuildSummary *h_sum = (BuildSummary *)g_pin.get(sizeof(BuildSummary));
+  if (!h_sum) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
+  if (n_faces) WN_CUDA(cudaMemsetAsync(F->face_ok, 1, n_faces, st2));
+
+  auto plan_pass = [&](const int *pair_beta, const int *pair_s) -> wn_status_t {
+    WN_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(BuildSummary), st2));
+    WN_CUDA(cudaMemsetAsync(&d_sum->first_bad, 0xFF, sizeof(unsigned long long), st2));
+    if (n_faces) {
+      k_plan_count<<<(n_faces + 127) / 128, 128, 0, st2>>>(
+          n_faces, n_loops, face_loop_off, face_periodic, face_domain, B.info, angle ? 1 : 0, O.strict ? 1 : 0,
+          O.hierarchy ? 1 : 0, fp32 ? 1 : 0, pair_beta, pair_s, d_status, F->face_per, F->face_dom, F->face_M,
+          d_cnt4, d_okey, d_oval, d_sum);
+      k_plan_scan<<<1, PLAN_SCAN_T, 0, st2>>>(n_faces, d_cnt4, d_off4, F->face_rec_off, F->face_cold_off, d_sum);
+      WN_CUDA(cub::DeviceRadixSort::SortPairs(d_sort_tmp, sort_tmp, d_okey, d_okey2, d_oval, F->face_order, n_faces,
+                                              0, 32, st2));
+      g_build_launches += 2 + 4;
+    } else {
+      WN_CUDA(cudaMemsetAsync(F->face_rec_off, 0, sizeof(int32_t), st2));
+      WN_CUDA(cudaMemsetAsync(F->face_cold_off, 0, sizeof(int32_t), st2));
+    }
+    WN_CUDA(cudaGetLastError());
+    WN_CUDA(cudaMemcpyAsync(h_sum, d_sum, sizeof(BuildSummary), cudaMemcpyDeviceToHost, st2));
+    WN_CUDA(cudaEventRecord(g_ev_plan[dev], st2));
+    return WN_OK;
+  };
+  {
+    wn_status_t rc = plan_pass(nullptr, nullptr);
+    if (rc != WN_OK) return rc;
+  }
   // segments sorted by degree so that k_prep's warps run one degree variant
   int32_t *d_order = nullptr;
   if (n_segs) {
@@ -1140,78 +1459,57 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   }
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep + k_s0pre"); }
-  WN_CUDA(cudaEventSynchronize(g_info_ev));
-  tr.mark("loop summaries d2h");
+  WN_CUDA(cudaEventSynchronize(g_ev_plan[dev]));
+  tr.mark("device plan summary");
   // CSR / domain checks on the host (the kernels above clamp every CSR index,
   // so a bad input is reported here without any out-of-bounds access)
+  auto fail = [&](wn_status_t rc) {
+    cudaStreamSynchronize(st2);
+    return rc;
+  };
   bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
   for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
   for (int f = 0; csr_ok && f < n_faces; ++f) csr_ok = h_flo[f] <= h_flo[f + 1];
-  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return WN_ERR_ARG; }
-  if (*h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return WN_ERR_ARG; }
+  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return fail(WN_ERR_ARG); }
+  if (*h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return fail(WN_ERR_ARG); }
   for (int f = 0; f < n_faces; ++f) {
     const double *d = &h_dom[4 * f];
     if ((h_per[f] & 1) && !(std::isfinite(d[0]) && std::isfinite(d[1]) && d[1] > 0)) {
       set_error("face %d: bad u period", f);
-      return WN_ERR_GEOM;
+      return fail(WN_ERR_GEOM);
     }
     if ((h_per[f] & 2) && !(std::isfinite(d[2]) && std::isfinite(d[3]) && d[3] > 0)) {
       set_error("face %d: bad v period", f);
-      return WN_ERR_GEOM;
+      return fail(WN_ERR_GEOM);
     }
   }
+  auto report_bad = [&]() {
+    const int first = (int)(h_sum->first_bad >> 32), code = (int)(h_sum->first_bad & 0xffffffffu);
+    set_error("wn_build_faces: face %d invalid (code %d)", first, code);
+    return fail(h_sum->geom ? WN_ERR_GEOM : (h_sum->unsup ? WN_ERR_UNSUPPORTED : WN_ERR_TOPOLOGY));
+  };
+  if (h_sum->bad) return report_bad();
   tr.mark("host checks");
 
-  // --- K2b: validation + planning (host) ---
-  static std::vector<int32_t> status;
-  static std::vector<FaceCtx> ctx;
-  status.assign(n_faces, WN_FACE_OK);
-  ctx.resize(n_faces);
-  // pairing requests for bi-periodic faces
-  struct Cand { int face, alpha, beta, s; double px, py; };
-  std::vector<int> need_pair;
-  static std::vector<uint8_t> needp;
-  needp.assign(n_faces, 0);
-#pragma omp parallel for schedule(static, 256)
-  for (int f = 0; f < n_faces; ++f) {
-    FaceCtx &C = ctx[f];
-    C.per = h_per[f] & 3;
-    C.u0 = h_dom[4 * f]; C.Tu = h_dom[4 * f + 1]; C.v0 = h_dom[4 * f + 2]; C.Tv = h_dom[4 * f + 3];
-    if (!(C.per & 1)) { C.u0 = 0; C.Tu = 0; }
-    if (!(C.per & 2)) { C.v0 = 0; C.Tv = 0; }
-    C.angle = angle;
-    C.M = face_margin(L, h_flo[f], h_flo[f + 1], C, fp32);
-    int cp = 0, cq = 0, nA = 0, nB = 0;
-    for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
-      const LoopInfo &I = L[l];
-      if (I.err) status[f] = WN_FACE_GEOM;
-      if (I.nseg == 0 || (I.cu == 0 && I.cv == 0)) continue;
-      if (C.per == 1 && std::abs(I.cu) > 1) status[f] = WN_FACE_B1;
-      if (C.per == 2 && std::abs(I.cv) > 1) status[f] = WN_FACE_B1;
-      if (gcd_i(I.cu, I.cv) != 1 && !status[f]) status[f] = WN_FACE_CLASS;
-      if (cp == 0 && cq == 0) { cp = I.cu; cq = I.cv; }
-      if (I.cu == cp && I.cv == cq) ++nA;
-      else if (I.cu == -cp && I.cv == -cq) ++nB;
-      else if (!status[f]) status[f] = WN_FACE_CLASS;
+  const int *d_pair_beta = nullptr, *d_pair_s = nullptr;
+  if (h_sum->needp) {
+    // --- pairing (Algs. 7-9) for bi-periodic faces via probe queries (host) ---
+    LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
+    if (!L) { set_error("pinned host allocation failed"); return fail(WN_ERR_NOMEM); }
+    if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st2));
+    WN_CUDA(cudaStreamSynchronize(st2));
+    std::vector<FaceCtx> ctx(n_faces);
+    std::vector<int32_t> status(n_faces, WN_FACE_OK);
+    std::vector<int> need_pair;
+    for (int f = 0; f < n_faces; ++f) {
+      ctx[f] = face_ctx(h_per[f], &h_dom[4 * f], angle);
+      ctx[f].M = face_margin(L, h_flo[f], h_flo[f + 1], ctx[f], fp32);
+      int np = 0;
+      face_validate(L, h_flo[f], h_flo[f + 1], ctx[f], O.strict != 0, &np);
+      if (np) need_pair.push_back(f);
     }
-    if (status[f]) continue;
-    if (nA != nB && (O.strict || C.per == 3)) { status[f] = WN_FACE_UNBALANCED; continue; }
-    if (C.per == 3 && nA > 0) {
-      if (cp != 0 && cq != 0) { status[f] = WN_FACE_GENERAL_PQ; continue; }
-      needp[f] = 1;
-    }
-  }
-  for (int f = 0; f < n_faces; ++f)
-    if (needp[f]) need_pair.push_back(f);
-  bool any_bad = false;
-  for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
-
-  // --- pairing (Algs. 7-9) for bi-periodic faces via probe queries ---
-  // pair_beta[alpha] = beta, pair_s[alpha] = transverse translate of beta
-  static std::vector<int> pair_beta, pair_s;
-  pair_beta.assign(n_loops, -1);
-  pair_s.assign(n_loops, 0);
-  if (!any_bad && !need_pair.empty()) {
+    struct Cand { int face, alpha, beta, s; double px, py; };
+    std::vector<int> pair_beta(n_loops, -1), pair_s(n_loops, 0);
     // virtual faces: one uni-periodic extended curve per non-contractible loop
     std::vector<int> vface(n_loops, -1);
     Plan VP;
@@ -1231,13 +1529,12 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
         vM.push_back(C.M);
         VP.begin_face(vface[l]);
         VP.add(G_LINE, 0, l, 0, 0, I, C.M);
-        plan_extended_copies(VP, l, I, C, axis, 0, false);
+        plan_extended_copies(VP, l, I, C, axis, 0, false, O.hierarchy != 0);
       }
     }
     VP.end();
     // candidates: beta translates along the transverse axis (R16 window)
     std::vector<Cand> cands;
-    std::vector<int> cand_alpha_q;   // query index of ToLeft(cand, alpha)
     struct QueryRec { int vf; double x, y; };
     std::vector<QueryRec> qs;
     for (int f : need_pair) {
@@ -1263,6 +1560,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       }
     }
     // run probes through the query kernel on a temporary handle (fp64, crossing mode)
+    WN_CUDA(cudaStreamSynchronize(st));   // K1 outputs (bounds, span prefixes) are read by the probes' k_emit
     auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
       wn_faces_t T = new wn_faces_s();
       T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0;
@@ -1290,7 +1588,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     };
     std::vector<double> r1;
     wn_status_t rc = run_probes(qs, r1);
-    if (rc != WN_OK) return rc;
+    if (rc != WN_OK) return fail(rc);
     // candidates left of alpha (ToLeft, Alg. 7: omega > 0)
     std::vector<int> left;
     for (size_t i = 0; i < cands.size(); ++i)
@@ -1301,18 +1599,18 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     for (int i : left)
       for (int j : left) {
         if (i == j || cands[i].alpha != cands[j].alpha) continue;
-        const Cand &a = cands[i], &b = cands[j];
+        const Cand &a = cands[i], &bb = cands[j];
         const FaceCtx &C = ctx[a.face];
         const int tax = (L[a.alpha].cu != 0) ? 1 : 0;
         const double Tt = tax ? C.Tv : C.Tu;
         // omega(pt(c1) - s2*T_t e_t, beta2_ext) (translation identity, App. C.1)
-        q2.push_back({vface[b.beta], a.px - (tax ? 0.0 : b.s * Tt), a.py - (tax ? b.s * Tt : 0.0)});
+        q2.push_back({vface[bb.beta], a.px - (tax ? 0.0 : bb.s * Tt), a.py - (tax ? bb.s * Tt : 0.0)});
         q2pairs.push_back({i, j});
       }
     std::vector<double> r2;
     if (!q2.empty()) {
       rc = run_probes(q2, r2);
-      if (rc != WN_OK) return rc;
+      if (rc != WN_OK) return fail(rc);
     }
     auto to_left = [&](int i, int j) {
       for (size_t k = 0; k < q2pairs.size(); ++k)
@@ -1321,6 +1619,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     };
     // Alg. 9 PairLoops: greedy nearest-left proper translate per alpha
     std::vector<uint8_t> used(n_loops, 0);
+    int pairing_failed = -1;
     for (int f : need_pair) {
       for (int la = h_flo[f]; la < h_flo[f + 1]; ++la) {
         bool is_alpha = false;
@@ -1336,154 +1635,62 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
             if (cands[i].alpha != la || used[cands[i].beta]) continue;
             if (best < 0 || to_left(i, best)) best = i;
           }
-        if (best < 0) { status[f] = WN_FACE_PAIRING; break; }
+        if (best < 0) { status[f] = WN_FACE_PAIRING; if (pairing_failed < 0) pairing_failed = f; break; }
         used[cands[best].beta] = 1;
         pair_beta[la] = cands[best].beta;
         pair_s[la] = cands[best].s;
       }
     }
-    for (int f = 0; f < n_faces; ++f) any_bad |= status[f] != 0;
+    if (pairing_failed >= 0) {
+      if (face_status) {
+        for (int f = 0; f < n_faces; ++f)
+          if (status[f]) WN_CUDA(cudaMemcpyAsync(face_status + f, &status[f], sizeof(int32_t), cudaMemcpyHostToDevice, st2));
+      }
+      set_error("wn_build_faces: face %d invalid (code %d)", pairing_failed, (int)WN_FACE_PAIRING);
+      return fail(WN_ERR_TOPOLOGY);
+    }
+    int *d_pb = nullptr, *d_ps = nullptr;
+    WN_CUDA(D2.alloc(&d_pb, std::max(n_loops, 1)));
+    WN_CUDA(D2.alloc(&d_ps, std::max(n_loops, 1)));
+    if (n_loops) {
+      WN_CUDA(h2d(d_pb, pair_beta.data(), sizeof(int) * n_loops, st2));
+      WN_CUDA(h2d(d_ps, pair_s.data(), sizeof(int) * n_loops, st2));
+    }
+    rc = plan_pass(d_pb, d_ps);
+    if (rc != WN_OK) return fail(rc);
+    WN_CUDA(cudaEventSynchronize(g_ev_plan[dev]));
+    if (h_sum->bad) return report_bad();
+    tr.mark("pairing probes + re-plan");
+    // the fill pass below also needs the pairs
+    d_pair_beta = d_pb;
+    d_pair_s = d_ps;
   }
-  if (face_status && n_faces)
-    WN_CUDA(h2d(face_status, status.data(), sizeof(int32_t) * n_faces, st));
-  if (any_bad) {
-    WN_CUDA(cudaStreamSynchronize(st));
-    int first = 0;
-    while (first < n_faces && !status[first]) ++first;
-    set_error("wn_build_faces: face %d invalid (code %d)", first, status[first]);
-    bool geom = false, unsup = false;
-    for (int f = 0; f < n_faces; ++f) { geom |= status[f] == WN_FACE_GEOM; unsup |= status[f] == WN_FACE_GENERAL_PQ; }
-    return geom ? WN_ERR_GEOM : (unsup ? WN_ERR_UNSUPPORTED : WN_ERR_TOPOLOGY);
-  }
+  if (h_sum->toobig) { set_error("too many records (22/24-bit record indices)"); return fail(WN_ERR_ARG); }
 
-  tr.mark("validate + pairing");
-  // --- final plan: faces planned in parallel (contiguous face ranges per
-  // thread, concatenated in face order with offset fix-ups) ---
-  static std::vector<double> fdom;
-  fdom.resize(4 * (size_t)n_faces);
-  for (int f = 0; f < n_faces; ++f) {
-    const FaceCtx &C = ctx[f];
-    fdom[4 * f] = C.u0; fdom[4 * f + 1] = C.Tu; fdom[4 * f + 2] = C.v0; fdom[4 * f + 3] = C.Tv;
+  // --- K2c: record buffers, group fill (aux stream), emission (after K1) ---
+  F->n_records = h_sum->tot_r;
+  F->n_seg = h_sum->tot_c;
+  F->n_lines = (int64_t)h_sum->lines;
+  F->n_groups = (int64_t)h_sum->cull;
+  F->max_face_records = h_sum->maxr;
+  WN_CUDA(cache_alloc(&F->hot, (fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * (size_t)std::max(h_sum->tot_r, 1), st));
+  WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * (size_t)std::max(h_sum->tot_c, 1), st));
+  F->bytes = (int64_t)(fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * h_sum->tot_r +
+             (int64_t)(fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * h_sum->tot_c + (int64_t)n_faces * 50;
+  const int ng = h_sum->tot_g;
+  PlanGroup *d_groups = nullptr;
+  WN_CUDA(D2.alloc(&d_groups, std::max(ng, 1)));
+  if (ng) {
+    k_plan_fill<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, face_loop_off, F->face_per, F->face_dom,
+                                                        F->face_M, B.info, angle ? 1 : 0, O.hierarchy ? 1 : 0,
+                                                        d_pair_beta, d_pair_s, d_off4, d_groups);
+    ++g_build_launches;
+    WN_CUDA(cudaGetLastError());
   }
-  tr.mark("plan: fdom");
-  auto plan_face = [&](Plan &P, int f) {
-    const FaceCtx &C = ctx[f];
-    for (int l = h_flo[f]; l < h_flo[f + 1]; ++l) {
-      const LoopInfo &I = L[l];
-      if (I.nseg == 0) continue;
-      if (C.per == 0 || (I.cu == 0 && I.cv == 0)) {
-        plan_contractible(P, l, I, C);
-        continue;
-      }
-      const int axis = (I.cu != 0) ? 0 : 1;
-      if (C.per != 3) {
-        // uni-periodic non-contractible loop: omega(p,L) + copies (Eq. 5)
-        P.add(G_LINE, 0, l, 0, 0, I, C.M);
-        plan_extended_copies(P, l, I, C, axis, 0, false);
-        continue;
-      }
-      // bi-periodic: alpha loops drive Eq. 8 for their pair; beta loops are emitted with them
-      if (pair_beta[l] < 0) continue;
-      const int lb = pair_beta[l];
-      const int sb = pair_s[l];
-      const LoopInfo &Ib = L[lb];
-      const int tax = axis == 0 ? 1 : 0;
-      const double Tt = tax ? C.Tv : C.Tu, t0 = tax ? C.v0 : C.u0;
-      const double m = 1e-9 * (1.0 + std::fabs(C.u0) + C.Tu + std::fabs(C.v0) + C.Tv);
-      // transverse window: every band offset j whose lines or copies can meet the tile
-      const double ca = tax ? I.sy : I.sx, cb = (tax ? Ib.sy : Ib.sx) + sb * Tt;
-      const double lo = std::min({ca, cb, tax ? I.bb[1] : I.bb[0], (tax ? Ib.bb[1] : Ib.bb[0]) + sb * Tt});
-      const double hi = std::max({ca, cb, tax ? I.bb[3] : I.bb[2], (tax ? Ib.bb[3] : Ib.bb[2]) + sb * Tt});
-      int j0, j1;
-      k_range(lo, hi, t0, Tt, m, j0, j1);
-      for (int j = j0; j <= j1; ++j) {
-        // Eq. 8 band j: omega(p, L_alpha) + omega(p, L_beta) only when the strip meets the tile
-        const double la_c = ca + j * Tt, lb_c = cb + j * Tt;
-        if (std::min(la_c, lb_c) <= t0 + Tt + m && std::max(la_c, lb_c) >= t0 - m) {
-          if (axis == 0) { P.add(G_LINE, 0, l, 0, j, I, C.M); P.add(G_LINE, 0, lb, 0, sb + j, Ib, C.M); }
-          else { P.add(G_LINE, 0, l, j, 0, I, C.M); P.add(G_LINE, 0, lb, sb + j, 0, Ib, C.M); }
-        }
-        plan_extended_copies(P, l, I, C, axis, j, true);
-        plan_extended_copies(P, lb, Ib, C, axis, sb + j, true);
-      }
-    }
-  };
-  const int nth = std::max(1, std::min(omp_get_max_threads(), std::max(1, n_faces / 256)));
-  static std::vector<Plan> TP;
-  if ((int)TP.size() < nth) TP.resize(nth);
-  for (int i = 0; i < nth; ++i) TP[i].clear();
-#pragma omp parallel for num_threads(nth) schedule(static, 1)
-  for (int tid = 0; tid < nth; ++tid) {
-    const int f0 = (int)((int64_t)n_faces * tid / nth), f1 = (int)((int64_t)n_faces * (tid + 1) / nth);
-    Plan &Q = TP[tid];
-    Q.reserve((size_t)(h_flo[f1] - h_flo[f0]) * 2 + 16, (size_t)(f1 - f0));
-    for (int f = f0; f < f1; ++f) {
-      Q.begin_face(f);
-      plan_face(Q, f);
-    }
-  }
-  tr.mark("plan: parallel faces");
-  static Plan P;
-  P.clear();
-  {
-    // per-thread group / record / cold bases, then a parallel copy with offset fix-ups
-    static std::vector<size_t> gb, fb;
-    static std::vector<int32_t> rb, cb;
-    gb.assign(nth + 1, 0); fb.assign(nth + 1, 0); rb.assign(nth + 1, 0); cb.assign(nth + 1, 0);
-    for (int t = 0; t < nth; ++t) {
-      const Plan &Q = TP[t];
-      gb[t + 1] = gb[t] + Q.groups.size();
-      fb[t + 1] = fb[t] + Q.rec_off.size();
-      rb[t + 1] = rb[t] + Q.recs;
-      cb[t + 1] = cb[t] + Q.colds;
-      P.n_lines += Q.n_lines;
-      P.n_cull += Q.n_cull;
-    }
-    P.groups.resize(gb[nth]);
-    P.rec_off.resize(fb[nth]);
-    P.cold_off.resize(fb[nth]);
-#pragma omp parallel for num_threads(nth) schedule(static, 1)
-    for (int t = 0; t < nth; ++t) {
-      const Plan &Q = TP[t];
-      PlanGroup *dg = P.groups.data() + gb[t];
-      for (size_t i = 0; i < Q.groups.size(); ++i) {
-        PlanGroup G = Q.groups[i];
-        G.rec_off += rb[t];
-        G.cold_off += cb[t];
-        dg[i] = G;
-      }
-      for (size_t i = 0; i < Q.rec_off.size(); ++i) {
-        P.rec_off[fb[t] + i] = Q.rec_off[i] + rb[t];
-        P.cold_off[fb[t] + i] = Q.cold_off[i] + cb[t];
-      }
-    }
-    P.recs = rb[nth];
-    P.colds = cb[nth];
-  }
-  P.end();
-  if (P.recs < 0 || P.colds >= (1 << 23) * 64) { set_error("too many records"); return WN_ERR_ARG; }
-  for (int f = 0; f < n_faces; ++f)
-    if (P.cold_off[f + 1] - P.cold_off[f] >= (1 << 22) || P.rec_off[f + 1] - P.rec_off[f] >= (1 << 24)) {
-      set_error("face %d: too many records for the 22/24-bit record indices", f);
-      return WN_ERR_ARG;
-    }
-
-  tr.mark("plan: concat + checks");
-  wn_faces_t F = new wn_faces_s();
-  F->precision = fp32 ? 1 : 0;
-  F->opt = O;
-  F->eps = eps;
-  F->max_depth = maxd;
-  F->device = dev;
-  static std::vector<uint8_t> fper;
-  fper.resize(n_faces);
-  for (int f = 0; f < n_faces; ++f) fper[f] = ctx[f].per;
-  static std::vector<double> fM;
-  fM.resize(n_faces);
-  for (int f = 0; f < n_faces; ++f) fM[f] = ctx[f].M;
-  wn_status_t rc = fp32 ? materialise<float>(B, P, fper, fdom, fM, F) : materialise<double>(B, P, fper, fdom, fM, F);
-  if (rc != WN_OK) { free_handle(F); return rc; }
-  tr.mark("materialise (alloc+h2d+emit)");
+  WN_CUDA(cudaEventRecord(g_ev_fill[dev], st2));
+  WN_CUDA(cudaStreamWaitEvent(st, g_ev_fill[dev], 0));   // join: K2c after the plan and after K1
+  WN_CUDA(fp32 ? launch_emit<float>(B, ng, d_groups, F) : launch_emit<double>(B, ng, d_groups, F));
+  tr.mark("device plan fill + emit (enqueued)");
   // no final synchronisation: the handle's records are complete in stream
   // order, so queries enqueued on `stream` after this call see them
   {
@@ -1491,10 +1698,10 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&F->ready, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(F->last_use, st);
     if (e == cudaSuccess) e = cudaEventRecord(F->ready, st);
-    if (e != cudaSuccess) { free_handle(F); return cuda_fail(e, "build event"); }
+    if (e != cudaSuccess) return cuda_fail(e, "build event");
   }
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_emit"); }
-  *out = F;
+  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_plan_fill + k_emit"); }
+  *out = F_guard.release();
   return WN_OK;
 }
 

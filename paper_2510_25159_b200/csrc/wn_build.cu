@@ -86,6 +86,8 @@ __host__ __device__ constexpr double binom_c(int n, int k) {
 // i = 0..N, held in registers (templated on the degree, fully unrolled).
 // Written without accumulating into local arrays (an earlier version of that
 // shape was miscompiled by nvcc 12.9 -O3 on sm_100a: scripts/dev/kp.cu).
+// Norms are compared squared and rooted once; the bounds' rounding (a few
+// ulps) is covered by the (1 + 2^-40) factor k_emit applies (R5).
 //
 // Hodograph-numerator Bernstein bound: |gamma'| = |X'W - XW'| / W^2 with
 //   X'W - XW' = N sum_k D_k B_k^{2N-1},
@@ -95,7 +97,7 @@ __host__ __device__ constexpr double binom_c(int n, int k) {
 template <int N>
 __device__ __forceinline__ double hodo_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
                                              const double (&W)[N + 1]) {
-  double dmax = 0.0, emin = INFINITY;
+  double d2max = 0.0, emin = INFINITY;
 #pragma unroll
   for (int k = 0; k <= 2 * N - 1; ++k) {
     double dx = 0.0, dy = 0.0;
@@ -107,7 +109,7 @@ __device__ __forceinline__ double hodo_bound(const double (&X)[N + 1], const dou
       dx += c * (W[j] * (X[i + 1] - X[i]) - (W[i + 1] - W[i]) * X[j]);
       dy += c * (W[j] * (Y[i + 1] - Y[i]) - (W[i + 1] - W[i]) * Y[j]);
     }
-    dmax = fmax(dmax, hypot(dx, dy));
+    d2max = fmax(d2max, dx * dx + dy * dy);
   }
 #pragma unroll
   for (int k = 0; k <= 2 * N; ++k) {
@@ -120,58 +122,82 @@ __device__ __forceinline__ double hodo_bound(const double (&X)[N + 1], const dou
     }
     emin = fmin(emin, e);
   }
-  return N * dmax / emin;
+  return N * sqrt(d2max) / emin;
 }
 
+// Floater's rational bounds on the affine control points (x_i, y_i) and weights
 template <int N>
-__device__ __forceinline__ double floater_bound(const double (&X)[N + 1], const double (&Y)[N + 1],
+__device__ __forceinline__ double floater_bound(const double (&px)[N + 1], const double (&py)[N + 1],
                                                 const double (&W)[N + 1]) {
-  double wmax = W[0], wmin = W[0], dmax = 0.0, diam = 0.0, px[N + 1], py[N + 1];
+  double wmax = W[0], wmin = W[0], d2max = 0.0, diam2 = 0.0;
 #pragma unroll
   for (int i = 1; i <= N; ++i) { wmax = fmax(wmax, W[i]); wmin = fmin(wmin, W[i]); }
-#pragma unroll
-  for (int i = 0; i <= N; ++i) { px[i] = X[i] / W[i]; py[i] = Y[i] / W[i]; }
 #pragma unroll
   for (int i = 0; i <= N; ++i)
 #pragma unroll
     for (int j = i + 1; j <= N; ++j) {
-      const double l = hypot(px[j] - px[i], py[j] - py[i]);
-      diam = fmax(diam, l);
-      if (j == i + 1) dmax = fmax(dmax, l);
+      const double dx = px[j] - px[i], dy = py[j] - py[i];
+      const double l2 = dx * dx + dy * dy;
+      diam2 = fmax(diam2, l2);
+      if (j == i + 1) d2max = fmax(d2max, l2);
     }
+  const double dmax = sqrt(d2max);
   if (wmax == wmin) return N * dmax;
   const double r = wmax / wmin;
-  return fmin(N * r * diam, N * r * r * dmax);
+  return fmin(N * r * sqrt(diam2), N * r * r * dmax);
 }
 
-// piece [q/8,(q+1)/8]: three de Casteljau halvings along the bits of q
+// Subdivision matrices of the dyadic pieces [q/8, (q+1)/8]: piece control
+// point i = sum_j S[N][q][i][j] P_j.  Generated at compile time by three de
+// Casteljau halvings of the unit control vectors (entries are dyadic
+// rationals with denominators <= 2^15: exact in double).
+struct SubTab {
+  double m[5][8][6][6];
+};
+constexpr SubTab make_subtab() {
+  SubTab T{};
+  for (int N = 1; N <= 5; ++N)
+    for (int q = 0; q < 8; ++q)
+      for (int col = 0; col <= N; ++col) {
+        double a[6] = {0, 0, 0, 0, 0, 0};
+        a[col] = 1.0;
+        for (int lvl = 2; lvl >= 0; --lvl) {
+          const bool right = (q >> lvl) & 1;
+          double t[6] = {a[0], a[1], a[2], a[3], a[4], a[5]};
+          double o[6] = {0, 0, 0, 0, 0, 0};
+          o[0] = t[0];
+          o[N] = t[N];
+          // after round r, entry 0 is the left half's point r, entry N-r the right half's
+          for (int r = 1; r <= N; ++r) {
+            for (int j = 0; j <= N - r; ++j) t[j] = 0.5 * (t[j] + t[j + 1]);
+            if (right) o[N - r] = t[N - r];
+            else o[r] = t[0];
+          }
+          if (right) o[N] = a[N];
+          else o[0] = a[0];
+          for (int i = 0; i <= N; ++i) a[i] = o[i];
+        }
+        for (int i = 0; i <= N; ++i) T.m[N - 1][q][i][col] = a[i];
+      }
+  return T;
+}
+__constant__ SubTab c_sub = make_subtab();
+
 template <int N>
 __device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const double (&Y)[N + 1],
                                              const double (&W)[N + 1], int q, double (&a)[N + 1],
                                              double (&b)[N + 1], double (&c)[N + 1]) {
 #pragma unroll
-  for (int i = 0; i <= N; ++i) { a[i] = X[i]; b[i] = Y[i]; c[i] = W[i]; }
+  for (int i = 0; i <= N; ++i) {
+    double sa = 0.0, sb = 0.0, sc = 0.0;
 #pragma unroll
-  for (int lvl = 2; lvl >= 0; --lvl) {
-    const bool right = (q >> lvl) & 1;
-    double ta[N + 1], tb[N + 1], tc[N + 1];
-#pragma unroll
-    for (int i = 0; i <= N; ++i) { ta[i] = a[i]; tb[i] = b[i]; tc[i] = c[i]; }
-    // after round r, entry 0 is the left half's point r, entry N-r the right half's
-#pragma unroll
-    for (int r = 1; r <= N; ++r) {
-#pragma unroll
-      for (int j = 0; j <= N - r; ++j) {
-        ta[j] = 0.5 * (ta[j] + ta[j + 1]);
-        tb[j] = 0.5 * (tb[j] + tb[j + 1]);
-        tc[j] = 0.5 * (tc[j] + tc[j + 1]);
-      }
-      if (right) {
-        a[N - r] = ta[N - r]; b[N - r] = tb[N - r]; c[N - r] = tc[N - r];
-      } else {
-        a[r] = ta[0]; b[r] = tb[0]; c[r] = tc[0];
-      }
+    for (int j = 0; j <= N; ++j) {
+      const double m = c_sub.m[N - 1][q][i][j];
+      sa = fma(m, X[j], sa);
+      sb = fma(m, Y[j], sb);
+      sc = fma(m, W[j], sc);
     }
+    a[i] = sa; b[i] = sb; c[i] = sc;
   }
 }
 
@@ -182,7 +208,7 @@ __device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const dou
 template <int N>
 __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o, int q,
                                        SegPrep *__restrict__ out, uint8_t *__restrict__ err_out) {
-  double X[N + 1], Y[N + 1], W[N + 1];
+  double X[N + 1], Y[N + 1], W[N + 1], px[N + 1], py[N + 1];
   bool err = false;
   double lpoly = 0.0;
 #pragma unroll
@@ -190,12 +216,13 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1], wj = w ? w[o + j] : 1.0;
     err |= !isfinite(x) || !isfinite(y) || !isfinite(wj) || !(wj > 0.0);
     X[j] = wj * x; Y[j] = wj * y; W[j] = wj;
-    if (j) lpoly += hypot(x - ctrl[2 * (o + j - 1)], y - ctrl[2 * (o + j - 1) + 1]);
+    px[j] = x; py[j] = y;
+    if (j) lpoly += hypot(x - px[j - 1], y - py[j - 1]);
   }
   if (q == 8) {
     *err_out = err ? 1 : 0;
     if (err) { out->B = out->S0 = 0.0; return; }
-    const double B = fmin(floater_bound<N>(X, Y, W), hodo_bound<N>(X, Y, W));
+    const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
     out->B = B;
     out->S0 = fmin(B, lpoly);
     return;

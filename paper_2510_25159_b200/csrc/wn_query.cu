@@ -103,29 +103,37 @@ __device__ __forceinline__ void cnt_add(unsigned long long *c, int i, unsigned l
   if (COUNT && v) atomicAdd(c + i, v);
 }
 
-// Rational Bezier point by O(n) Horner in s = t/(1-t) (t <= 1/2) or
-// s = (1-t)/t (t > 1/2) on homogeneous coefficients (Table 1).
+// Rational Bezier point by O(n) homogeneous Horner on c_j = C(n,j) w_j (P_j, 1)
+// (Table 1):  sum_j c_j t^j (1-t)^(n-j)  =  (...(c_n t + c_{n-1} u) t
+// + c_{n-2} u^2) t + ...,  u = 1-t.  t and u lie in [0,1] (no t/(1-t) blow-up,
+// no branch on t), and the loop runs over the padded maximum degree with the
+// zero coefficients above n, so every lane of a warp runs the same code
+// whatever its segment's degree (the coefficient pairs load as 16-B vectors).
 template <typename R>
 __device__ __forceinline__ void eval_point(const Cold<R> *__restrict__ C, int n, R t, R &x, R &y) {
-  R X, Y, W;
-  if (t <= R(0.5)) {
-    R s = t / (R(1) - t);
-    X = __ldg(&C->cx[n]); Y = __ldg(&C->cy[n]); W = __ldg(&C->cw[n]);
-    for (int j = n - 1; j >= 0; --j) {
-      X = X * s + __ldg(&C->cx[j]);
-      Y = Y * s + __ldg(&C->cy[j]);
-      W = W * s + __ldg(&C->cw[j]);
+  const R u = R(1) - t;
+  R cx[6], cy[6], cw[6];
+  if constexpr (sizeof(R) == 8) {
+#pragma unroll
+    for (int j = 0; j < 6; j += 2) {
+      const double2 a = __ldg(reinterpret_cast<const double2 *>(&C->cx[j]));
+      const double2 b = __ldg(reinterpret_cast<const double2 *>(&C->cy[j]));
+      const double2 c = __ldg(reinterpret_cast<const double2 *>(&C->cw[j]));
+      cx[j] = a.x; cx[j + 1] = a.y; cy[j] = b.x; cy[j + 1] = b.y; cw[j] = c.x; cw[j + 1] = c.y;
     }
   } else {
-    R s = (R(1) - t) / t;
-    X = __ldg(&C->cx[0]); Y = __ldg(&C->cy[0]); W = __ldg(&C->cw[0]);
-    for (int j = 1; j <= n; ++j) {
-      X = X * s + __ldg(&C->cx[j]);
-      Y = Y * s + __ldg(&C->cy[j]);
-      W = W * s + __ldg(&C->cw[j]);
-    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) { cx[j] = __ldg(&C->cx[j]); cy[j] = __ldg(&C->cy[j]); cw[j] = __ldg(&C->cw[j]); }
   }
-  R iw = R(1) / W;
+  R X = 0, Y = 0, W = 0, up = 1;
+#pragma unroll
+  for (int j = 5; j >= 0; --j) {
+    X = X * t + cx[j] * up;
+    Y = Y * t + cy[j] * up;
+    W = W * t + cw[j] * up;
+    up = (j <= n) ? up * u : up;
+  }
+  const R iw = R(1) / W;
   x = X * iw;
   y = Y * iw;
 }

@@ -42,15 +42,23 @@ WORKLOAD = ("C5 synthetic B-Rep batch / tessellation: 20000 faces, loops 1-8 (ge
 
 # Roofline of the dominant kernel, k_phase1 (DESIGN.md 6 "Roofline"): after the
 # fp32 filter, the telescoped crossings and the path hierarchy it is bound by
-# SM instruction issue (ncu: issue-active ~59%, FP64 pipe ~8%, FMA pipe ~11%),
-# so the roofline is the issue rate: 148 SMs x 4 schedulers x 1 warp-instruction
-# per clock at the 1965 MHz max SM clock (MEASURED_PEAKS.json sm_max_mhz).
+# SM instruction issue (ncu: FP64 / FMA pipes far from busy, issue slots the
+# limiter), so the roofline is the issue rate: 148 SMs x 4 schedulers x 1
+# warp-instruction per clock at the 1965 MHz max SM clock.
 ISSUE_PEAK = 148 * 4 * 1.965e9 / 1e9          # G warp-instructions / s
-# Work per unit of k_phase1, this implementation (profiles/round1: ncu
-# smsp__inst_executed.sum / the counters of the same launch): warp instructions
-# per warp-record iteration (record read, tests of 32 queries, hierarchy
-# decisions, hard-pair pushes amortised).
-INSTR_PER_WARP_RECORD = 74.8
+# Work per unit (warp-record iteration) of THIS implementation and the DRAM
+# traffic per launch come from the committed ncu --set full capture of the
+# same bench command (scripts/ncu_k3_metrics.py writes the JSON); the unit
+# count (warp_records) is measured live by the device counters below.
+K3_METRICS = os.path.join(ROOT, "profiles", "round1", "k_phase1_metrics.json")
+
+
+def _k3_metrics():
+    try:
+        with open(K3_METRICS) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
 
 
 def _env_int(k, d):
@@ -257,15 +265,13 @@ def main():
     tw0 = time.time()
     e0.record(st)
     k3_ms, p1_ms, k3_n = 0.0, 0.0, 0
+    wn.freed_timing()              # drop stale entries
     for _ in range(args.steps):
-        h = step(timing=True)
-        ms, p1, n = h.timing()    # waits on the K3 events of this step (build already synced)
-        k3_ms += ms
-        p1_ms += p1
-        k3_n += n
+        h = step(timing=True)     # K3 events recorded on the stream; no host wait per step
         h.close()
     e1.record(st)
     torch.cuda.synchronize()
+    k3_ms, p1_ms, k3_n = wn.freed_timing()
     tw1 = time.time()
     if dist:
         dist.barrier()
@@ -340,18 +346,24 @@ def main():
 
     # ---- roofline of the dominant kernel (k_phase1) ----
     k3_avg = k3_ms / max(k3_n, 1)
-    p1_avg = p1_ms / max(k3_n, 1)
-    work = INSTR_PER_WARP_RECORD * cnt["warp_records"] / 1e9          # G warp-instructions per launch
-    achieved = work / (p1_avg / 1e3)
-    # dram traffic of k_phase1 per launch from the committed ncu --set full capture
+    p1_avg = p1_ms / max(k3_n, 1)      # measured live in the timed region (CUDA events on the stream)
+    met = _k3_metrics()
+    if met:
+        ipr = met["inst_executed"] / met["warp_records"]
+        work = ipr * cnt["warp_records"] / 1e9          # G warp-instructions per launch
+        achieved = work / (p1_avg / 1e3)
+        traffic = met["dram_bytes"]
+    else:
+        ipr, achieved, traffic = None, None, None
     roofline = {"bound": "alu", "achieved": achieved, "peak": ISSUE_PEAK, "unit": "Gwarp-inst/s",
-                "frac": achieved / ISSUE_PEAK, "traffic": 2.278e9,
+                "frac": (achieved / ISSUE_PEAK) if achieved else None, "traffic": traffic,
                 "kernel": "wn::k_phase1<double>", "kernel_ms": p1_avg, "kernel_share_of_step": p1_avg / ms_step,
                 "k3_ms": k3_avg,
                 "peak_source": "derived: 148 SMs x 4 schedulers x 1 warp-inst/clk x 1.965 GHz (max SM clock)",
-                "units": {"warp_records": cnt["warp_records"], "instr_per_warp_record": INSTR_PER_WARP_RECORD},
-                "pipes_ncu": {"fp64_pct": 7.6, "fma_pct": 11.2, "alu_pct": 46.3, "xu_pct": 11.8,
-                              "issue_active_pct": 58.9, "src": "profiles/round1/ncu_full_k3_raw.csv"}}
+                "units": {"warp_records": cnt["warp_records"], "instr_per_warp_record": ipr,
+                          "src": os.path.relpath(K3_METRICS, ROOT) if met else None},
+                "pipes_ncu": ({k: met[k] for k in ("fp64_pct", "fma_pct", "alu_pct", "xu_pct", "issue_active_pct")
+                               if k in met} if met else None)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

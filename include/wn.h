@@ -136,7 +136,8 @@ wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [hos
  * launching stream around every K3 launch -- phase 1, hard pairs, overflow,
  * finish -- and after its phase 1, while enabled).  wn_get_timing waits for the
  * recorded events, returns the summed K3 and phase-1 milliseconds and the
- * number of timed queries since the last call, and resets them. */
+ * number of timed queries since the last call, and resets them.  faces = NULL
+ * reads the timing of handles that were freed before it was read. */
 wn_status_t wn_set_timing(wn_faces_t faces, int enable);
 wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, double *phase1_ms /* [host] or NULL */,
                           int64_t *k3_launches /* [host] */);

@@ -248,6 +248,17 @@ class Faces:
             pass
 
 
+def freed_timing():
+    """(K3 ms, phase-1 ms, timed queries) of handles freed before their timing was read."""
+    ms = C.c_double()
+    p1 = C.c_double()
+    n = C.c_int64()
+    rc = load().wn_get_timing(None, C.byref(ms), C.byref(p1), C.byref(n))
+    if rc != WN_OK:
+        raise WNError(rc, last_error())
+    return ms.value, p1.value, n.value
+
+
 def segment_prep(ctrl_uv, ctrl_w, seg_degree, device=None, stream=None):
     """K1 alone: [n_segs, 10] = (B, S0, Bq[8]) per segment (no margins)."""
     torch = _torch()

@@ -1195,8 +1195,12 @@ struct DevBuf {
 
 void free_handle(wn_faces_t F) {
   if (!F) return;
-  for (auto &pr : F->k3_events) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
-  for (auto &e : F->k3_mid) cudaEventDestroy(e);
+  if (!F->k3_events.empty()) {   // unread timing survives the handle (wn_get_timing(NULL, ...))
+    std::vector<K3Timing> ev;
+    for (size_t i = 0; i < F->k3_events.size(); ++i)
+      ev.push_back({F->k3_events[i].first, F->k3_mid[i], F->k3_events[i].second});
+    orphan_timing(std::move(ev));
+  }
   // stream-ordered frees on the legacy stream, after the handle's last use
   // (its build or its latest query, on whatever stream that ran)
   if (F->last_use) cudaStreamWaitEvent(0, F->last_use, 0);

@@ -207,6 +207,10 @@ struct wn_faces_s {
 };
 
 namespace wn {
+// K3 timing events (begin, after phase 1, end) of handles freed before their
+// timing was read: wn_get_timing(NULL, ...) reads them
+struct K3Timing { cudaEvent_t e0, em, e1; };
+void orphan_timing(std::vector<K3Timing> &&ev);
 void ensure_pool(int dev);
 cudaError_t cache_alloc(void **out, size_t bytes, cudaStream_t st);
 void cache_free(void *p, cudaStream_t st);

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "wn_common.cuh"
 
@@ -1018,25 +1019,42 @@ extern "C" wn_status_t wn_set_timing(wn_faces_t F, int enable) {
   return WN_OK;
 }
 
+namespace wn {
+static std::mutex g_orphan_mu;
+static std::vector<K3Timing> g_orphan;
+void orphan_timing(std::vector<K3Timing> &&ev) {
+  std::lock_guard<std::mutex> lk(g_orphan_mu);
+  for (auto &x : ev) g_orphan.push_back(x);
+}
+}  // namespace wn
+
 extern "C" wn_status_t wn_get_timing(wn_faces_t F, double *ms, double *phase1_ms, int64_t *launches) {
-  if (!F || !ms || !launches) { wn::set_error("wn_get_timing: NULL"); return WN_ERR_ARG; }
+  if (!ms || !launches) { wn::set_error("wn_get_timing: NULL"); return WN_ERR_ARG; }
+  std::vector<wn::K3Timing> ev;
+  if (F) {
+    for (size_t i = 0; i < F->k3_events.size(); ++i) ev.push_back({F->k3_events[i].first, F->k3_mid[i], F->k3_events[i].second});
+    F->k3_events.clear();
+    F->k3_mid.clear();
+  } else {
+    std::lock_guard<std::mutex> lk(wn::g_orphan_mu);
+    ev.swap(wn::g_orphan);
+  }
   double tot = 0.0, p1 = 0.0;
-  for (size_t i = 0; i < F->k3_events.size(); ++i) {
-    auto &pr = F->k3_events[i];
-    WN_CUDA(cudaEventSynchronize(pr.second));
+  wn_status_t rc = WN_OK;
+  for (auto &x : ev) {
     float t = 0.f, tm = 0.f;
-    WN_CUDA(cudaEventElapsedTime(&t, pr.first, pr.second));
-    WN_CUDA(cudaEventElapsedTime(&tm, pr.first, F->k3_mid[i]));
+    cudaError_t e = cudaEventSynchronize(x.e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, x.e0, x.e1);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&tm, x.e0, x.em);
+    if (e != cudaSuccess && rc == WN_OK) rc = wn::cuda_fail(e, "wn_get_timing");
     tot += t;
     p1 += tm;
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
-    cudaEventDestroy(F->k3_mid[i]);
+    cudaEventDestroy(x.e0);
+    cudaEventDestroy(x.em);
+    cudaEventDestroy(x.e1);
   }
   *ms = tot;
   if (phase1_ms) *phase1_ms = p1;
-  *launches = (int64_t)F->k3_events.size();
-  F->k3_events.clear();
-  F->k3_mid.clear();
-  return WN_OK;
+  *launches = (int64_t)ev.size();
+  return rc;
 }

@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
   const int s0 = loop_off[l], s1 = loop_off[l + 1];
   const int r_first = G.rec_off + cull + 1;              // first record after GROUP? and MOVE
   const bool tree = (G.flags & PF_TREE) != 0;
+  const bool omit_root = tree && (G.flags & PF_OMIT_ROOT) != 0;
   __shared__ double2 s_end[EMIT_WARPS][EMIT_STAGE];      // translated lifted end points
   __shared__ double s_pre[EMIT_WARPS][EMIT_STAGE];       // S0 prefix sums
   const int wib = (threadIdx.x >> 5);
@@ -673,8 +674,15 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
         if (s == s0) put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVE | fa);
         else put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVEG | fa);
       }
+      bool omit = omit_root && ch.y >= 2;                // closed loop: no root SPAN
       while (a < bnd) {
         const int mid = (a + bnd) >> 1;
+        if (omit) {                                      // root level without its record
+          omit = false;
+          if (j <= mid) bnd = mid;
+          else { off += 2 * (mid - a + 1) - 1; a = mid + 1; }
+          continue;
+        }
         if (j == a) {
           // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
           const int se = s0 + ch.x + bnd;                // last segment of the run
@@ -740,7 +748,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
     }
   }
   if (lane == 0) {
-    int r = tree ? G.rec_off + cull + 2 * (s1 - s0) : r_first + (s1 - s0) + carry;
+    int r = tree ? G.rec_off + cull + 2 * (s1 - s0) - (omit_root && s1 - s0 >= 2 ? 1 : 0)
+                 : r_first + (s1 - s0) + carry;
     if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
     if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
     if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
@@ -831,8 +840,10 @@ struct FaceCtx {
 // hot records of one planned group (must match k_emit's layout)
 __host__ __device__ inline int group_nrec(int kind, int flags, const LoopInfo &I) {
   if (kind == G_LINE) return 1;
-  // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg
-  return ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) +
+  // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg,
+  // minus the omitted root SPAN of a closed single-chain loop
+  return ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) -
+         ((flags & PF_OMIT_ROOT) && I.nseg >= 2 ? 1 : 0) +
          ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
 }
 
@@ -846,6 +857,10 @@ __host__ __device__ inline int loop_flags(const LoopInfo &I, bool angle, bool co
     const bool closed = I.closed && I.nbrk == 0;
     if (closed) fl |= PF_CULL;
     else if (!angle) fl |= PF_TAIL_CLOSEG;
+    // a closed loop is one chain whose ends coincide: the root SPAN's ellipse is
+    // the circle of radius sum(S0)/2 around its start -- it (almost) never
+    // prunes, so the tree starts at the root's two children
+    if (closed && tree) fl |= PF_OMIT_ROOT;
   }
   return fl;
 }

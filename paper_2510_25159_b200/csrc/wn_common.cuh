@@ -97,7 +97,8 @@ struct HardEntry {
 
 // build-plan group (host -> device), 32 B
 enum : int32_t { G_LOOP = 0, G_COPY = 1, G_LINE = 2 };
-enum : int32_t { PF_CULL = 1, PF_ANGLE = 2, PF_TAIL_CLOSEG = 4, PF_TAIL_XCH = 8, PF_TAIL_NCH = 16, PF_TREE = 32 };
+enum : int32_t { PF_CULL = 1, PF_ANGLE = 2, PF_TAIL_CLOSEG = 4, PF_TAIL_XCH = 8, PF_TAIL_NCH = 16, PF_TREE = 32,
+                 PF_OMIT_ROOT = 64 };   // closed single-chain loop: no root SPAN (its foci coincide)
 struct PlanGroup {
   int32_t kind, flags;
   int32_t loop;

@@ -314,7 +314,8 @@ constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushe
 #ifndef WN_P1_MINB
 #define WN_P1_MINB 4
 #endif
-template <typename R, bool COUNT>
+// ANGLE: the build's angle_mode (every record of a handle carries the same F_ANGLE)
+template <typename R, bool COUNT, bool ANGLE>
 __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
   constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
@@ -463,9 +464,9 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             const bool descend = act && !pr;
             if (!__any_sync(0xffffffffu, descend)) {
               // every active lane substitutes the run's chord (homotopy)
-              if (__any_sync(0xffffffffu, act && (u1 != up || (meta & F_ANGLE)))) {
+              if (__any_sync(0xffffffffu, act && (u1 != up || ANGLE))) {
                 if (act) {
-                  if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                  if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
                   else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
                 }
               }
@@ -474,13 +475,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
               if (COUNT && lane == 0) ++c_cull;
             } else if (act && pr) {
               // this lane prunes the run: chord now, inactive for the subtree
-              if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+              if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
               else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
               zx = h.x; zy = h.y; cdf = df; up = u1;
               skip_end = gr + 1 + (int)(meta >> 8);
             }
           } else {
-            const bool need = act && (!pr || u1 != up || (meta & F_ANGLE));
+            const bool need = act && (!pr || u1 != up || ANGLE);
             if (__any_sync(0xffffffffu, need)) {
               bool hard = false;
               if (need) {
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                   }
                 }
                 if (cdf + df > h.fs && !onb) {                   // pruned: chord (a5)
-                  if (meta & F_ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                  if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
                   else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
                 } else {
                   hard = !onb;                                   // exact recursion in phase 2
@@ -508,7 +509,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                   H.px = px;
                   H.py = py;
                   H.q = qi;
-                  H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | ((meta & F_ANGLE) ? 0x80000000u : 0u);
+                  H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | (ANGLE ? 0x80000000u : 0u);
                   s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
                   pend |= 1 | 4;
                   if (COUNT) ++c_hard;
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           else nd = sqrtf((float)(nx * nx + ny * ny));
           if (act) {
             if (!(nd > eps_c)) onb |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
-            if (kind == K_MOVEG && !(meta & F_ANGLE)) {
+            if (kind == K_MOVEG && !ANGLE) {
               // gap chord Z -> A': -omega(p,Z,A') + its crossing
               const double ax = zx - px, ay = zy - py;
               const double cr = canon_cross(ax, ay, nx, ny);
@@ -948,15 +949,18 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
     WN_CUDA(cudaEventRecord(e0, st));
   }
   const int hb = 148 * 8;
+  const bool ang = F->opt.angle_mode == 1;
   if (F->counters_on) {
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
-    k_phase1<R, true><<<max_tiles, NTH, 0, st>>>(P);
+    if (ang) k_phase1<R, true, true><<<max_tiles, NTH, 0, st>>>(P);
+    else k_phase1<R, true, false><<<max_tiles, NTH, 0, st>>>(P);
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
     k_finish<<<148 * 8, 256, 0, st>>>(n, winding, flag, P.rule, F->counters);
   } else {
-    k_phase1<R, false><<<max_tiles, NTH, 0, st>>>(P);
+    if (ang) k_phase1<R, false, true><<<max_tiles, NTH, 0, st>>>(P);
+    else k_phase1<R, false, false><<<max_tiles, NTH, 0, st>>>(P);
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);

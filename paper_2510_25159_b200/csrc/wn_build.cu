@@ -201,20 +201,13 @@ __device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const dou
   }
 }
 
-// K1 output, structure of arrays over SORTED positions p (coalesced writes):
-// B[p], S0[p], Bq[q * n + p]; inv[s] = p maps a segment to its position.
-struct PrepSoA {
-  double *B, *S0, *Bq;
-  int32_t *inv;
-  int32_t n;
-};
-
-// One thread per segment (at sorted position p): loads its control points
-// once and computes B, S0 and the 8 piece bounds (the degree sort makes the
-// warp run one degree variant).
+// One thread per segment (taken in degree-sorted order so that a warp runs one
+// degree variant): loads its control points once and computes B, S0 and the 8
+// piece bounds, written as one 80-B record prep[s] (five 16-B stores), which
+// k_emit then reads coalesced in segment order.
 template <int N>
-__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o, int p,
-                                       const PrepSoA &out, uint8_t *__restrict__ err_out) {
+__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o,
+                                       SegPrep *__restrict__ out, uint8_t *__restrict__ err_out) {
   double X[N + 1], Y[N + 1], W[N + 1], px[N + 1], py[N + 1];
   bool err = false;
   double lpoly = 0.0;
@@ -226,55 +219,47 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     px[j] = x; py[j] = y;
     if (j) lpoly += hypot(x - px[j - 1], y - py[j - 1]);
   }
-  err_out[p] = err ? 1 : 0;
+  *err_out = err ? 1 : 0;
+  double2 *o2 = reinterpret_cast<double2 *>(out);
   if (err) {
-    out.B[p] = out.S0[p] = 0.0;
-    for (int q = 0; q < 8; ++q) out.Bq[(int64_t)q * out.n + p] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o2[k] = make_double2(0.0, 0.0);
     return;
   }
   const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
-  out.B[p] = B;
-  out.S0[p] = fmin(B, lpoly);
+  o2[0] = make_double2(B, fmin(B, lpoly));
 #pragma unroll 1
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < 8; q += 2) {
     double a[N + 1], bb[N + 1], c[N + 1];
     dyadic_piece<N>(X, Y, W, q, a, bb, c);
-    out.Bq[(int64_t)q * out.n + p] = 8.0 * hodo_bound<N>(a, bb, c);
+    const double b0 = 8.0 * hodo_bound<N>(a, bb, c);
+    dyadic_piece<N>(X, Y, W, q + 1, a, bb, c);
+    const double b1 = 8.0 * hodo_bound<N>(a, bb, c);
+    o2[1 + q / 2] = make_double2(b0, b1);
   }
 }
 
 __global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
                                               const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                                              const double *__restrict__ w, PrepSoA out,
+                                              const double *__restrict__ w, SegPrep *__restrict__ prep,
                                               uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n_segs) return;
   const int s = order ? order[p] : p;   // degree-sorted: warp-uniform N
-  out.inv[s] = p;
   const int o = coff[s];
   const int n = deg[s];
   switch (n) {
-    case 1: prep_n<1>(ctrl, w, o, p, out, serr); break;
-    case 2: prep_n<2>(ctrl, w, o, p, out, serr); break;
-    case 3: prep_n<3>(ctrl, w, o, p, out, serr); break;
-    case 4: prep_n<4>(ctrl, w, o, p, out, serr); break;
-    case 5: prep_n<5>(ctrl, w, o, p, out, serr); break;
-    default:   // rejected on the host (k_deg flag); never read past the arrays
-      serr[p] = 1;
-      out.B[p] = out.S0[p] = 0.0;
-      for (int q = 0; q < 8; ++q) out.Bq[(int64_t)q * out.n + p] = 0.0;
+    case 1: prep_n<1>(ctrl, w, o, prep + s, serr + s); break;
+    case 2: prep_n<2>(ctrl, w, o, prep + s, serr + s); break;
+    case 3: prep_n<3>(ctrl, w, o, prep + s, serr + s); break;
+    case 4: prep_n<4>(ctrl, w, o, prep + s, serr + s); break;
+    case 5: prep_n<5>(ctrl, w, o, prep + s, serr + s); break;
+    default: {   // rejected on the host (k_deg flag); never read past the arrays
+      serr[s] = 1;
+      double2 *o2 = reinterpret_cast<double2 *>(prep + s);
+      for (int k = 0; k < 5; ++k) o2[k] = make_double2(0.0, 0.0);
+    }
   }
-}
-
-// the public AoS layout of wn_segment_prep: out[s] = {B, S0, Bq[8]} (identity order)
-__global__ void k_prep_aos(int32_t n_segs, PrepSoA in, SegPrep *__restrict__ out) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_segs) return;
-  SegPrep r;
-  r.B = in.B[s];
-  r.S0 = in.S0[s];
-  for (int q = 0; q < 8; ++q) r.Bq[q] = in.Bq[(int64_t)q * in.n + s];
-  out[s] = r;
 }
 
 __global__ void k_iota(int32_t n, int32_t *__restrict__ a) {
@@ -463,7 +448,7 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
 // the path-hierarchy spans are differences of them.  Summation
 // order differs from a serial sum by a few ulps, far inside the R5 margin.
 __global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, const int32_t *__restrict__ loop_off,
-                                               PrepSoA prep, double *__restrict__ s0pre) {
+                                               const SegPrep *__restrict__ prep, double *__restrict__ s0pre) {
   const int l = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (l >= n_loops) return;
@@ -471,7 +456,7 @@ __global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, 
   double carry = 0.0;
   for (int base = s0; base < s1; base += 32) {
     const int s = base + lane;
-    double v = s < s1 ? prep.S0[prep.inv[s]] : 0.0;
+    double v = s < s1 ? prep[s].S0 : 0.0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double u = __shfl_up_sync(0xffffffffu, v, o);
@@ -575,7 +560,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
                        const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                       const double *__restrict__ wts, PrepSoA prep,
+                       const double *__restrict__ wts, const SegPrep *__restrict__ prep,
                        const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const double2 *__restrict__ lend,
@@ -705,8 +690,9 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
       }
       r = off;
     }
-    const int pp = prep.inv[s];
-    const double bpB = prep.B[pp], bpS0 = prep.S0[pp];
+    const double2 *pr2 = reinterpret_cast<const double2 *>(prep + s);
+    const double2 bs = pr2[0];                            // (B, S0)
+    const double bpB = bs.x, bpS0 = bs.y;
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // and the filter's (1 - 2^-18) error shrink folded in as a further
@@ -723,8 +709,9 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
     *reinterpret_cast<int2 *>(&Cp->n) = make_int2(n, 0);
 #pragma unroll
     for (int q = 0; q < 8; q += 2) {
-      const double b0 = (dbg_flags & 1 ? bpB : fmin(bpB, prep.Bq[(int64_t)q * prep.n + pp])) * (1.0 + rel);
-      const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, prep.Bq[(int64_t)(q + 1) * prep.n + pp])) * (1.0 + rel);
+      const double2 bq = pr2[1 + q / 2];
+      const double b0 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.x)) * (1.0 + rel);
+      const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.y)) * (1.0 + rel);
       st2<R>(&Cp->Bq[q], (sizeof(R) == 4) ? (R)f_up(b0) : (R)b0, (sizeof(R) == 4) ? (R)f_up(b1) : (R)b1);
     }
     R cxv[6], cyv[6], cwv[6];
@@ -1235,7 +1222,7 @@ struct BuildCtx {
   const uint8_t *per;
   const double *dom;
   int32_t *coff, *loop_face;
-  PrepSoA prep;
+  SegPrep *prep;
   int2 *shift;
   uint8_t *brk;
   int2 *chain;      // per segment: (chain start index within its loop, chain length)
@@ -1415,11 +1402,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   tr.mark("csr copies + degree scan (async)");
   // --- K1 prep, loop->face, K2a lift ---
   uint8_t *d_serr = nullptr;
-  B.prep.n = n_segs;
-  WN_CUDA(D.alloc(&B.prep.B, n_segs));
-  WN_CUDA(D.alloc(&B.prep.S0, n_segs));
-  WN_CUDA(D.alloc(&B.prep.Bq, 8 * (size_t)n_segs));
-  WN_CUDA(D.alloc(&B.prep.inv, n_segs));
+  WN_CUDA(D.alloc(&B.prep, n_segs));
   WN_CUDA(D.alloc(&d_serr, n_segs));
   WN_CUDA(D.alloc(&B.loop_face, n_loops));
   WN_CUDA(D.alloc(&B.shift, n_segs));
@@ -1808,14 +1791,12 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
   WN_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
   if (h_bad) { set_error("wn_segment_prep: segment degree outside 1..5"); return WN_ERR_ARG; }
-  PrepSoA soa;
-  soa.n = n_segs;
-  WN_CUDA(D.alloc(&soa.B, n_segs));
-  WN_CUDA(D.alloc(&soa.S0, n_segs));
-  WN_CUDA(D.alloc(&soa.Bq, 8 * (size_t)n_segs));
-  WN_CUDA(D.alloc(&soa.inv, n_segs));
-  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, soa, serr, nullptr);
-  k_prep_aos<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, soa, (SegPrep *)out);
+  // k_prep writes 16-B vectors: stage through an aligned buffer if needed
+  SegPrep *dst = (SegPrep *)out;
+  if ((uintptr_t)out & 15) WN_CUDA(D.alloc(&dst, n_segs));
+  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, dst, serr, nullptr);
+  if ((void *)dst != (void *)out)
+    WN_CUDA(cudaMemcpyAsync(out, dst, sizeof(SegPrep) * (size_t)n_segs, cudaMemcpyDeviceToDevice, st));
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaStreamSynchronize(st));
   return WN_OK;

@@ -318,13 +318,11 @@ def main():
         d2h = nq * 9
 
         def e2e_step():
+            # geometry to the device, build, then the streamed host query
+            # (wn_query_host: chunked copies in / kernels / copies out overlap)
             g = [t.to(dev, non_blocking=True) for t in h_geo]
-            f = h_fid.to(dev, non_blocking=True)
-            q = h_uv.to(dev, non_blocking=True)
             fc = wn.Faces.build(*g, **kw)
-            r = fc.query(f, q)
-            h_w.copy_(r.winding, non_blocking=True)
-            h_f.copy_(r.flag, non_blocking=True)
+            fc.query_host(h_fid, h_uv, out=(h_w, h_f), sync=False)
             torch.cuda.current_stream(dev).synchronize()
             fc.close()
 

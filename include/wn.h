@@ -110,6 +110,17 @@ wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, con
 wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face_id, const double *uv,
                      double *winding, uint8_t *flag, void *stream);
 
+/* Streamed batched query from HOST buffers (pinned for overlap; pageable works
+ * synchronously): the batch is cut into chunks of `chunk` queries (<= 0: auto)
+ * that are copied in on an internal copy stream, queried with wn_query on
+ * `stream`, and copied back on a second copy stream, three chunks deep, so
+ * host<->device transfers in both directions overlap the kernels.  Arguments
+ * as for wn_query, but h_* are host pointers owned by the caller that must stay
+ * valid until `stream` is synchronised; the results are in h_winding / h_flag
+ * once it is.  Same per-query semantics as wn_query. */
+wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t *h_face_id, const double *h_uv,
+                          double *h_winding, uint8_t *h_flag, int64_t chunk, void *stream);
+
 typedef struct {
   int64_t n_records;     /* hot records (MOVE/SEG/GROUP/LINE/...) over all faces */
   int64_t n_seg_records; /* SEG records (input segments x emitted lattice copies) */

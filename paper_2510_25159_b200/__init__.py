@@ -29,7 +29,7 @@ STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4
 FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
-           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory"]
+           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "warp_skips", "on_boundary", "span_tests", "warp_records", "_r10", "_r11"]
 
@@ -70,6 +70,8 @@ def load():
                                      C.POINTER(Options), vp, C.POINTER(vp), vp]
         L.wn_query.restype = C.c_int
         L.wn_query.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp]
+        L.wn_query_host.restype = C.c_int
+        L.wn_query_host.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]
         L.wn_faces_info.restype = C.c_int
         L.wn_faces_info.argtypes = [vp, C.POINTER(FacesInfo)]
         L.wn_set_counters.restype = C.c_int
@@ -197,6 +199,40 @@ class Faces:
                                  _stream(stream, self.device))
         if rc != WN_OK:
             raise WNError(rc, last_error())
+        return QueryResult(wnd, flg)
+
+    def query_host(self, face_id, uv, out=None, chunk=0, stream=None, sync=True):
+        """Streamed query of HOST arrays (wn_query_host): chunks are copied in,
+        queried and copied back on overlapping streams.  face_id / uv: CPU
+        tensors or numpy arrays (pinned CPU tensors give the overlap); returns
+        (winding float64 [n], flag uint8 [n]) as CPU tensors, valid after the
+        stream is synchronised (sync=True waits)."""
+        torch = _torch()
+
+        def cpu(x, dt):
+            t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+            if t.is_cuda:
+                raise WNError(1, "query_host takes host arrays")
+            return t.to(dt).contiguous()
+
+        fid = cpu(face_id, torch.int32)
+        q = cpu(uv, torch.float64).reshape(-1, 2)
+        n = fid.numel()
+        if out is None:
+            pin = fid.is_pinned()
+            wnd = torch.empty(n, dtype=torch.float64, pin_memory=pin)
+            flg = torch.empty(n, dtype=torch.uint8, pin_memory=pin)
+        else:
+            wnd, flg = out
+        s = _stream(stream, self.device)
+        with torch.cuda.device(self.device):
+            rc = load().wn_query_host(self._h, n, C.c_void_p(fid.data_ptr()), C.c_void_p(q.data_ptr()),
+                                      C.c_void_p(wnd.data_ptr()), C.c_void_p(flg.data_ptr()), int(chunk), s)
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        if sync:
+            torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+        self._keep = (fid, q)   # inputs must outlive the asynchronous copies
         return QueryResult(wnd, flg)
 
     def query_raw(self, n, face_id_ptr, uv_ptr, winding_ptr, flag_ptr, stream_handle):

@@ -1017,6 +1017,84 @@ extern "C" wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face
 
 extern "C" int32_t wn_last_query_launches(void) { return wn::g_launches; }
 
+// Streamed query from HOST buffers: chunks of the batch go host->device on a
+// copy-in stream, through wn_query on `stream`, and back on a copy-out stream,
+// three chunk slots deep, so the PCIe transfers in both directions overlap the
+// kernels of the neighbouring chunks.  Face-sorted input stays face-sorted per
+// chunk (K4 then skips its scatter).
+extern "C" wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t *h_face_id, const double *h_uv,
+                                     double *h_winding, uint8_t *h_flag, int64_t chunk, void *stream) {
+  using namespace wn;
+  if (!faces) { set_error("wn_query_host: NULL handle"); return WN_ERR_ARG; }
+  if (n < 0) { set_error("wn_query_host: n < 0"); return WN_ERR_ARG; }
+  if (n == 0) { g_launches = 0; return WN_OK; }
+  if (!h_face_id || !h_uv || !h_winding || !h_flag) { set_error("wn_query_host: NULL array"); return WN_ERR_ARG; }
+  const int dev = faces->device;
+  WN_CUDA(cudaSetDevice(dev));
+  ensure_pool(dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  constexpr int NS = 3;
+  static std::mutex mu;
+  static cudaStream_t s_in[64] = {}, s_out[64] = {};
+  static cudaEvent_t ev_in[64][NS], ev_q[64][NS], ev_out[64][NS];
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 0 || dev >= 64) { set_error("device index out of range"); return WN_ERR_ARG; }
+  if (!s_in[dev]) {
+    WN_CUDA(cudaStreamCreateWithFlags(&s_in[dev], cudaStreamNonBlocking));
+    WN_CUDA(cudaStreamCreateWithFlags(&s_out[dev], cudaStreamNonBlocking));
+    for (int i = 0; i < NS; ++i) {
+      WN_CUDA(cudaEventCreateWithFlags(&ev_in[dev][i], cudaEventDisableTiming));
+      WN_CUDA(cudaEventCreateWithFlags(&ev_q[dev][i], cudaEventDisableTiming));
+      WN_CUDA(cudaEventCreateWithFlags(&ev_out[dev][i], cudaEventDisableTiming));
+    }
+  }
+  if (chunk <= 0) chunk = std::min<int64_t>(std::max<int64_t>(n / 8, (int64_t)1 << 20), (int64_t)1 << 24);
+  chunk = std::min(chunk, n);
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const int nslots = (int)std::min<int64_t>(NS, nchunks);
+  // device slots, allocated in the copy-in stream's order (their first use)
+  int32_t *d_f[NS] = {};
+  double *d_uv[NS] = {}, *d_w[NS] = {};
+  uint8_t *d_fl[NS] = {};
+  // the copy-in stream must not start before the caller's prior work on `stream`
+  WN_CUDA(cudaEventRecord(ev_q[dev][0], st));
+  WN_CUDA(cudaStreamWaitEvent(s_in[dev], ev_q[dev][0], 0));
+  for (int i = 0; i < nslots; ++i) {
+    WN_CUDA(cache_alloc((void **)&d_f[i], sizeof(int32_t) * chunk, s_in[dev]));
+    WN_CUDA(cache_alloc((void **)&d_uv[i], sizeof(double) * 2 * chunk, s_in[dev]));
+    WN_CUDA(cache_alloc((void **)&d_w[i], sizeof(double) * chunk, s_in[dev]));
+    WN_CUDA(cache_alloc((void **)&d_fl[i], chunk, s_in[dev]));
+  }
+  int launches = 0;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int k = (int)(c % NS);
+    const int64_t a = c * chunk, cn = std::min(chunk, n - a);
+    if (c >= NS) WN_CUDA(cudaStreamWaitEvent(s_in[dev], ev_out[dev][k], 0));   // slot drained
+    WN_CUDA(cudaMemcpyAsync(d_f[k], h_face_id + a, sizeof(int32_t) * cn, cudaMemcpyHostToDevice, s_in[dev]));
+    WN_CUDA(cudaMemcpyAsync(d_uv[k], h_uv + 2 * a, sizeof(double) * 2 * cn, cudaMemcpyHostToDevice, s_in[dev]));
+    WN_CUDA(cudaEventRecord(ev_in[dev][k], s_in[dev]));
+    WN_CUDA(cudaStreamWaitEvent(st, ev_in[dev][k], 0));
+    wn_status_t rc = wn_query(faces, cn, d_f[k], d_uv[k], d_w[k], d_fl[k], st);
+    if (rc != WN_OK) return rc;
+    launches += g_launches;
+    WN_CUDA(cudaEventRecord(ev_q[dev][k], st));
+    WN_CUDA(cudaStreamWaitEvent(s_out[dev], ev_q[dev][k], 0));
+    WN_CUDA(cudaMemcpyAsync(h_winding + a, d_w[k], sizeof(double) * cn, cudaMemcpyDeviceToHost, s_out[dev]));
+    WN_CUDA(cudaMemcpyAsync(h_flag + a, d_fl[k], cn, cudaMemcpyDeviceToHost, s_out[dev]));
+    WN_CUDA(cudaEventRecord(ev_out[dev][k], s_out[dev]));
+  }
+  // `stream` completes only after every result reached the host
+  for (int i = 0; i < nslots; ++i) WN_CUDA(cudaStreamWaitEvent(st, ev_out[dev][i], 0));
+  for (int i = 0; i < nslots; ++i) {
+    cache_free(d_f[i], st);
+    cache_free(d_uv[i], st);
+    cache_free(d_w[i], st);
+    cache_free(d_fl[i], st);
+  }
+  g_launches = launches;
+  return WN_OK;
+}
+
 extern "C" wn_status_t wn_set_timing(wn_faces_t F, int enable) {
   if (!F) { wn::set_error("wn_set_timing: NULL"); return WN_ERR_ARG; }
   F->timing_on = enable ? 1 : 0;

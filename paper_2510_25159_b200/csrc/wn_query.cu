@@ -602,19 +602,111 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
 // ---------------------------------------------------------------------------
 template <typename R, bool COUNT>
 __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
+  // Each lane runs Alg. 1 on its pairs i, i + stride, ... as a state machine
+  // that advances ONE recursion node per loop iteration and starts its next
+  // pair as soon as the current one ends, so a warp waits for its slowest lane
+  // once (at the end) instead of once per pair (the recursion depth is data
+  // dependent).  Same decisions and arithmetic as hard_pair().
   const int total = min(*P.hq_count, P.hq_cap);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const HardEntry H = P.hq[i];
-    const bool angle = H.c >> 31;
-    const Cold<R> *C = P.cold + (H.c & 0x7fffffffu);
-    const HardResult r = hard_pair<R, COUNT>(C, (R)H.px, (R)H.py, angle, (R)P.eps, P.max_depth, P.counters);
-    double *w = P.winding + H.q;
-    if (r.ob) {
-      atomicExch(reinterpret_cast<unsigned long long *>(w), 0x7ff8000000000000ULL);
-    } else {
-      const double add = (double)r.xsum + r.fsum * (1.0 / TWO_PI);
-      if (add != 0.0) atomicAdd(w, add);
+  const int stride = gridDim.x * blockDim.x;
+  const R eps = (R)P.eps;
+  const int max_depth = P.max_depth;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  R stx[MAXD + 1], sty[MAXD + 1];
+  int8_t std_[MAXD + 1];
+  const Cold<R> *C = nullptr;
+  R qx = 0, qy = 0, M = 0, Lx = 0, Ly = 0, dL = 0;
+  int n = 0, sp = 0, xsum = 0, q = 0;
+  double ta = 0.0, fsum = 0.0;
+  bool live = false, root = false, angle = false;
+  unsigned long long nodes = 0, evals = 0, leaves = 0;
+  int dmax = 0;
+  while (true) {
+    if (!live) {
+      if (i >= total) break;
+      const HardEntry H = P.hq[i];
+      angle = H.c >> 31;
+      C = P.cold + (H.c & 0x7fffffffu);
+      qx = (R)H.px;
+      qy = (R)H.py;
+      q = H.q;
+      M = __ldg(&C->M);
+      n = __ldg(&C->n);
+      Lx = __ldg(&C->f0x) - qx;
+      Ly = __ldg(&C->f0y) - qy;
+      dL = dsqrt(Lx * Lx + Ly * Ly);
+      stx[0] = __ldg(&C->f1x) - qx;
+      sty[0] = __ldg(&C->f1y) - qy;
+      std_[0] = 0;
+      sp = 1;
+      ta = 0.0;
+      xsum = 0;
+      fsum = 0.0;
+      root = true;
+      live = true;
     }
+    // one node [ta, ta + 2^-d] with right end point (rx, ry), top of the stack
+    const R rx = stx[sp - 1], ry = sty[sp - 1];
+    const int d = std_[sp - 1];
+    const R dR = dsqrt(rx * rx + ry * ry);
+    bool split, ob;
+    ++nodes;
+    if (root) {
+      root = false;
+      ob = dL < eps || dR < eps;                            // Alg. 1 line 1 on the root
+      split = true;
+    } else {
+      ob = dR < eps;                                        // Alg. 1 line 1
+      // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
+      const int q0 = (int)(ta * 8.0);
+      R Bn = __ldg(&C->Bq[q0]);
+      if (d < 3) {
+        const int nq = 8 >> d;
+        for (int k = 1; k < nq; ++k) Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+      }
+      const R span = ldexp(Bn, -d) + M;
+      split = !(dL + dR > span);                            // Alg. 1 line 3
+    }
+    bool done = ob;
+    if (!ob && split && d >= max_depth) { ob = true; done = true; }   // depth cap (R6)
+    if (!done) {
+      if (!split) {                                         // chord substitution
+        if (angle) fsum += (double)chord_angle(Lx, Ly, rx, ry);
+        else xsum += xcount(Lx, Ly, rx, ry);
+        ++leaves;
+        Lx = rx; Ly = ry; dL = dR;
+        ta += ldexp(1.0, -d);
+        done = --sp == 0;
+      } else {
+        const double tm = ta + ldexp(1.0, -(d + 1));       // m = (a+b)/2
+        R mx, my;
+        eval_point(C, n, (R)tm, mx, my);
+        ++evals;
+        std_[sp - 1] = (int8_t)(d + 1);
+        stx[sp] = mx - qx;
+        sty[sp] = my - qy;
+        std_[sp] = (int8_t)(d + 1);
+        ++sp;
+        dmax = max(dmax, d + 1);
+      }
+    }
+    if (done) {
+      double *w = P.winding + q;
+      if (ob) {
+        atomicExch(reinterpret_cast<unsigned long long *>(w), 0x7ff8000000000000ULL);
+      } else {
+        const double add = (double)xsum + fsum * (1.0 / TWO_PI);
+        if (add != 0.0) atomicAdd(w, add);
+      }
+      live = false;
+      i += stride;
+    }
+  }
+  if (COUNT) {
+    cnt_add<COUNT>(P.counters, 2, nodes);
+    cnt_add<COUNT>(P.counters, 3, evals);
+    cnt_add<COUNT>(P.counters, 4, leaves);
+    atomicMax(P.counters + 5, (unsigned long long)dmax);
   }
 }
 

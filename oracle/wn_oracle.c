@@ -29,11 +29,12 @@
  *       finite N: sum_{k=-N..N} omega(p, gamma + k v) + omega(p,L)
  *       - omega(p, beta_{-N}, beta_{N+1}), omega(p,L) = +-1/2 by the left/right
  *       test (on L counts as left, R11);
- *     - bi-periodic (classes +-(1,0) / +-(0,1)): contractible loops summed over
- *       a lattice window; each proper pair (alpha, beta-bar) by Eq. 8
- *        summed over every band offset s in a window, each term an
- *       Eq. 5 extended winding; pairing by the paper's ToLeft / PairLoop /
- *       PairLoops (Algs. 7-9) over a transverse window (R16).
+ *     - bi-periodic (any coprime class (p,q), Prop. 2): contractible
+ *       loops summed over a lattice window; each proper pair (alpha, beta-bar)
+ *       by Eq. 8 summed over every band (r,s) -- indexed by the
+ *       integer m = p*s - q*r -- in a window, each term an Eq. 5 extended
+ *       winding; pairing by the paper's ToLeft / PairLoop / PairLoops (Algs.
+ *       7-9) over a transverse window (R16).
  *   Classification: nonzero rule (R10): inside iff |round_half_away(w)| >= 1;
  *   "positive" rule optional.
  *   Distance certificate: dist_lb(p) = min over terminal pieces of the distance
@@ -306,17 +307,23 @@ static double line_wn(double px, double py, double bx, double by, double vx, dou
 
 /* Eq. 5 literally for the periodically extended curve of loop l
  * translated by (tx,ty), extension vector v = (vx,vy):
- *   sum_{k=-N..N} omega(p, g_k) + omega(p,L) - omega(p, beta_{-N}, beta_{N+1}),
- * g_k = g + k v, beta_k = g(0) + k v.  Translation applied to p (App. C.1). */
+ *   sum_{k=kc-N..kc+N} omega(p, g_k) + omega(p,L) - omega(p, beta_{kc-N}, beta_{kc+N+1}),
+ * g_k = g + k v, beta_k = g(0) + k v.  Translation applied to p (App. C.1).
+ * The truncation window is centred on p's position along v (kc), so that the
+ * copies which can wind around p are inside it whatever lattice representative
+ * (tx,ty) of the extended curve is passed (Eq. 5 holds for any window that
+ * contains them; the omitted copy-minus-chord loops do not enclose p). */
 static void ext_wn(const model_t *M, int l, double tx, double ty, double vx, double vy,
                    double px, double py, double delta, acc_t *A) {
   int N = M->N5;
   int64_t o = M->ctrl_off[M->loop_off[l]];
   double b0x = M->P[2 * o] + tx, b0y = M->P[2 * o + 1] + ty;
-  for (int k = -N; k <= N; k++)
+  int kc = (int)round(((px - b0x) * vx + (py - b0y) * vy) / (vx * vx + vy * vy));
+  for (int k = kc - N; k <= kc + N; k++)
     loop_wn(M, l, px - tx - k * vx, py - ty - k * vy, delta, A);
   nadd(A, line_wn(px, py, b0x, b0y, vx, vy));
-  nadd(A, -orc_chord(px, py, b0x - N * vx, b0y - N * vy, b0x + (N + 1) * vx, b0y + (N + 1) * vy));
+  nadd(A, -orc_chord(px, py, b0x + (kc - N) * vx, b0y + (kc - N) * vy, b0x + (kc + N + 1) * vx,
+                     b0y + (kc + N + 1) * vy));
 }
 
 static int gcd_i(int a, int b) { a = abs(a); b = abs(b); while (b) { int t = a % b; a = b; b = t; } return a; }
@@ -335,12 +342,49 @@ static int to_left(const model_t *M, int l1, double t1x, double t1y, int l2, dou
   return acc_val(&A) > 0.0;
 }
 
+/* Band index of a bi-periodic face with non-contractible class (cp,cq)
+ * (Prop. 2): nu(x) = cp*y/Tv - cq*x/Tu.  A lattice translate
+ * (i Tu, j Tv) shifts nu by m = cp*j - cq*i, an integer; translates with the
+ * same m differ by multiples of the extension vector v = (cp Tu, cq Tv) and
+ * give the same extended curve, so the extended curves gamma_{r,s} of Eq. (8)
+ * are indexed by m (gcd(cp,cq) = 1 makes every integer occur exactly once,
+ * r in [0,|p|), s in Z).  rep_m returns one translate (i,j) with shift m. */
+static double band_nu(int cp, int cq, const double *D, double x, double y) {
+  return (double)cp * y / D[3] - (double)cq * x / D[1];
+}
+static void band_rep(int cp, int cq, int m, int *i, int *j) {
+  /* extended Euclid: cp*y0 - cq*x0 = 1 */
+  int r0 = cp, r1 = -cq, s0 = 1, s1 = 0, t0 = 0, t1 = 1;   /* s*cp + t*(-cq) = r */
+  while (r1 != 0) {
+    int qq = r0 / r1, tmp;
+    tmp = r0 - qq * r1; r0 = r1; r1 = tmp;
+    tmp = s0 - qq * s1; s0 = s1; s1 = tmp;
+    tmp = t0 - qq * t1; t0 = t1; t1 = tmp;
+  }
+  if (r0 < 0) { s0 = -s0; t0 = -t0; }                     /* r0 = gcd = 1 */
+  *j = m * s0; *i = m * t0;                                /* cp*j - cq*i = m */
+}
+/* nu-range of a loop's control-point box shifted by (i,j) tiles */
+static void box_nu(const model_t *M, int l, int cp, int cq, const double *D, int i, int j,
+                   double *lo, double *hi) {
+  const double *bb = M->bbox + 4 * l;
+  *lo = INFINITY; *hi = -INFINITY;
+  for (int c = 0; c < 4; c++) {
+    double x = bb[(c & 1) ? 2 : 0] + i * D[1], y = bb[(c & 2) ? 3 : 1] + j * D[3];
+    double nu = band_nu(cp, cq, D, x, y);
+    *lo = fmin(*lo, nu); *hi = fmax(*hi, nu);
+  }
+}
+
 /* Validation (Props. 1, B.1, B.3 as input checks) and
- * pairing (Algs. 8-9, R16: transverse search window derived from extents).
- * Error codes: 1 = |class|>1 on a uni-periodic axis (B.1), 2 = unbalanced
- * A/B (Prop. 1), 3 = mixed / non-coprime classes (B.3 / B.4), 4 = class
- * (p,q) with p,q both nonzero (general bands: not supported), 5 = pairing
- * failure. */
+ * pairing (Algs. 8-9, R16: search over the beta-translates modulo the
+ * extension vector, i.e. over the band index m, in a window derived from the
+ * loops' extents).  Error codes: 1 = |class|>1 on a uni-periodic axis (B.1),
+ * 2 = unbalanced A/B (Prop. 1), 3 = mixed / non-coprime classes (B.3 / B.4),
+ * 5 = pairing failure.  General classes (p,q), p,q != 0 (Prop. 2, Dataset B
+ * P:804) are paired like the axis classes: the candidate translate of band m
+ * is moved along v next to alpha (any representative gives the same extended
+ * curve; a nearby one keeps the ToLeft probe inside Eq. 5's window). */
 static void validate_and_pair(model_t *M) {
   for (int f = 0; f < M->n_faces; f++) {
     M->face_err[f] = 0;
@@ -363,36 +407,44 @@ static void validate_and_pair(model_t *M) {
     if (M->face_err[f]) continue;
     if (nA != nB) { M->face_err[f] = 2; continue; }
     if (!(pu && pv) || nA == 0) continue;
-    if (cp != 0 && cq != 0) { M->face_err[f] = 4; continue; }
-    /* bi-periodic pairing.  Extension of A loops: v = (cp*Tu, cq*Tv); the
-     * transverse lattice direction e is e2 for class (+-1,0), e1 for (0,+-1). */
+    /* bi-periodic pairing.  Extension of A loops: v = (cp*Tu, cq*Tv). */
     double vAx = cp * D[1], vAy = cq * D[3];
-    double ex = (cq != 0) ? D[1] : 0.0, ey = (cq != 0) ? 0.0 : D[3];
+    int general = (cp != 0 && cq != 0);
     int *used = (int *)calloc((size_t)(l1 - l0), sizeof(int));
     for (int la = l0; la < l1; la++) {
       if (!(M->cls[2 * la] == cp && M->cls[2 * la + 1] == cq)) continue;
-      int best = -1, bests = 0;
+      int best = -1, bi = 0, bj = 0;
+      int64_t oa = M->ctrl_off[M->loop_off[la]];
+      double sax = M->P[2 * oa], say = M->P[2 * oa + 1];
+      double alo, ahi;
+      box_nu(M, la, cp, cq, D, 0, 0, &alo, &ahi);
       for (int lb = l0; lb < l1; lb++) {
         if (used[lb - l0] || !(M->cls[2 * lb] == -cp && M->cls[2 * lb + 1] == -cq)) continue;
-        /* window: translates whose transverse extent lies within 3 periods */
-        double ext = (ey != 0.0) ? (M->bbox[4 * lb + 3] - M->bbox[4 * lb + 1]) / D[3]
-                                 : (M->bbox[4 * lb + 2] - M->bbox[4 * lb]) / D[1];
-        double da = (ey != 0.0) ? (M->bbox[4 * la + 1] - M->bbox[4 * lb + 1]) / D[3]
-                                : (M->bbox[4 * la] - M->bbox[4 * lb]) / D[1];
-        int J = 3 + (int)ceil(ext + fabs(da));
-        for (int s = -J; s <= J; s++) {
-          double tx = s * ex, ty = s * ey;
+        /* window: translates whose transverse (nu) extent lies within 3 bands */
+        double blo, bhi;
+        box_nu(M, lb, cp, cq, D, 0, 0, &blo, &bhi);
+        int J = 3 + (int)ceil((bhi - blo) + fabs(alo - blo));
+        int64_t ob = M->ctrl_off[M->loop_off[lb]];
+        for (int m = -J; m <= J; m++) {
+          int i, j;
+          band_rep(cp, cq, m, &i, &j);
+          if (general) {   /* representative next to alpha along v */
+            double dx = sax - (M->P[2 * ob] + i * D[1]), dy = say - (M->P[2 * ob + 1] + j * D[3]);
+            int k = (int)round((dx * vAx + dy * vAy) / (vAx * vAx + vAy * vAy));
+            i += k * cp; j += k * cq;
+          }
+          double tx = i * D[1], ty = j * D[3];
           if (!to_left(M, lb, tx, ty, la, 0.0, 0.0, vAx, vAy)) continue;
-          if (best < 0 || to_left(M, lb, tx, ty, best, bests * ex, bests * ey, -vAx, -vAy)) {
-            best = lb; bests = s;
+          if (best < 0 || to_left(M, lb, tx, ty, best, bi * D[1], bj * D[3], -vAx, -vAy)) {
+            best = lb; bi = i; bj = j;
           }
         }
       }
       if (best < 0) { M->face_err[f] = 5; break; }
       used[best - l0] = 1;
       M->pair_beta[la] = best;
-      M->pair_shift[2 * la] = (ex != 0.0) ? bests : 0;
-      M->pair_shift[2 * la + 1] = (ey != 0.0) ? bests : 0;
+      M->pair_shift[2 * la] = bi;
+      M->pair_shift[2 * la + 1] = bj;
     }
     free(used);
   }
@@ -420,20 +472,23 @@ static void face_wn(const model_t *M, int f, double px, double py, double delta,
     }
     double vx = a * D[1], vy = b * D[3];
     if (!(pu && pv)) { ext_wn(M, l, 0.0, 0.0, vx, vy, px, py, delta, A); continue; }
-    /* bi-periodic: only alpha loops (class == face class A) drive Eq. 8 */
+    /* bi-periodic: only alpha loops (class == face class A) drive Eq. 8
+     * (P:583-590): sum over the bands m (the (r,s) of Eq. 8) of the extended
+     * windings of alpha + rep(m) and of the proper beta-bar + rep(m), over
+     * every band whose nu-extent lies within 3 bands of p. */
     if (M->pair_beta[l] < 0) continue;
     int lb = M->pair_beta[l];
-    double ex = (b != 0) ? D[1] : 0.0, ey = (b != 0) ? 0.0 : D[3];
-    double sbx = M->pair_shift[2 * l] * D[1], sby = M->pair_shift[2 * l + 1] * D[3];
-    const double *ba = M->bbox + 4 * l, *bbb = M->bbox + 4 * lb;
-    double c = (ey != 0.0) ? py : px;
-    double lo = (ey != 0.0) ? fmin(ba[1], bbb[1] + sby) : fmin(ba[0], bbb[0] + sbx);
-    double hi = (ey != 0.0) ? fmax(ba[3], bbb[3] + sby) : fmax(ba[2], bbb[2] + sbx);
-    double Tt = (ey != 0.0) ? D[3] : D[1];
-    int slo = (int)floor((c - hi) / Tt) - 3, shi = (int)ceil((c - lo) / Tt) + 3;
-    for (int s = slo; s <= shi; s++) {
-      ext_wn(M, l, s * ex, s * ey, vx, vy, px, py, delta, A);
-      ext_wn(M, lb, sbx + s * ex, sby + s * ey, -vx, -vy, px, py, delta, A);
+    int si = M->pair_shift[2 * l], sj = M->pair_shift[2 * l + 1];
+    double lo1, hi1, lo2, hi2;
+    box_nu(M, l, a, b, D, 0, 0, &lo1, &hi1);
+    box_nu(M, lb, a, b, D, si, sj, &lo2, &hi2);
+    double lo = fmin(lo1, lo2), hi = fmax(hi1, hi2), c = band_nu(a, b, D, px, py);
+    int mlo = (int)floor(c - hi) - 3, mhi = (int)ceil(c - lo) + 3;
+    for (int m = mlo; m <= mhi; m++) {
+      int i, j;
+      band_rep(a, b, m, &i, &j);
+      ext_wn(M, l, i * D[1], j * D[3], vx, vy, px, py, delta, A);
+      ext_wn(M, lb, (si + i) * D[1], (sj + j) * D[3], -vx, -vy, px, py, delta, A);
     }
   }
 }

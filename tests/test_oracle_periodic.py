@@ -163,3 +163,101 @@ def test_c3_torus_closed_form():
             assert abs(r["w"][i] - total) < 1e-12, (p, r["w"][i], total)
             n_ok += 1
     assert n_ok > 550
+
+
+def _ext_gcd_rep(p, q, m):
+    """A lattice translate (i, j) with p*j - q*i = m (brute force over a small box)."""
+    for i in range(-abs(p) - 1, abs(p) + 2):
+        for j in range(-abs(q) - 1, abs(q) + 2):
+            if p * j - q * i == 1:
+                return m * i, m * j
+    raise RuntimeError
+
+
+def _band_f(segs, tau, a0, v, nu0):
+    """nu-offset of a band loop (a graph over tau: tau is monotone along every
+    Hermite segment) at band-coordinate tau, by bisection on the Bernstein form."""
+    vv = float(v @ v)
+    for P, w in segs:
+        ta_, tb_ = ((P[[0, -1]] - a0) @ v) / vv
+        lo, hi = min(ta_, tb_), max(ta_, tb_)
+        if lo <= tau <= hi:
+            a, b = 0.0, 1.0
+            inc = tb_ > ta_
+            for _ in range(70):
+                tm = 0.5 * (a + b)
+                x = H.bern_eval(P, w, tm)[0]
+                if (((x - a0) @ v) / vv < tau) == inc:
+                    a = tm
+                else:
+                    b = tm
+            x = H.bern_eval(P, w, 0.5 * (a + b))[0]
+            return nu0(x)
+    raise RuntimeError(tau)
+
+
+@pytest.mark.parametrize("pq,T", [((2, 1), None), ((3, 2), None), ((1, -2), None), ((2, 3), (2 * math.pi, math.pi))])
+def test_c3pq_general_class_closed_form(pq, T):
+    """General bi-periodic class (p,q) (Prop. 2, Eq. 8):
+    the face interior is the band between alpha and the proper translate of
+    beta, modulo the lattice, minus two CW holes plus one CCW island.  Band
+    membership in band coordinates (tau along v, nu across), by bisection on
+    the loops as graphs over tau -- independent of the oracle's Eq. 5/8 sums."""
+    p, q = pq
+    kw = {} if T is None else dict(Tu=T[0], Tv=T[1])
+    wl = G.gen_c3pq(p=p, q=q, n_queries=250, **kw)
+    meta = wl["meta"]
+    Tu, Tv, v, a0 = meta["Tu"], meta["Tv"], meta["v"], meta["a0"]
+    s = float(np.linalg.norm(meta["w"]))
+    nu = lambda x: p * x[1] / Tv - q * x[0] / Tu
+    nu0 = lambda x: nu(x) - nu(a0)
+    vv = float(v @ v)
+    r = oracle.query(wl)
+    n_ok = 0
+    for k, x in enumerate(wl["uv"]):
+        tx = float((x - a0) @ v) / vv
+        nx = nu0(x)
+        inband, marg = False, 1e9
+        for m in range(int(math.floor(nx)) - 2, int(math.floor(nx)) + 3):
+            i, j = _ext_gcd_rep(p, q, m)
+            dt = (i * Tu * v[0] + j * Tv * v[1]) / vv
+            t = tx - dt
+            fa = _band_f(meta["alpha"], t - math.floor(t), a0, v, nu0)
+            tb0 = ((meta["beta"][-1][0][-1] - a0) @ v) / vv      # beta's tau range [tb0, tb0 + 1]
+            tt = t - math.floor(t - tb0)
+            fb = _band_f(meta["beta"], tt, a0, v, nu0)
+            if fa + m < nx < fb + m:
+                inband = True
+            marg = min(marg, abs(nx - fa - m) * s, abs(nx - fb - m) * s)
+        total = 1 if inband else 0
+        for c, rad, orient in meta["circles"]:
+            i0, j0 = round((x[0] - c[0]) / Tu), round((x[1] - c[1]) / Tv)
+            d = min(math.hypot(x[0] - c[0] - i_ * Tu, x[1] - c[1] - j_ * Tv)
+                    for i_ in (i0 - 1, i0, i0 + 1) for j_ in (j0 - 1, j0, j0 + 1))
+            marg = min(marg, abs(d - rad))
+            if d < rad:
+                total += orient
+        if marg > 1e-7 and r["comparable"][k]:
+            assert abs(r["w"][k] - total) < 1e-12, (x, r["w"][k], total)
+            n_ok += 1
+    assert n_ok > 230
+
+
+@pytest.mark.parametrize("pq", [(2, 1), (-3, 2)])
+def test_c3pq_tile_periodicity_and_pairing_invariance(pq):
+    """omega(p) = omega(p + Tu e1) = omega(p + Tv e2) (unreduced), and the
+    value does not depend on which lattice translate beta is stored at."""
+    wl = G.gen_c3pq(p=pq[0], q=pq[1], n_queries=120)
+    wl2 = G.gen_c3pq(p=pq[0], q=pq[1], n_queries=120, beta_shift=(3, -2))
+    Tu, Tv = wl["meta"]["Tu"], wl["meta"]["Tv"]
+    q = wl["uv"]
+    r1 = oracle.query(wl)
+    r2 = oracle.query(wl, uv=q + [Tu, 0.0], reduce=False)
+    r3 = oracle.query(wl, uv=q + [0.0, -Tv], reduce=False)
+    r4 = oracle.query(wl2)
+    ok = r1["comparable"] & r2["comparable"] & r3["comparable"] & r4["comparable"]
+    assert ok.mean() > 0.95
+    for rr in (r2, r3, r4):
+        assert np.max(np.abs(r1["w"][ok] - rr["w"][ok])) < 1e-9
+    assert np.max(np.abs(r1["w"][ok] - np.round(r1["w"][ok]))) < 1e-12
+    assert set(np.round(r1["w"][ok]).astype(int)) <= {-1, 0, 1}

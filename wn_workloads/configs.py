@@ -349,6 +349,89 @@ def gen_c3(seed=3, n_queries=1_000_000):
 
 
 # ----------------------------------------------------------------------------
+# C3pq — bi-periodic torus with a general coprime class (p,q) (SURVEY 8(f)
+# NEXT-2; the paper's Dataset B has 2 <= p,q <= 5).  Not one of the five
+# BASELINE configs: a parity case for the general band path.
+# ----------------------------------------------------------------------------
+
+def _band_frame(p, q, Tu, Tv):
+    """Extension vector v = (p Tu, q Tv), the transverse vector w (w perpendicular
+    to v, band coordinate nu(w) = 1 with nu(x) = p*y/Tv - q*x/Tu) -- input
+    construction only."""
+    v = np.array([p * Tu, q * Tv])
+    L = math.hypot(v[0], v[1])
+    w = np.array([-v[1], v[0]]) / L * (Tu * Tv / L)
+    return v, w
+
+
+def _hermite_band_loop(a0, v, w, f, fp, tau0, direction, n_seg):
+    """x(tau) = a0 + tau v + f(tau) w over one period of tau (direction +1: tau0 ->
+    tau0+1, class (p,q); -1: class -(p,q)), as cubic Hermite segments with
+    Q40-quantised control points; the end is the start + direction*v exactly."""
+    taus = tau0 + direction * np.arange(n_seg + 1) / n_seg
+    X = lambda t: a0 + t * v + f(t) * w
+    dX = lambda t: v + fp(t) * w
+    K = [quant(X(t)) for t in taus]
+    K[-1] = K[0] + direction * v                     # exact closure (Q40 arithmetic)
+    segs = []
+    for k in range(n_seg):
+        h = taus[k + 1] - taus[k]
+        P0, P3 = K[k], K[k + 1]
+        P1 = quant(P0 + (h / 3.0) * dX(taus[k]))
+        P2 = quant(P3 - (h / 3.0) * dX(taus[k + 1]))
+        segs.append((np.stack([P0, P1, P2, P3]), np.ones(4)))
+    return segs
+
+
+def gen_c3pq(seed=6, p=2, q=1, n_queries=100_000, Tu=None, Tv=None, n_seg=None, beta_shift=(0, 1)):
+    """Bi-periodic face whose separation loops alpha / beta have classes (p,q) /
+    -(p,q): alpha at band coordinate nu = 0.2 + 0.05 sin(2 pi (2 tau) + phi_a),
+    beta at nu = 0.6 + 0.05 sin(...) (the band between them is the interior),
+    two CW hole circles inside the band (nu = 0.4) and one CCW island outside it
+    (nu = 0.9).  beta is stored shifted by `beta_shift` tiles before wrapping so
+    that pairing must find its proper translate.  All loops stored
+    seam-discontinuous (R18); queries uniform in the fundamental domain."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    Tu = TWO_PI_Q if Tu is None else float(quant(Tu))
+    Tv = TWO_PI_Q if Tv is None else float(quant(Tv))
+    assert math.gcd(abs(p), abs(q)) == 1
+    if n_seg is None:
+        n_seg = 12 * max(abs(p), abs(q), 1)
+    v, w = _band_frame(p, q, Tu, Tv)
+    s = float(np.linalg.norm(w))                     # distance per unit nu
+    a0 = quant(rng.uniform(0, 1, size=2) * [Tu, Tv])
+    ph_a, ph_b = rng.uniform(0, 2 * math.pi, size=2)
+    A = 0.05
+    fa = lambda t: 0.2 + A * np.sin(4 * math.pi * t + ph_a)
+    fpa = lambda t: 4 * math.pi * A * math.cos(4 * math.pi * t + ph_a)
+    fb = lambda t: 0.6 + A * np.sin(4 * math.pi * t + ph_b)
+    fpb = lambda t: 4 * math.pi * A * math.cos(4 * math.pi * t + ph_b)
+    tb = float(rng.uniform(0, 1))
+    alpha = _hermite_band_loop(a0, v, w, fa, fpa, 0.0, +1, n_seg)
+    beta = _hermite_band_loop(a0, v, w, fb, fpb, tb, -1, n_seg)
+    shift = np.array([beta_shift[0] * Tu, beta_shift[1] * Tv])
+    beta_stored = [(P + shift, wt) for P, wt in beta]
+    r = float(quant(0.075 * s))
+    circles = []
+    for tau_c, nu_c, orient in ((0.3, 0.4, -1), (0.75, 0.4, -1), (0.5, 0.9, +1)):
+        c = quant(a0 + tau_c * v + nu_c * w)
+        circles.append((c, r, orient))
+    b = _Builder()
+    loops = [alpha, beta_stored] + [[(quant(P), wt) for P, wt in _circle_arcs(c, r, ccw=(o > 0))]
+                                     for c, r, o in circles]
+    for segs in loops:
+        for P, wt in segs:
+            b.seg(_wrap_store(P, Tu, Tv, True, True), wt)
+        b.end_loop()
+    b.end_face(periodic=3, domain=(0.0, Tu, 0.0, Tv))
+    uv = rng.uniform(0.0, 1.0, size=(n_queries, 2)) * [Tu, Tv]
+    uv = np.minimum(uv, np.nextafter(np.array([Tu, Tv]), 0.0))
+    meta = dict(kind="C3pq", p=p, q=q, Tu=Tu, Tv=Tv, a0=a0, v=v, w=w, alpha=alpha, beta=beta,
+                circles=[(tuple(c), r, o) for c, r, o in circles])
+    return _finish(b, np.zeros(n_queries), uv, False, "C3pq(%d,%d)" % (p, q), meta)
+
+
+# ----------------------------------------------------------------------------
 # C4 — robustness set: gapped / open cubic loops (BASELINE configs[3])
 # ----------------------------------------------------------------------------
 

@@ -46,7 +46,7 @@ enum {
   WN_FACE_B1 = 1,          /* |class| > 1 on a uni-periodic axis (Prop. B.1) */
   WN_FACE_UNBALANCED = 2,  /* #A != #B: loops not null-homologous (Prop. 1) */
   WN_FACE_CLASS = 3,       /* mixed classes or gcd(|p|,|q|) != 1 (Props. B.3/B.4) */
-  WN_FACE_GENERAL_PQ = 4,  /* bi-periodic class (p,q) with p,q both nonzero: not implemented yet */
+  WN_FACE_GENERAL_PQ = 4,  /* (unused: general bi-periodic classes (p,q), Prop. 2, are supported) */
   WN_FACE_PAIRING = 5,     /* PairLoops (Alg. 9) found no proper translate */
   WN_FACE_GEOM = 6         /* bad degree / weight / non-finite data in this face */
 };

@@ -585,6 +585,10 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
     // omega(p, L) for the line through beta_0 along the extension vector (Eq. 5)
     if (lane == 0) {
       const double bx = TX(I.sx), by = TY(I.sy);
+      if (I.cu != 0 && I.cv != 0) {                                    // general class: slanted line
+        put_rec<R>(hot, G.rec_off, bx, by, 0.0, sline_meta(I.cu, I.cv));
+        return;
+      }
       uint32_t meta = K_LINE;
       double c;
       if (I.cu != 0) { c = by; if (I.cu > 0) meta |= F_GE; }          // v = (+-T,0): left iff p.v >=/<= c
@@ -891,6 +895,93 @@ __host__ __device__ void plan_extended_copies(S &P, int l, const LoopInfo &I, co
   }
 }
 
+// ---- general bi-periodic classes (p,q), p,q != 0 (Prop. 2; Eq. 8) ----
+// Band coordinate nu(x) = p*y/Tv - q*x/Tu: the lattice translate (i Tu, j Tv)
+// shifts it by m = p*j - q*i, and translates with equal m differ by multiples
+// of the extension vector v = (p Tu, q Tv), i.e. give the same extended curve.
+// So the extended curves gamma_{r,s} of Eq. (8) are indexed by the integer m
+// (gcd = 1: every m occurs once over r in [0,|p|), s in Z).
+__host__ __device__ inline double band_nu(int p, int q, const FaceCtx &C, double x, double y) {
+  return (double)p * y / C.Tv - (double)q * x / C.Tu;
+}
+// one translate (i, j) with p*j - q*i = m
+__host__ __device__ inline void band_rep(int p, int q, int m, int &i, int &j) {
+  int x0 = 0, y0 = 0;
+  if (p == 0) {
+    x0 = -q;                                    // q = +-1
+  } else {
+    const int ap = p < 0 ? -p : p;
+    for (int x = 0; x < ap; ++x)
+      if ((1 + q * x) % p == 0) { x0 = x; y0 = (1 + q * x) / p; break; }
+  }
+  i = m * x0;
+  j = m * y0;
+}
+__host__ __device__ inline void box_nu(const double *bb, int p, int q, const FaceCtx &C, int i, int j, double &lo,
+                                       double &hi) {
+  lo = INFINITY; hi = -INFINITY;
+  for (int c = 0; c < 4; ++c) {
+    const double nu = band_nu(p, q, C, bb[(c & 1) ? 2 : 0] + i * C.Tu, bb[(c & 2) ? 3 : 1] + j * C.Tv);
+    lo = fmin(lo, nu); hi = fmax(hi, nu);
+  }
+}
+__host__ __device__ inline int floor_div(int a, int b) { int d = a / b; return (a % b != 0 && ((a < 0) != (b < 0))) ? d - 1 : d; }
+__host__ __device__ inline int ceil_div(int a, int b) { return -floor_div(-a, b); }
+// k with lo <= t + k d <= hi, intersected into [klo, khi]
+__host__ __device__ inline void k_restrict(int t, int d, int lo, int hi, int &klo, int &khi) {
+  if (d > 0) { klo = max(klo, ceil_div(lo - t, d)); khi = min(khi, floor_div(hi - t, d)); }
+  else if (d < 0) { klo = max(klo, ceil_div(hi - t, d)); khi = min(khi, floor_div(lo - t, d)); }
+  else if (t < lo || t > hi) khi = klo - 1;
+}
+// copies (loop + (ti + k p, tj + k q) tiles) of one extended curve whose box meets the tile
+template <class S>
+__host__ __device__ void plan_band_copies(S &P, int l, const LoopInfo &I, const FaceCtx &C, int p, int q, int ti,
+                                          int tj, bool tree) {
+  const int fl = loop_flags(I, C.angle, true, tree);
+  const double m = tile_margin(C);
+  int a0, a1, b0, b1;
+  k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, a0, a1);   // u-translates meeting the tile
+  k_range(I.bb[1], I.bb[3], C.v0, C.Tv, m, b0, b1);   // v-translates meeting the tile
+  if (a0 > a1 || b0 > b1) return;
+  int klo = -(1 << 29), khi = 1 << 29;
+  k_restrict(ti, p, a0, a1, klo, khi);
+  k_restrict(tj, q, b0, b1, klo, khi);
+  for (int k = klo; k <= khi; ++k) P.add(G_COPY, fl, l, ti + k * p, tj + k * q, I, C.M);
+}
+// Eq. 8 for a general pair (alpha, beta-bar = beta + rep(mb)): every band m
+// whose strip or copies can meet the base tile
+template <class S>
+__host__ __device__ void plan_general_pair(S &P, int l, const LoopInfo &I, int lb, const LoopInfo &Ib, int mb,
+                                           const FaceCtx &C, bool tree) {
+  const int p = I.cu, q = I.cv;
+  int bi, bj;
+  band_rep(p, q, mb, bi, bj);
+  double alo, ahi, blo, bhi;
+  box_nu(I.bb, p, q, C, 0, 0, alo, ahi);
+  box_nu(Ib.bb, p, q, C, bi, bj, blo, bhi);
+  const double na = band_nu(p, q, C, I.sx, I.sy), nb = band_nu(p, q, C, Ib.sx + bi * C.Tu, Ib.sy + bj * C.Tv);
+  const double lo = fmin(fmin(alo, blo), fmin(na, nb)), hi = fmax(fmax(ahi, bhi), fmax(na, nb));
+  const double mt = tile_margin(C);
+  double tlo = INFINITY, thi = -INFINITY;
+  for (int c = 0; c < 4; ++c) {
+    const double nu = band_nu(p, q, C, (c & 1) ? C.u0 + C.Tu + mt : C.u0 - mt, (c & 2) ? C.v0 + C.Tv + mt : C.v0 - mt);
+    tlo = fmin(tlo, nu); thi = fmax(thi, nu);
+  }
+  const double sl = 1e-6;                       // slack: extra bands only cost records
+  const int m0 = (int)floor(tlo - hi - sl) - 1, m1 = (int)ceil(thi - lo + sl) + 1;
+  for (int m = m0; m <= m1; ++m) {
+    int i, j;
+    band_rep(p, q, m, i, j);
+    // omega(p, L_alpha) + omega(p, L_beta) cancel unless the strip meets the tile
+    if (fmin(na, nb) + m <= thi + sl && fmax(na, nb) + m >= tlo - sl) {
+      P.add(G_LINE, 0, l, i, j, I, C.M);
+      P.add(G_LINE, 0, lb, bi + i, bj + j, Ib, C.M);
+    }
+    plan_band_copies(P, l, I, C, p, q, i, j, tree);
+    plan_band_copies(P, lb, Ib, C, p, q, bi + i, bj + j, tree);
+  }
+}
+
 // the groups of one (validated, paired) face
 template <class S>
 __host__ __device__ void plan_face(S &P, const LoopInfo *L, int l0, int l1, const FaceCtx &C,
@@ -914,6 +1005,10 @@ __host__ __device__ void plan_face(S &P, const LoopInfo *L, int l0, int l1, cons
     const int lb = pair_beta[l];
     const int sb = pair_s[l];
     const LoopInfo &Ib = L[lb];
+    if (I.cu != 0 && I.cv != 0) {
+      plan_general_pair(P, l, I, lb, Ib, sb, C, tree);
+      continue;
+    }
     const int tax = axis == 0 ? 1 : 0;
     const double Tt = tax ? C.Tv : C.Tu, t0 = tax ? C.v0 : C.u0;
     const double m = tile_margin(C);
@@ -977,10 +1072,7 @@ __host__ __device__ inline int face_validate(const LoopInfo *L, int l0, int l1, 
   }
   if (st) return st;
   if (nA != nB && (strict || C.per == 3)) return WN_FACE_UNBALANCED;
-  if (C.per == 3 && nA > 0) {
-    if (cp != 0 && cq != 0) return WN_FACE_GENERAL_PQ;
-    *needp = 1;
-  }
+  if (C.per == 3 && nA > 0) *needp = 1;
   return WN_FACE_OK;
 }
 
@@ -1563,10 +1655,76 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       face_validate(L, h_flo[f], h_flo[f + 1], ctx[f], O.strict != 0, &np);
       if (np) need_pair.push_back(f);
     }
-    struct Cand { int face, alpha, beta, s; double px, py; };
+    // Candidates (R16): the beta-translates modulo alpha's extension vector,
+    // indexed by the band offset s (axis classes: the transverse lattice
+    // index; general classes (p,q): m = p*j - q*i, with the translate moved
+    // along v next to alpha so the probe stays near the emitted copies).
+    struct Cand { int face, alpha, beta, s, ti, tj; double px, py; };
     std::vector<int> pair_beta(n_loops, -1), pair_s(n_loops, 0);
-    // virtual faces: one uni-periodic extended curve per non-contractible loop
+    std::vector<Cand> cands;
+    auto face_class = [&](int f, int &cp, int &cq) {
+      cp = cq = 0;
+      for (int l = h_flo[f]; l < h_flo[f + 1]; ++l)
+        if (L[l].nseg && (L[l].cu || L[l].cv)) { cp = L[l].cu; cq = L[l].cv; break; }
+    };
+    for (int f : need_pair) {
+      const FaceCtx &C = ctx[f];
+      int cp, cq;
+      face_class(f, cp, cq);
+      const bool general = cp != 0 && cq != 0;
+      const int tax = (cp != 0) ? 1 : 0;                // transverse axis (axis classes)
+      const double Tt = tax ? C.Tv : C.Tu;
+      const double vx = cp * C.Tu, vy = cq * C.Tv;
+      for (int la = h_flo[f]; la < h_flo[f + 1]; ++la) {
+        if (!(L[la].nseg && L[la].cu == cp && L[la].cv == cq)) continue;
+        for (int lb = h_flo[f]; lb < h_flo[f + 1]; ++lb) {
+          if (!(L[lb].nseg && L[lb].cu == -cp && L[lb].cv == -cq)) continue;
+          int J;
+          if (general) {
+            double alo, ahi, blo, bhi;
+            box_nu(L[la].bb, cp, cq, C, 0, 0, alo, ahi);
+            box_nu(L[lb].bb, cp, cq, C, 0, 0, blo, bhi);
+            J = 3 + (int)std::ceil((bhi - blo) + std::fabs(alo - blo));
+          } else {
+            const double ext = tax ? (L[lb].bb[3] - L[lb].bb[1]) / Tt : (L[lb].bb[2] - L[lb].bb[0]) / Tt;
+            const double da = tax ? (L[la].bb[1] - L[lb].bb[1]) / Tt : (L[la].bb[0] - L[lb].bb[0]) / Tt;
+            J = 3 + (int)std::ceil(ext + std::fabs(da));
+          }
+          for (int sidx = -J; sidx <= J; ++sidx) {
+            int ti = tax ? 0 : sidx, tj = tax ? sidx : 0;
+            if (general) {
+              band_rep(cp, cq, sidx, ti, tj);
+              const double dx = L[la].sx - (L[lb].sx + ti * C.Tu), dy = L[la].sy - (L[lb].sy + tj * C.Tv);
+              const int k = (int)std::lround((dx * vx + dy * vy) / (vx * vx + vy * vy));
+              ti += k * cp;
+              tj += k * cq;
+            }
+            cands.push_back({f, la, lb, sidx, ti, tj, L[lb].sx + ti * C.Tu, L[lb].sy + tj * C.Tv});
+          }
+        }
+      }
+    }
+    // virtual faces: one extended curve per non-contractible loop.  Axis
+    // classes: a uni-periodic face along the class axis (queries reduced along
+    // it).  General classes: a face without reduction (per = 4) holding the
+    // slanted line and every copy that can contain a probe point.
     std::vector<int> vface(n_loops, -1);
+    std::vector<double> tmin(n_loops, INFINITY), tmax(n_loops, -INFINITY);
+    auto cover = [&](int l, double x, double y, const FaceCtx &C) {
+      const double vx = L[l].cu * C.Tu, vy = L[l].cv * C.Tv;
+      const double t = ((x - L[l].sx) * vx + (y - L[l].sy) * vy) / (vx * vx + vy * vy);
+      tmin[l] = std::min(tmin[l], t);
+      tmax[l] = std::max(tmax[l], t);
+    };
+    for (size_t i = 0; i < cands.size(); ++i) {
+      const Cand &a = cands[i];
+      const FaceCtx &C = ctx[a.face];
+      if (!(L[a.alpha].cu && L[a.alpha].cv)) continue;
+      cover(a.alpha, a.px, a.py, C);                    // batch 1: omega(pt(beta~), alpha_ext)
+      for (size_t j = 0; j < cands.size(); ++j)         // batch 2 (any later left pair)
+        if (j != i && cands[j].alpha == a.alpha)
+          cover(cands[j].beta, a.px - cands[j].ti * C.Tu, a.py - cands[j].tj * C.Tv, C);
+    }
     Plan VP;
     std::vector<uint8_t> vper;
     std::vector<double> vdom, vM;
@@ -1575,50 +1733,36 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
         const LoopInfo &I = L[l];
         if (I.nseg == 0 || (I.cu == 0 && I.cv == 0)) continue;
         FaceCtx C = ctx[f];
-        const int axis = (I.cu != 0) ? 0 : 1;
-        C.per = axis == 0 ? 1 : 2;
         C.angle = false;
+        const bool general = I.cu != 0 && I.cv != 0;
+        const int axis = (I.cu != 0) ? 0 : 1;
         vface[l] = (int)vper.size();
-        vper.push_back(C.per);
+        vper.push_back(general ? 4 : (axis == 0 ? 1 : 2));
         vdom.insert(vdom.end(), {ctx[f].u0, ctx[f].Tu, ctx[f].v0, ctx[f].Tv});
         vM.push_back(C.M);
         VP.begin_face(vface[l]);
         VP.add(G_LINE, 0, l, 0, 0, I, C.M);
-        plan_extended_copies(VP, l, I, C, axis, 0, false, O.hierarchy != 0);
-      }
-    }
-    VP.end();
-    // candidates: beta translates along the transverse axis (R16 window)
-    std::vector<Cand> cands;
-    struct QueryRec { int vf; double x, y; };
-    std::vector<QueryRec> qs;
-    for (int f : need_pair) {
-      const FaceCtx &C = ctx[f];
-      int cp = 0, cq = 0;
-      for (int l = h_flo[f]; l < h_flo[f + 1]; ++l)
-        if (L[l].nseg && (L[l].cu || L[l].cv)) { cp = L[l].cu; cq = L[l].cv; break; }
-      const int tax = (cp != 0) ? 1 : 0;                // transverse axis
-      const double Tt = tax ? C.Tv : C.Tu;
-      for (int la = h_flo[f]; la < h_flo[f + 1]; ++la) {
-        if (!(L[la].nseg && L[la].cu == cp && L[la].cv == cq)) continue;
-        for (int lb = h_flo[f]; lb < h_flo[f + 1]; ++lb) {
-          if (!(L[lb].nseg && L[lb].cu == -cp && L[lb].cv == -cq)) continue;
-          const double ext = tax ? (L[lb].bb[3] - L[lb].bb[1]) / Tt : (L[lb].bb[2] - L[lb].bb[0]) / Tt;
-          const double da = tax ? (L[la].bb[1] - L[lb].bb[1]) / Tt : (L[la].bb[0] - L[lb].bb[0]) / Tt;
-          const int J = 3 + (int)std::ceil(ext + std::fabs(da));
-          for (int s = -J; s <= J; ++s) {
-            Cand c{f, la, lb, s, L[lb].sx + (tax ? 0.0 : s * Tt), L[lb].sy + (tax ? s * Tt : 0.0)};
-            cands.push_back(c);
-            qs.push_back({vface[la], c.px, c.py});
-          }
+        if (!general) {
+          C.per = axis == 0 ? 1 : 2;
+          plan_extended_copies(VP, l, I, C, axis, 0, false, O.hierarchy != 0);
+        } else if (tmin[l] <= tmax[l]) {
+          const double vx = I.cu * C.Tu, vy = I.cv * C.Tv;
+          const double E = 2.0 * std::hypot(I.bb[2] - I.bb[0], I.bb[3] - I.bb[1]) / std::hypot(vx, vy) + 1.0;
+          const int k0 = (int)std::floor(tmin[l] - E) - 1, k1 = (int)std::ceil(tmax[l] + E) + 1;
+          const int fl = loop_flags(I, false, true, O.hierarchy != 0);
+          for (int k = k0; k <= k1; ++k) VP.add(G_COPY, fl, l, k * I.cu, k * I.cv, I, C.M);
         }
       }
     }
+    VP.end();
+    struct QueryRec { int vf; double x, y; };
+    std::vector<QueryRec> qs;
+    for (const Cand &c : cands) qs.push_back({vface[c.alpha], c.px, c.py});
     // run probes through the query kernel on a temporary handle (fp64, crossing mode)
     WN_CUDA(cudaStreamSynchronize(st));   // K1 outputs (bounds, span prefixes) are read by the probes' k_emit
     auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
       wn_faces_t T = new wn_faces_s();
-      T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0;
+      T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0; T->opt.angle_mode = 0;   // the probe records are crossing-mode (C.angle = false)
       wn_status_t rc = materialise<double>(B, VP, vper, vdom, vM, T);
       if (rc != WN_OK) { free_handle(T); return rc; }
       const int nq = (int)Q.size();
@@ -1656,10 +1800,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
         if (i == j || cands[i].alpha != cands[j].alpha) continue;
         const Cand &a = cands[i], &bb = cands[j];
         const FaceCtx &C = ctx[a.face];
-        const int tax = (L[a.alpha].cu != 0) ? 1 : 0;
-        const double Tt = tax ? C.Tv : C.Tu;
-        // omega(pt(c1) - s2*T_t e_t, beta2_ext) (translation identity, App. C.1)
-        q2.push_back({vface[bb.beta], a.px - (tax ? 0.0 : bb.s * Tt), a.py - (tax ? bb.s * Tt : 0.0)});
+        // omega(pt(c1) - t2, beta2_ext) (translation identity, App. C.1)
+        q2.push_back({vface[bb.beta], a.px - bb.ti * C.Tu, a.py - bb.tj * C.Tv});
         q2pairs.push_back({i, j});
       }
     std::vector<double> r2;

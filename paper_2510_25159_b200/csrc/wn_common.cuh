@@ -31,12 +31,18 @@ enum : uint32_t {
   K_XCH = 7,     // extended copy closing (crossing mode): -c(A -> Z)
   K_NCH = 8,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
   K_CLOSEG = 9,  // open contractible loop: gap chord Z -> A (crossing mode)
-  K_PAD = 10     // (unused)
+  K_SLINE = 10   // (x,y) = point of a line along v = (p Tu, q Tv), aux = (p, q) as two signed 12-bit
+                 // fields: omega(p,L) = +-1/2 for the bands of a general class (Prop. 2)
 };
 // SEG and SPAN (the records of the inner loop) are kinds 1 and 2: one compare
 constexpr uint32_t F_ANGLE = 1u << 4;   // literal atan2 chord angles (angle_mode = 1)
 constexpr uint32_t F_AXISV = 1u << 5;   // LINE parallel to v: test the u coordinate
 constexpr uint32_t F_GE = 1u << 6;      // LINE: left iff q >= c (else q <= c)
+
+// K_SLINE aux: class (p, q) packed in meta bits 8..19 / 20..31
+__host__ __device__ __forceinline__ uint32_t sline_meta(int p, int q) {
+  return K_SLINE | ((uint32_t)(p & 0xFFF) << 8) | ((uint32_t)(q & 0xFFF) << 20);
+}
 
 template <typename R>
 struct Hot;

@@ -295,6 +295,20 @@ __device__ __forceinline__ bool group_out_v(const HotView<float> &h, double px, 
   return !(h.fx <= x && x <= __half2float(hi.x) && h.fy <= y && y <= __half2float(hi.y));
 }
 
+// omega(p, L) for a slanted line (K_SLINE): +1/2 iff p is left of the line
+// through b along v = (p Tu, q Tv), i.e. cross(v, p - b) >= 0 (on L
+// counts as left, R11).  Evaluated without contraction, in the order of the
+// plain definition, so the decision is the correctly rounded one of that
+// expression.
+__device__ __forceinline__ bool sline_left(uint32_t meta, double bx, double by, double px, double py,
+                                           const double *__restrict__ dom) {
+  const int p = ((int)(meta << 12)) >> 20;
+  const int q = ((int)meta) >> 20;
+  const double vx = __dmul_rn((double)p, __ldg(dom + 1)), vy = __dmul_rn((double)q, __ldg(dom + 3));
+  const double cr = __dsub_rn(__dmul_rn(vx, __dsub_rn(py, by)), __dmul_rn(vy, __dsub_rn(px, bx)));
+  return cr >= 0.0;
+}
+
 // approximate fp32 |(dx,dy)| with flush-to-zero rsqrt (1 MUFU); a zero or
 // overflowing argument gives NaN/inf and every filter test treats it as
 // "not certified" (conservative)
@@ -553,6 +567,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           const double q = (meta & F_AXISV) ? px : py;
           const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
           if (act) halves += left ? 1 : -1;
+        } else if (kind == K_SLINE) {
+          if (act) halves += sline_left(meta, h.x, h.y, px, py, dom) ? 1 : -1;
         } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
           if (act) {
             const double cx = zx - px, cy = zy - py, ax = gax - px, ay = gay - py;
@@ -762,6 +778,8 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id, in
       } else if (kind == K_LINE) {
         const double q = (meta & F_AXISV) ? u : v;
         halves += ((meta & F_GE) ? (q >= hx) : (q <= hx)) ? 1 : -1;
+      } else if (kind == K_SLINE) {
+        halves += sline_left(meta, hx, hy, u, v, dom) ? 1 : -1;
       } else if (kind == K_XCH) {
         xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
       } else if (kind == K_NCH) {

@@ -282,3 +282,23 @@ def test_query_host_streamed_equals_device():
         assert np.array_equal(r.flag.numpy(), rf), chunk
         assert np.array_equal(np.nan_to_num(r.winding.numpy(), nan=9.0), np.nan_to_num(rw, nan=9.0)), chunk
     faces.close()
+
+
+@pytest.mark.parametrize("pq,angle_mode,hierarchy,dom", [
+    ((2, 1), 0, True, None), ((2, 1), 1, True, None), ((3, 2), 0, True, None), ((3, 2), 0, False, None),
+    ((1, -2), 0, True, None), ((-2, 3), 1, False, None), ((2, 3), 0, True, (6.283185307179586, 3.141592653589793)),
+    ((5, 2), 0, True, None)])
+def test_c3pq_general_class(pq, angle_mode, hierarchy, dom):
+    """General bi-periodic classes (p,q) (Prop. 2, Eq. 8):
+    slanted band lines, band copies along v, pairing over the band index."""
+    kw = {} if dom is None else dict(Tu=dom[0], Tv=dom[1])
+    wl = G.gen_c3pq(p=pq[0], q=pq[1], n_queries=8_000, **kw)
+    w, fl = _gpu(wl, angle_mode=angle_mode, hierarchy=hierarchy)
+    _check(wl, w, fl, min_cmp=0.99)
+
+
+def test_c3pq_beta_stored_off_tile():
+    """Pairing must find the proper beta translate wherever beta is stored."""
+    wl = G.gen_c3pq(p=3, q=-2, n_queries=6_000, beta_shift=(4, 3))
+    w, fl = _gpu(wl)
+    _check(wl, w, fl, min_cmp=0.99)

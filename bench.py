@@ -342,6 +342,82 @@ def main():
         e2e = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
+    # ---- implicit-grid path (wn_query_grid, Sec. 5.4.3 tessellation): the same
+    # C5 cell-centred 64x64 grids, generated in the kernel (0 B/query in) ----
+    ng_ = len(wl["meta"]["grid_box"])
+    gn = wl["meta"]["grid"]
+    gb = T(wl["meta"]["grid_box"], torch.float64)
+    gface = torch.arange(ng_, dtype=torch.int32, device=dev)
+
+    def gstep():
+        fc = wn.Faces.build(*geo, **kw)
+        fc.query_grid(gface, gb, gn, gn, out=(wnd, flg))
+        fc.close()
+
+    for _ in range(args.warmup):
+        gstep()
+    torch.cuda.synchronize()
+    g0 = torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
+    g0.record(st)
+    for _ in range(args.steps):
+        gstep()
+    g1.record(st)
+    torch.cuda.synchronize()
+    g_ms = max_over_ranks(g0.elapsed_time(g1), dist, dev) / args.steps
+    fc = wn.Faces.build(*geo, **kw)
+    fc.query_grid(gface, gb, gn, gn, out=(wnd, flg))
+    torch.cuda.synchronize()
+    g0.record(st)
+    for _ in range(nrep):
+        fc.query_grid(gface, gb, gn, gn, out=(wnd, flg))
+    g1.record(st)
+    torch.cuda.synchronize()
+    gq_ms = g0.elapsed_time(g1) / nrep
+    fc.close()
+    grid = {"api": "wn_query_grid", "ms_per_step": g_ms, "value": nq * world / (g_ms / 1e3), "unit": UNIT,
+            "query_ms": gq_ms, "query_queries_per_s": nq / (gq_ms / 1e3), "steps": args.steps,
+            "input_bytes_per_query": 0, "e2e": None}
+    if not args.no_e2e:
+        h_gb = pin(wl["meta"]["grid_box"])
+        side = torch.cuda.Stream(dev)
+        nch = 8
+        cg = (ng_ + nch - 1) // nch
+        gq = gn * gn
+
+        def grid_e2e_step():
+            g = [t.to(dev, non_blocking=True) for t in h_geo]
+            b = h_gb.to(dev, non_blocking=True)
+            fc = wn.Faces.build(*g, **kw)
+            for c in range(nch):
+                lo, hi = c * cg, min(ng_, (c + 1) * cg)
+                if lo >= hi:
+                    break
+                fc.query_grid(gface[lo:hi], b[lo:hi], gn, gn, out=(wnd[lo * gq:hi * gq], flg[lo * gq:hi * gq]))
+                ev = torch.cuda.Event()
+                ev.record(st)
+                side.wait_event(ev)
+                with torch.cuda.stream(side):
+                    h_w[lo * gq:hi * gq].copy_(wnd[lo * gq:hi * gq], non_blocking=True)
+                    h_f[lo * gq:hi * gq].copy_(flg[lo * gq:hi * gq], non_blocking=True)
+            st.wait_stream(side)
+            torch.cuda.current_stream(dev).synchronize()
+            fc.close()
+
+        grid_e2e_step()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(ksteps):
+            grid_e2e_step()
+        b.record(st)
+        torch.cuda.synchronize()
+        et = max_over_ranks(a.elapsed_time(b), dist, dev)
+        grid["e2e"] = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in h_geo) + h_gb.numel() * 8),
+                       "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
+
     # ---- roofline of the dominant kernel (k_phase1) ----
     k3_avg = k3_ms / max(k3_n, 1)
     p1_avg = p1_ms / max(k3_n, 1)      # measured live in the timed region (CUDA events on the stream)
@@ -379,6 +455,7 @@ def main():
                 "pairs_per_s": pairs_s,
                 "query_only": {"ms": q_ms, "queries_per_s": nq / (q_ms / 1e3), "pairs_per_s": pairs / (q_ms / 1e3)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+                "grid": grid,
                 "clocks": clocks, "counters": cnt, "faces_info": info, "flags": flags}
         print(json.dumps(line), flush=True)
     if dist:

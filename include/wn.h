@@ -121,6 +121,25 @@ wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face_id, const 
 wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t *h_face_id, const double *h_uv,
                           double *h_winding, uint8_t *h_flag, int64_t chunk, void *stream);
 
+/* Implicit-grid query: the tessellation application of Sec. 5.4.3 (P:884-895:
+ * "sample a uniform grid in the parametric domain", then classify) and the
+ * paper's per-shape 256x256 sample grids.  Grid g queries the nu x nv
+ * cell centres of the box grid_box[g] of face grid_face[g]; no uv is read from
+ * memory (0 B/query in), only the results are written.
+ *   n_grid     number of grids (>= 0); grid_face [n_grid] int32 (device).
+ *   grid_box   [n_grid][4] float64 (device, 16-B aligned) = (u_lo, v_lo, u_hi, v_hi).
+ *   nu, nv     cells per grid along u and v (>= 0); n_grid * nu * nv < 2^31.
+ *   winding, flag  [n_grid][nv][nu] (row-major: v outer, u inner), semantics
+ *            as for wn_query.  Query (g, iv, iu) is the point
+ *              u = u_lo + (iu + 0.5) * ((u_hi - u_lo) / nu),
+ *              v = v_lo + (iv + 0.5) * ((v_hi - v_lo) / nv),
+ *            each operation rounded in this order (no contraction), so an
+ *            explicit batch built by the same formula gives identical points.
+ *   An invalid grid_face sets flag 3 for the grid's queries; a non-finite box
+ *   gives non-finite points (flag 3).  Asynchronous on `stream` like wn_query. */
+wn_status_t wn_query_grid(wn_faces_t faces, int32_t n_grid, const int32_t *grid_face, const double *grid_box,
+                          int32_t nu, int32_t nv, double *winding, uint8_t *flag, void *stream);
+
 typedef struct {
   int64_t n_records;     /* hot records (MOVE/SEG/GROUP/LINE/...) over all faces */
   int64_t n_seg_records; /* SEG records (input segments x emitted lattice copies) */

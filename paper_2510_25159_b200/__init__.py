@@ -29,7 +29,7 @@ STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4
 FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
-           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host"]
+           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host", "wn_query_grid"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "warp_skips", "on_boundary", "span_tests", "warp_records", "_r10", "_r11"]
 
@@ -72,6 +72,8 @@ def load():
         L.wn_query.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp]
         L.wn_query_host.restype = C.c_int
         L.wn_query_host.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]
+        L.wn_query_grid.restype = C.c_int
+        L.wn_query_grid.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, vp, vp]
         L.wn_faces_info.restype = C.c_int
         L.wn_faces_info.argtypes = [vp, C.POINTER(FacesInfo)]
         L.wn_set_counters.restype = C.c_int
@@ -199,6 +201,32 @@ class Faces:
                                  _stream(stream, self.device))
         if rc != WN_OK:
             raise WNError(rc, last_error())
+        return QueryResult(wnd, flg)
+
+    def query_grid(self, grid_face, grid_box, nu, nv, out=None, stream=None):
+        """Implicit-grid query (wn_query_grid): nu x nv cell centres of each box
+        grid_box[g] = (u_lo, v_lo, u_hi, v_hi) of face grid_face[g]; returns
+        (winding float64 [n_grid*nv*nu], flag uint8 [...]) as CUDA tensors, row
+        major per grid (v outer, u inner); asynchronous on `stream`."""
+        torch = _torch()
+        gf = _dev(grid_face, torch.int32, self.device)
+        gb = _dev(grid_box, torch.float64, self.device).reshape(-1, 4)
+        ng = gf.numel()
+        n = ng * int(nu) * int(nv)
+        if out is None:
+            wnd = torch.empty(n, dtype=torch.float64, device=self.device)
+            flg = torch.empty(n, dtype=torch.uint8, device=self.device)
+        else:
+            wnd, flg = out
+        with torch.cuda.device(self.device):
+            rc = load().wn_query_grid(self._h, ng, _ptr(gf), _ptr(gb), int(nu), int(nv), _ptr(wnd), _ptr(flg),
+                                      _stream(stream, self.device))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        if stream is not None and hasattr(stream, "cuda_stream"):
+            gf.record_stream(stream)
+            gb.record_stream(stream)
+        self._keep_grid = (gf, gb)
         return QueryResult(wnd, flg)
 
     def query_host(self, face_id, uv, out=None, chunk=0, stream=None, sync=True):

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "wn_common.cuh"
 
@@ -93,7 +94,30 @@ struct QParams {
   int max_depth;
   int rule;
   unsigned long long *counters;
+  // implicit-grid batches (wn_query_grid; grid_box == nullptr: explicit uv):
+  // query q = g * grid_n + iv * grid_nu + iu is the cell centre (iu, iv) of
+  // grid g over the box grid_box[g] = (u_lo, v_lo, u_hi, v_hi) of face grid_face[g]
+  const double2 *grid_box;  // [n_grid][2] = (u_lo, v_lo), (u_hi, v_hi)
+  const int32_t *grid_face;
+  int64_t grid_n;
+  int32_t grid_nu, grid_nv;
 };
+
+// Cell-centred grid point (iu + 1/2) * (hi - lo) / n + lo, rounded step by step
+// in exactly this order (no contraction): the uv an explicit batch built by
+// lo + (i + 0.5) * ((hi - lo) / n) carries, bit for bit.
+__device__ __forceinline__ double grid_coord(double lo, double hi, int i, int n) {
+  return __dadd_rn(lo, __dmul_rn((double)i + 0.5, __ddiv_rn(__dsub_rn(hi, lo), (double)n)));
+}
+template <typename R>
+__device__ __forceinline__ void grid_point(const QParams<R> &P, int64_t q, double &u, double &v) {
+  const int64_t g = q / P.grid_n;
+  const int loc = (int)(q - g * P.grid_n);
+  const int iv = loc / P.grid_nu, iu = loc - iv * P.grid_nu;
+  const double2 lo = __ldg(P.grid_box + 2 * g), hi = __ldg(P.grid_box + 2 * g + 1);
+  u = grid_coord(lo.x, hi.x, iu, P.grid_nu);
+  v = grid_coord(lo.y, hi.y, iv, P.grid_nv);
+}
 
 // Counters (optional, COUNT=true): 0 (query, segment) root tests, 1 hard pairs,
 // 2 nodes, 3 evaluations, 4 leaves, 5 max depth, 6 warp-level skips (culled
@@ -328,8 +352,9 @@ constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushe
 #ifndef WN_P1_MINB
 #define WN_P1_MINB 4
 #endif
-// ANGLE: the build's angle_mode (every record of a handle carries the same F_ANGLE)
-template <typename R, bool COUNT, bool ANGLE>
+// ANGLE: the build's angle_mode (every record of a handle carries the same F_ANGLE);
+// GRID: implicit-grid batch (wn_query_grid) instead of explicit uv
+template <typename R, bool COUNT, bool ANGLE, bool GRID>
 __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
   constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
@@ -341,6 +366,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   const Tile T = P.tiles[blockIdx.x];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int f = T.face;
+  if (f < 0) {                                             // grid of an invalid face id: flag 3
+    for (int i = t; i < T.qcnt; i += NTH) {
+      P.winding[T.qbeg + i] = nan_d();
+      P.flag[T.qbeg + i] = 3;
+    }
+    return;
+  }
   const int rec0 = P.face_rec_off[f];
   const int nrec = P.face_rec_off[f + 1] - rec0;
   // a face program that fits one chunk is staged once and reused by every
@@ -359,6 +391,22 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   const double *dom = P.face_dom + 4 * f;
   const int unsorted = *P.unsorted;
   const int cold0 = P.face_cold_off[f];
+  // implicit grid: a unit lies inside one grid (units are cut per grid), so the
+  // grid index, its box and the cell steps are per-CTA values
+  // (kept in shared memory, not in registers across the record loop)
+  __shared__ double s_grid[4];   // u_lo, v_lo, (u_hi - u_lo) / nu, (v_hi - v_lo) / nv
+  __shared__ int s_gloc0;
+  if constexpr (GRID) {
+    if (t == 0) {
+      const int64_t g = T.qbeg / P.grid_n;
+      s_gloc0 = (int)(T.qbeg - g * P.grid_n);
+      const double2 lo = __ldg(P.grid_box + 2 * g), hi = __ldg(P.grid_box + 2 * g + 1);
+      s_grid[0] = lo.x;
+      s_grid[1] = lo.y;
+      s_grid[2] = __ddiv_rn(__dsub_rn(hi.x, lo.x), (double)P.grid_nu);   // as in grid_coord
+      s_grid[3] = __ddiv_rn(__dsub_rn(hi.y, lo.y), (double)P.grid_nv);
+    }
+  }
   const double eps = P.eps;
   // fp32-filter constant: a distance df > eps_c certifies d >= eps
   // (fp64 records; margins 2^-16 scale + 2^-17 relative)
@@ -406,7 +454,16 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     const int32_t qi = valid ? (unsorted ? P.perm[pos] : pos) : 0;
     double px = 0.0, py = 0.0;
     if (valid) {
-      double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+      double u, v;
+      if constexpr (GRID) {
+        const int loc = s_gloc0 + sub + t;
+        const int iv = loc / P.grid_nu, iu = loc - iv * P.grid_nu;
+        u = __dadd_rn(s_grid[0], __dmul_rn((double)iu + 0.5, s_grid[2]));   // = grid_coord(), bit for bit
+        v = __dadd_rn(s_grid[1], __dmul_rn((double)iv + 0.5, s_grid[3]));
+      } else {
+        u = P.uv[2 * (int64_t)qi];
+        v = P.uv[2 * (int64_t)qi + 1];
+      }
       if (!isfinite(u) || !isfinite(v)) {
         P.winding[qi] = nan_d();
         P.flag[qi] = 3;
@@ -734,8 +791,10 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id, in
   if (*P.hq_count <= P.hq_cap) return;   // nothing overflowed (uniform)
   for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < n; qi += (int64_t)gridDim.x * blockDim.x) {
     if (P.flag[qi] != FLAG_OVERFLOW) continue;
-    const int f = face_id[qi];
-    double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+    double u, v;
+    int f;
+    if (P.grid_box) { grid_point(P, qi, u, v); f = P.grid_face[qi / P.grid_n]; }
+    else { f = face_id[qi]; u = P.uv[2 * (int64_t)qi]; v = P.uv[2 * (int64_t)qi + 1]; }
     const uint8_t per = P.face_per[f];
     const double *dom = P.face_dom + 4 * f;
     if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
@@ -965,7 +1024,86 @@ __global__ void k_tiles(int32_t n_faces, int32_t max_tiles, int32_t qu, const in
   tiles[i] = T;
 }
 
+// Implicit-grid batches (wn_query_grid): units are cut per grid, largest
+// faces first; no bucketing (a grid is one face's contiguous query range).
+__global__ void k_grid_keys(int32_t n_grid, const int32_t *__restrict__ grid_face, int32_t n_faces,
+                            const int32_t *__restrict__ face_rec_off, uint32_t *__restrict__ key,
+                            int32_t *__restrict__ val) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n_grid) return;
+  const int f = grid_face[g];
+  const int nrec = (f >= 0 && f < n_faces) ? face_rec_off[f + 1] - face_rec_off[f] : 0;
+  key[g] = 0xffffffffu - (uint32_t)nrec;     // ascending key = descending record count
+  val[g] = g;
+}
+
+__global__ void k_grid_tiles(int32_t n_grid, int32_t tpg, int32_t qu, int64_t G, const int32_t *__restrict__ order,
+                             const int32_t *__restrict__ grid_face, int32_t n_faces, Tile *__restrict__ tiles,
+                             int32_t *__restrict__ ntiles) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)n_grid * tpg;
+  if (i == 0) *ntiles = (int32_t)total;
+  if (i >= total) return;
+  const int g = order[i / tpg];
+  const int k = (int)(i % tpg);
+  const int f = grid_face[g];
+  Tile T;
+  T.face = (f >= 0 && f < n_faces) ? f : -1;
+  T.qbeg = (int64_t)g * G + (int64_t)k * qu;
+  const int64_t rem = G - (int64_t)k * qu;
+  T.qcnt = (int32_t)(rem < qu ? rem : qu);
+  tiles[i] = T;
+}
+
 static thread_local int32_t g_launches = 0;
+
+// K3 (phase 1, hard pairs, overflow, finish) on prepared tiles
+template <typename R>
+static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const int32_t *face_id, int max_tiles,
+                             cudaStream_t st, int &launches) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
+  if (F->timing_on) {
+    WN_CUDA(cudaEventCreate(&e0));
+    WN_CUDA(cudaEventCreate(&em));
+    WN_CUDA(cudaEventCreate(&e1));
+    WN_CUDA(cudaEventRecord(e0, st));
+  }
+  const int hb = 148 * 8;
+  const bool ang = F->opt.angle_mode == 1;
+  const bool grid = P.grid_box != nullptr;
+  auto phase1 = [&](auto cnt_tag) {
+    constexpr bool C_ = decltype(cnt_tag)::value;
+    if (ang) {
+      if (grid) k_phase1<R, C_, true, true><<<max_tiles, NTH, 0, st>>>(P);
+      else k_phase1<R, C_, true, false><<<max_tiles, NTH, 0, st>>>(P);
+    } else {
+      if (grid) k_phase1<R, C_, false, true><<<max_tiles, NTH, 0, st>>>(P);
+      else k_phase1<R, C_, false, false><<<max_tiles, NTH, 0, st>>>(P);
+    }
+  };
+  if (F->counters_on) {
+    WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
+    phase1(std::true_type{});
+    if (em) WN_CUDA(cudaEventRecord(em, st));
+    k_hard<R, true><<<hb, 256, 0, st>>>(P);
+    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters);
+  } else {
+    phase1(std::false_type{});
+    if (em) WN_CUDA(cudaEventRecord(em, st));
+    k_hard<R, false><<<hb, 256, 0, st>>>(P);
+    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr);
+  }
+  launches += 4;
+  if (F->timing_on) {
+    WN_CUDA(cudaEventRecord(e1, st));
+    F->k3_events.push_back({e0, e1});
+    F->k3_mid.push_back(em);
+  }
+  WN_CUDA(cudaGetLastError());
+  return WN_OK;
+}
 
 template <typename R>
 static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id, const double *uv,
@@ -1051,36 +1189,96 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.max_depth = F->max_depth;
   P.rule = F->opt.rule;
   P.counters = F->counters;
-  cudaEvent_t e0 = nullptr, e1 = nullptr, em = nullptr;
-  if (F->timing_on) {
-    WN_CUDA(cudaEventCreate(&e0));
-    WN_CUDA(cudaEventCreate(&em));
-    WN_CUDA(cudaEventCreate(&e1));
-    WN_CUDA(cudaEventRecord(e0, st));
+  P.grid_box = nullptr;
+  P.grid_face = nullptr;
+  P.grid_n = 0;
+  P.grid_nu = P.grid_nv = 0;
+  {
+    const wn_status_t rc = launch_k3<R>(F, P, n, face_id, max_tiles, st, launches);
+    if (rc != WN_OK) return rc;
   }
-  const int hb = 148 * 8;
-  const bool ang = F->opt.angle_mode == 1;
-  if (F->counters_on) {
-    WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
-    if (ang) k_phase1<R, true, true><<<max_tiles, NTH, 0, st>>>(P);
-    else k_phase1<R, true, false><<<max_tiles, NTH, 0, st>>>(P);
-    if (em) WN_CUDA(cudaEventRecord(em, st));
-    k_hard<R, true><<<hb, 256, 0, st>>>(P);
-    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, winding, flag, P.rule, F->counters);
-  } else {
-    if (ang) k_phase1<R, false, true><<<max_tiles, NTH, 0, st>>>(P);
-    else k_phase1<R, false, false><<<max_tiles, NTH, 0, st>>>(P);
-    if (em) WN_CUDA(cudaEventRecord(em, st));
-    k_hard<R, false><<<hb, 256, 0, st>>>(P);
-    k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, winding, flag, P.rule, nullptr);
+  WN_CUDA(cudaGetLastError());
+  cache_free(base, st);
+  if (F->last_use) WN_CUDA(cudaEventRecord(F->last_use, st));
+  g_launches = launches;
+  return WN_OK;
+}
+
+template <typename R>
+static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t *grid_face, const double *grid_box,
+                                     int32_t nu, int32_t nv, double *winding, uint8_t *flag, cudaStream_t st) {
+  const int nf = F->n_faces;
+  const int64_t G = (int64_t)nu * nv;
+  const int64_t n = G * n_grid;
+  if (n > INT32_MAX - 1) {
+    set_error("wn_query_grid: batch too large (%lld queries); split it", (long long)n);
+    return WN_ERR_ARG;
   }
+  int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
+  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(64, atoi(s)));
+  const int qu = QT * sub;
+  const int tpg = (int)((G + qu - 1) / qu);
+  const int64_t max_tiles64 = (int64_t)n_grid * tpg;
+  if (max_tiles64 > INT32_MAX) { set_error("wn_query_grid: too many tiles"); return WN_ERR_ARG; }
+  const int max_tiles = (int)max_tiles64;
+  int hq_cap = (int)std::min<int64_t>(std::max<int64_t>(n / 8, 1 << 20), 1 << 26);
+  if (const char *cap = std::getenv("WN_HQ_CAP")) hq_cap = std::max(1, atoi(cap));
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                  (const int32_t *)nullptr, (int32_t *)nullptr, n_grid, 0, 32, st);
+  size_t need = 0;
+  auto carve = [&](size_t bytes) { size_t o = need; need += (bytes + 255) & ~(size_t)255; return o; };
+  const size_t o_flags = carve(sizeof(int32_t) * 8);
+  const size_t o_k0 = carve(sizeof(uint32_t) * n_grid), o_k1 = carve(sizeof(uint32_t) * n_grid);
+  const size_t o_v0 = carve(sizeof(int32_t) * n_grid), o_v1 = carve(sizeof(int32_t) * n_grid);
+  const size_t o_tiles = carve(sizeof(Tile) * (size_t)max_tiles);
+  const size_t o_hq = carve(sizeof(HardEntry) * (size_t)hq_cap);
+  const size_t o_tmp = carve(tmp);
+  char *base = nullptr;
+  WN_CUDA(cache_alloc((void **)&base, need, st));
+  int32_t *flags = (int32_t *)(base + o_flags);
+  uint32_t *k0 = (uint32_t *)(base + o_k0), *k1 = (uint32_t *)(base + o_k1);
+  int32_t *v0 = (int32_t *)(base + o_v0), *v1 = (int32_t *)(base + o_v1);
+  Tile *tiles = (Tile *)(base + o_tiles);
+  int launches = 0;
+  WN_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * 8, st));
+  const int TB = 256;
+  k_grid_keys<<<(n_grid + TB - 1) / TB, TB, 0, st>>>(n_grid, grid_face, nf, F->face_rec_off, k0, v0);
+  ++launches;
+  cub::DeviceRadixSort::SortPairs(base + o_tmp, tmp, k0, k1, v0, v1, n_grid, 0, 32, st);
   launches += 4;
-  if (F->timing_on) {
-    WN_CUDA(cudaEventRecord(e1, st));
-    F->k3_events.push_back({e0, e1});
-    F->k3_mid.push_back(em);
+  k_grid_tiles<<<(max_tiles + TB - 1) / TB, TB, 0, st>>>(n_grid, tpg, qu, G, v1, grid_face, nf, tiles, flags + 1);
+  ++launches;
+  QParams<R> P;
+  P.hot = (const Hot<R> *)F->hot;
+  P.cold = (const Cold<R> *)F->cold;
+  P.face_rec_off = F->face_rec_off;
+  P.face_cold_off = F->face_cold_off;
+  P.face_dom = F->face_dom;
+  P.face_per = F->face_per;
+  P.face_M = F->face_M;
+  P.uv = nullptr;
+  P.winding = winding;
+  P.flag = flag;
+  P.tiles = tiles;
+  P.ntiles = flags + 1;
+  P.perm = nullptr;
+  P.unsorted = flags;            // 0: the query index is the position
+  P.hq = (HardEntry *)(base + o_hq);
+  P.hq_count = flags + 2;
+  P.hq_cap = hq_cap;
+  P.eps = F->eps;
+  P.max_depth = F->max_depth;
+  P.rule = F->opt.rule;
+  P.counters = F->counters;
+  P.grid_box = reinterpret_cast<const double2 *>(grid_box);
+  P.grid_face = grid_face;
+  P.grid_n = G;
+  P.grid_nu = nu;
+  P.grid_nv = nv;
+  {
+    const wn_status_t rc = launch_k3<R>(F, P, n, nullptr, max_tiles, st, launches);
+    if (rc != WN_OK) return rc;
   }
   WN_CUDA(cudaGetLastError());
   cache_free(base, st);
@@ -1123,6 +1321,23 @@ extern "C" wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face
   if (faces->ready) WN_CUDA(cudaStreamWaitEvent(st, faces->ready, 0));
   if (faces->precision == 1) return wn::launch_query<float>(faces, n, face_id, uv, winding, flag, st);
   return wn::launch_query<double>(faces, n, face_id, uv, winding, flag, st);
+}
+
+extern "C" wn_status_t wn_query_grid(wn_faces_t faces, int32_t n_grid, const int32_t *grid_face,
+                                     const double *grid_box, int32_t nu, int32_t nv, double *winding, uint8_t *flag,
+                                     void *stream) {
+  if (!faces) { wn::set_error("wn_query_grid: NULL handle"); return WN_ERR_ARG; }
+  if (n_grid < 0 || nu < 0 || nv < 0) { wn::set_error("wn_query_grid: negative size"); return WN_ERR_ARG; }
+  if (n_grid == 0 || nu == 0 || nv == 0) { wn::g_launches = 0; return WN_OK; }
+  if (!grid_face || !grid_box || !winding || !flag) { wn::set_error("wn_query_grid: NULL array"); return WN_ERR_ARG; }
+  if (((uintptr_t)grid_box & 15) != 0) { wn::set_error("wn_query_grid: grid_box must be 16-B aligned"); return WN_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  WN_CUDA(cudaSetDevice(faces->device));
+  wn::ensure_pool(faces->device);
+  if (faces->ready) WN_CUDA(cudaStreamWaitEvent(st, faces->ready, 0));
+  if (faces->precision == 1)
+    return wn::launch_query_grid<float>(faces, n_grid, grid_face, grid_box, nu, nv, winding, flag, st);
+  return wn::launch_query_grid<double>(faces, n_grid, grid_face, grid_box, nu, nv, winding, flag, st);
 }
 
 extern "C" int32_t wn_last_query_launches(void) { return wn::g_launches; }

@@ -302,3 +302,69 @@ def test_c3pq_beta_stored_off_tile():
     wl = G.gen_c3pq(p=3, q=-2, n_queries=6_000, beta_shift=(4, 3))
     w, fl = _gpu(wl)
     _check(wl, w, fl, min_cmp=0.99)
+
+
+def _grid_uv(boxes, nu, nv):
+    """Explicit uv of an implicit grid batch, by the formula include/wn.h documents."""
+    out = []
+    for b in np.asarray(boxes, dtype=np.float64).reshape(-1, 4):
+        us = b[0] + (np.arange(nu) + 0.5) * ((b[2] - b[0]) / nu)
+        vs = b[1] + (np.arange(nv) + 0.5) * ((b[3] - b[1]) / nv)
+        U, V = np.meshgrid(us, vs)
+        out.append(np.stack([U.ravel(), V.ravel()], 1))
+    return np.concatenate(out)
+
+
+@pytest.mark.parametrize("angle_mode", [0, 1])
+def test_grid_query_c5_reduced(angle_mode):
+    """wn_query_grid (implicit cell-centred grids, Sec. 5.4.3 tessellation,
+    P:884-895) = wn_query on the explicit points, and parity with the oracle."""
+    wl = G.gen_c5(n_faces=120, grid=32)
+    gb = wl["meta"]["grid_box"]
+    faces = wn.Faces.from_workload(wl, angle_mode=angle_mode)
+    rg = faces.query_grid(np.arange(len(gb)), gb, 32, 32)
+    re_ = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    wg, fg = rg.winding.cpu().numpy(), rg.flag.cpu().numpy()
+    we, fe = re_.winding.cpu().numpy(), re_.flag.cpu().numpy()
+    faces.close()
+    assert np.array_equal(fg, fe)
+    tol = 0.0 if angle_mode == 0 else 1e-12     # angle mode: atomic fp64 sums in any order
+    assert np.nanmax(np.abs(wg - we)) <= tol
+    _check(wl, wg, fg, min_cmp=0.97)
+
+
+def test_grid_query_nonsquare_periodic_and_invalid():
+    """Rectangular grids (nu != nv) on the C3 torus, an invalid face id and a
+    non-finite box (flag 3), grids in any face order."""
+    wl = G.gen_c3(n_queries=10)
+    T = wl["meta"]["T"]
+    boxes = np.array([[0.0, 0.0, T, T], [1.0, 2.0, 3.5, 2.5], [0.0, 0.0, 1.0, 1.0], [np.nan, 0.0, 1.0, 1.0]])
+    gf = np.array([0, 0, 5, 0], dtype=np.int32)
+    nu, nv = 37, 23
+    faces = wn.Faces.from_workload(wl)
+    r = faces.query_grid(gf, boxes, nu, nv)
+    torch.cuda.synchronize()
+    w, fl = r.winding.cpu().numpy(), r.flag.cpu().numpy()
+    faces.close()
+    G_ = nu * nv
+    assert np.all(fl[2 * G_:] == 3) and np.all(np.isnan(w[2 * G_:]))
+    uv = _grid_uv(boxes[:2], nu, nv)
+    wl2 = dict(wl)
+    wl2["face_id"] = np.zeros(len(uv), dtype=np.int32)
+    wl2["uv"] = uv
+    _check(wl2, w[:2 * G_], fl[:2 * G_], min_cmp=0.99)
+
+
+def test_grid_query_c5_full_size_equals_explicit():
+    """BASELINE configs[4] at full size: all 81.92M grid results equal the
+    explicit-uv results (crossing mode: bit-identical)."""
+    wl = G.gen_c5()
+    gb = wl["meta"]["grid_box"]
+    faces = wn.Faces.from_workload(wl)
+    re_ = faces.query(wl["face_id"], wl["uv"])
+    rg = faces.query_grid(np.arange(len(gb)), gb, 64, 64)
+    torch.cuda.synchronize()
+    assert torch.equal(rg.flag, re_.flag)
+    assert torch.equal(rg.winding, re_.winding)
+    faces.close()

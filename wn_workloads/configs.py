@@ -497,6 +497,7 @@ def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
     T = TWO_PI_Q
     b = _Builder()
     uvs = []
+    boxes = []   # per-face grid box (u_lo, v_lo, u_hi, v_hi): the implicit-grid form of the batch
     fids = []
     n_periodic = 0
     slots = [(i, j) for i in (-1, 0, 1) for j in (-1, 0, 1)]
@@ -522,6 +523,7 @@ def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
                 b.end_loop()
             b.end_face(periodic=0, domain=(0.0, 1.0, 0.0, 1.0))
             allp = np.concatenate(pts)
+            boxes.append((*allp.min(0), *allp.max(0)))
             uvs.append(_grid(allp.min(0), allp.max(0), grid))
         else:
             n_periodic += 1
@@ -555,9 +557,11 @@ def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
                     b.seg(_wrap_store(P, T, 1.0, True, False), w)
                 b.end_loop()
             b.end_face(periodic=1, domain=(0.0, T, 0.0, 1.0))
+            boxes.append((0.0, 0.0, T, 1.0))
             uvs.append(_grid((0.0, 0.0), (T, 1.0), grid))
         fids.append(np.full(grid * grid, f))
-    meta = dict(kind="C5", n_periodic=n_periodic)
+    meta = dict(kind="C5", n_periodic=n_periodic, grid=grid,
+                grid_box=np.ascontiguousarray(np.asarray(boxes, dtype=np.float64).reshape(-1, 4)))
     return _finish(b, np.concatenate(fids), np.concatenate(uvs), True, "C5", meta)
 
 

@@ -52,6 +52,8 @@ def lib():
         L.orc_lift.argtypes = geo + [ip, ip, dp]
         L.orc_pairs.restype = C.c_int
         L.orc_pairs.argtypes = geo + [C.c_int, ip, ip, ip]
+        L.orc_nurbs_decompose.restype = C.c_int
+        L.orc_nurbs_decompose.argtypes = [C.c_int, C.c_int, dp, dp, dp, C.c_int, dp, dp]
         L.orc_query.restype = C.c_int
         L.orc_query.argtypes = geo + [C.c_int64, ip, dp, C.c_double, C.c_double, C.c_int, C.c_int,
                                       C.c_int, C.c_int, C.c_int, dp, u8, u8, dp, i64p, ip]
@@ -155,3 +157,43 @@ def query(wl, face_id=None, uv=None, delta=1e-9, tol=1e-9, N5=8, rule=0, reduce=
     if rc != 0:
         raise ValueError("oracle query: invalid geometry rc=%d" % rc)
     return dict(w=w, flag=fl, comparable=cm.astype(bool), dist_lb=dl, pieces=pc, face_err=fe)
+
+
+def nurbs_decompose(p, P, w, U):
+    """Oracle NURBS -> rational Bezier (repeated knot insertion).  Returns a list
+    of (P [p+1,2], w [p+1]) segments."""
+    P = np.ascontiguousarray(P, dtype=np.float64).reshape(-1, 2)
+    w = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    cap = len(U)
+    oP = np.zeros((cap, p + 1, 2))
+    ow = np.zeros((cap, p + 1))
+    rc = lib().orc_nurbs_decompose(int(p), P.shape[0], _p(P, C.c_double), _p(w, C.c_double), _p(U, C.c_double),
+                                   cap, _p(oP, C.c_double), _p(ow, C.c_double))
+    if rc < 0:
+        raise ValueError("oracle nurbs_decompose: rc=%d" % rc)
+    return [(oP[i].copy(), ow[i].copy()) for i in range(rc)]
+
+
+def nurbs_to_bezier_workload(wl):
+    """The oracle's own Bezier form of a NURBS workload (wn_workloads.gen_nurbs
+    layout): every curve decomposed by nurbs_decompose, loops re-indexed."""
+    ctrl, wts, deg, lso = [], [], [], [0]
+    co, ko, lco = wl["curve_ctrl_off"], wl["curve_knot_off"], wl["loop_curve_off"]
+    for l in range(len(lco) - 1):
+        nseg = 0
+        for c in range(lco[l], lco[l + 1]):
+            p = int(wl["curve_degree"][c])
+            segs = nurbs_decompose(p, wl["ctrl_uv"][co[c]:co[c + 1]],
+                                   None if wl["ctrl_w"] is None else wl["ctrl_w"][co[c]:co[c + 1]],
+                                   wl["knots"][ko[c]:ko[c + 1]])
+            for P, w in segs:
+                ctrl.append(P)
+                wts.append(w)
+                deg.append(p)
+            nseg += len(segs)
+        lso.append(lso[-1] + nseg)
+    out = dict(wl)
+    out.update(ctrl_uv=np.ascontiguousarray(np.concatenate(ctrl)), ctrl_w=np.ascontiguousarray(np.concatenate(wts)),
+               seg_degree=np.asarray(deg, dtype=np.int32), loop_seg_off=np.asarray(lso, dtype=np.int32))
+    return out

@@ -631,3 +631,94 @@ int orc_query(int n_faces, int n_loops, int n_segs, const double *ctrl_uv, const
   model_free(&M);
   return 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * NURBS ingest ("B-spline or NURBS curves can always be subdivided
+ * into (rational) Bezier segments"; SPEC decompose_bspline).  Plain repeated
+ * single knot insertion (Boehm's rule in homogeneous coordinates (w x, w y,
+ * w)): every distinct interior knot value of multiplicity s is inserted p - s
+ * times; afterwards every interior knot has multiplicity p and the control
+ * polygon splits into Bezier segments j = points [j p, j p + p].
+ *   Single insertion of u with K[l] <= u < K[l+1] (NURBS Book eq. 5.15):
+ *     Q_i = P_i                                  i <= l - p
+ *     Q_i = a_i P_i + (1 - a_i) P_{i-1},          l-p+1 <= i <= l,
+ *           a_i = (u - K[i]) / (K[i+p] - K[i])
+ *     Q_i = P_{i-1}                              i >= l + 1
+ * PINNED (tests/test_oracle_nurbs.py) by an independent Cox-de Boor evaluation
+ * of the spline at random parameters, SPEC's single-span / two-span examples
+ * and the exact 9-point NURBS circle.
+ * Input: degree p (1..5), n_ctrl points P[n_ctrl][2], weights w (NULL = 1),
+ * knots U[n_ctrl + p + 1] (clamped, non-decreasing, interior multiplicity <= p).
+ * Output: up to cap segments of p+1 points (outP [seg][p+1][2], outw
+ * [seg][p+1]; the curve's two end points are copied from P exactly); returns the number of segments, -1 invalid knots, -2 cap too
+ * small, -3 bad degree / weight. */
+int orc_nurbs_decompose(int p, int n_ctrl, const double *P, const double *w, const double *U, int cap,
+                        double *outP, double *outw) {
+  if (p < 1 || p > ORC_MAXDEG || n_ctrl < p + 1) return -3;
+  int nk = n_ctrl + p + 1;
+  for (int i = 0; i + 1 < nk; i++) if (!(U[i] <= U[i + 1])) return -1;
+  for (int i = 1; i <= p; i++) if (U[i] != U[0] || U[nk - 1 - i] != U[nk - 1]) return -1;
+  if (!(U[p] < U[nk - 1 - p])) return -1;
+  for (int i = p + 1; i < nk - 1 - p; i++) {        /* interior multiplicity <= p */
+    int s = 1;
+    while (i + s < nk - 1 - p && U[i + s] == U[i]) s++;
+    if (s > p) return -1;
+    i += s - 1;
+  }
+  if (w) for (int i = 0; i < n_ctrl; i++) if (!(w[i] > 0.0)) return -3;
+  int maxn = n_ctrl + p * nk;                       /* room for all insertions */
+  double *H = (double *)malloc(sizeof(double) * 3 * (size_t)maxn);
+  double *H2 = (double *)malloc(sizeof(double) * 3 * (size_t)maxn);
+  double *K = (double *)malloc(sizeof(double) * (size_t)(nk + p * nk));
+  for (int i = 0; i < n_ctrl; i++) {
+    double wi = w ? w[i] : 1.0;
+    H[3 * i] = wi * P[2 * i]; H[3 * i + 1] = wi * P[2 * i + 1]; H[3 * i + 2] = wi;
+  }
+  memcpy(K, U, sizeof(double) * (size_t)nk);
+  int n = n_ctrl, m = nk;
+  double u_end = U[nk - 1 - p];
+  int i = p + 1;
+  while (K[i] < u_end) {
+    double u = K[i];
+    int s = 0;
+    while (K[i + s] == u) s++;
+    for (int r = 0; r < p - s; r++) {
+      int l = i + s - 1 + r;                         /* last index with K[l] <= u */
+      for (int j = 0; j <= n; j++) {
+        if (j <= l - p) { memcpy(H2 + 3 * j, H + 3 * j, 3 * sizeof(double)); }
+        else if (j >= l + 1) { memcpy(H2 + 3 * j, H + 3 * (j - 1), 3 * sizeof(double)); }
+        else {
+          double a = (u - K[j]) / (K[j + p] - K[j]);
+          for (int c = 0; c < 3; c++) H2[3 * j + c] = a * H[3 * j + c] + (1.0 - a) * H[3 * (j - 1) + c];
+        }
+      }
+      double *t = H; H = H2; H2 = t;
+      n++;
+      memmove(K + l + 2, K + l + 1, sizeof(double) * (size_t)(m - l - 1));
+      K[l + 1] = u;
+      m++;
+    }
+    i += p;                                          /* now multiplicity p */
+  }
+  int nseg = (n - 1) / p;
+  int rc = nseg;
+  if (nseg > cap) rc = -2;
+  else
+    for (int sgi = 0; sgi < nseg; sgi++)
+      for (int j = 0; j <= p; j++) {
+        const double *h = H + 3 * (sgi * p + j);
+        outw[sgi * (p + 1) + j] = h[2];
+        outP[2 * (sgi * (p + 1) + j)] = h[0] / h[2];
+        outP[2 * (sgi * (p + 1) + j) + 1] = h[1] / h[2];
+      }
+  if (rc > 0) {
+    /* the curve's end points are P_0 and P_n exactly (clamped knots): keep
+     * them bit-identical (junctions with the neighbouring curves of a loop) */
+    outP[0] = P[0]; outP[1] = P[1]; outw[0] = w ? w[0] : 1.0;
+    int e = (nseg - 1) * (p + 1) + p;
+    outP[2 * e] = P[2 * (n_ctrl - 1)]; outP[2 * e + 1] = P[2 * (n_ctrl - 1) + 1];
+    outw[e] = w ? w[n_ctrl - 1] : 1.0;
+  }
+  free(H); free(H2); free(K);
+  return rc;
+}

@@ -196,3 +196,30 @@ def polygon_loop(V):
     V = np.asarray(V, dtype=np.float64)
     n = len(V)
     return [(np.stack([V[k], V[(k + 1) % n]]), None) for k in range(n)]
+
+
+def deboor_eval(p, P, w, U, t):
+    """NURBS point by the Cox-de Boor recursion (textbook definition of the
+    B-spline basis, 0/0 := 0; half-open spans, t = U[-1] in the last span):
+    C(t) = sum N_ip(t) w_i P_i / sum N_ip(t) w_i."""
+    P = np.asarray(P, dtype=np.float64)
+    n = len(P)
+    w = np.ones(n) if w is None else np.asarray(w, dtype=np.float64)
+    U = np.asarray(U, dtype=np.float64)
+    m = len(U)
+    # degree-0 basis
+    N = np.zeros(m - 1)
+    last = max(i for i in range(m - 1) if U[i] < U[i + 1])
+    for i in range(m - 1):
+        if U[i] <= t < U[i + 1] or (t == U[-1] and i == last):
+            N[i] = 1.0
+    for k in range(1, p + 1):
+        N2 = np.zeros(m - 1 - k)
+        for i in range(m - 1 - k):
+            a = (t - U[i]) / (U[i + k] - U[i]) * N[i] if U[i + k] != U[i] else 0.0
+            b = (U[i + k + 1] - t) / (U[i + k + 1] - U[i + 1]) * N[i + 1] if U[i + k + 1] != U[i + 1] else 0.0
+            N2[i] = a + b
+        N = N2
+    N = N[:n]
+    den = N @ w
+    return (N * w) @ P / den

@@ -565,6 +565,100 @@ def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
     return _finish(b, np.concatenate(fids), np.concatenate(uvs), True, "C5", meta)
 
 
+# ----------------------------------------------------------------------------
+# NURBS ingest workload ("B-spline or NURBS
+# curves can always be subdivided into (rational) Bezier segments").  Not a
+# BASELINE config: a parity case for wn_build_faces_nurbs.  Layout (ABI of
+# wn_build_faces_nurbs, include/wn.h):
+#   ctrl_uv [n_ctrl,2], ctrl_w [n_ctrl], curve_degree [n_curves],
+#   curve_ctrl_off [n_curves+1], knots [n_knots], curve_knot_off [n_curves+1],
+#   loop_curve_off [n_loops+1], face_loop_off, face_periodic, face_domain,
+#   face_id, uv.
+# ----------------------------------------------------------------------------
+
+def _clamped_knots(rng, n_ctrl, p, max_mult=None):
+    """Clamped knot vector on [0,1] for n_ctrl control points of degree p with
+    random interior knots, some repeated (multiplicity <= max_mult <= p)."""
+    n_int = n_ctrl - p - 1
+    max_mult = p if max_mult is None else max_mult
+    ks = []
+    while len(ks) < n_int:
+        u = float(rng.uniform(0.02, 0.98))
+        mult = int(rng.integers(1, max_mult + 1)) if rng.uniform() < 0.3 else 1
+        ks.extend([u] * min(mult, n_int - len(ks)))
+    ks = sorted(ks)
+    return np.concatenate([np.zeros(p + 1), np.asarray(ks), np.ones(p + 1)])
+
+
+def gen_nurbs(seed=7, n_faces=200, q_per_face=256, max_curves=3):
+    """Faces bounded by closed loops made of 1..max_curves clamped NURBS curves
+    (degree 1..5, 1..8 knot spans, weights U[0.5,2], random interior knot
+    multiplicities): an outer star-like loop (CCW) about (0.5,0.5) of radius
+    0.38 +- 0.04 and 0..2 CW holes of radius 0.07 at (0.5 +- 0.17, 0.5);
+    queries uniform in the unit square."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    ctrl, wts, deg, coff, knots, koff, lco, flo = [], [], [], [0], [], [0], [0], [0]
+    n_loops = 0
+
+    def loop(center, r_mean, r_jit, cw):
+        nonlocal n_loops
+        k = int(rng.integers(1, max_curves + 1))
+        cuts = np.sort(rng.uniform(0, 2 * math.pi, size=k))
+        th0 = cuts[0]
+        bounds = list(cuts) + [th0 + 2 * math.pi]
+        start_pt = None
+        pts_prev_end = None
+        curves = []
+        for c in range(k):
+            a, b_ = bounds[c], bounds[c + 1]
+            p = int(rng.integers(1, 6))
+            spans = int(rng.integers(1, 9))
+            # control polygon fine enough (<= 30 deg per leg) that the curve
+            # follows the star polygon (stays simple, encloses the centre)
+            need = int(math.ceil((b_ - a) / (math.pi / 6))) + 1
+            spans = max(spans, need - p)
+            n_ctrl = p + spans
+            th = np.linspace(a, b_, n_ctrl)
+            rad = r_mean + rng.uniform(-r_jit, r_jit, size=n_ctrl)
+            P = np.stack([center[0] + rad * np.cos(th), center[1] + rad * np.sin(th)], 1)
+            if pts_prev_end is not None:
+                P[0] = pts_prev_end
+            pts_prev_end = P[-1].copy()
+            if start_pt is None:
+                start_pt = P[0].copy()
+            w = rng.uniform(0.5, 2.0, size=n_ctrl)
+            U = _clamped_knots(rng, n_ctrl, p)
+            curves.append([P, w, p, U])
+        curves[-1][0][-1] = start_pt          # closed loop: bit-identical junctions
+        if cw:                                # reverse: curves in reverse order, each reversed
+            curves = [[P[::-1].copy(), w[::-1].copy(), p, (1.0 - U[::-1]).copy()] for P, w, p, U in curves[::-1]]
+        for P, w, p, U in curves:
+            ctrl.append(P); wts.append(w); deg.append(p)
+            coff.append(coff[-1] + len(P))
+            knots.append(U); koff.append(koff[-1] + len(U))
+        lco.append(lco[-1] + len(curves))
+        n_loops += 1
+
+    fids, uvs = [], []
+    for f in range(n_faces):
+        loop((0.5, 0.5), 0.38, 0.04, False)
+        nh = int(rng.integers(0, 3))
+        for h in range(nh):
+            loop((0.5 + (0.17 if h == 0 else -0.17), 0.5), 0.07, 0.005, True)
+        flo.append(n_loops)
+        fids.append(np.full(q_per_face, f))
+        uvs.append(rng.uniform(0, 1, size=(q_per_face, 2)))
+    return dict(
+        ctrl_uv=np.ascontiguousarray(np.concatenate(ctrl)), ctrl_w=np.ascontiguousarray(np.concatenate(wts)),
+        curve_degree=np.asarray(deg, dtype=np.int32), curve_ctrl_off=np.asarray(coff, dtype=np.int32),
+        knots=np.ascontiguousarray(np.concatenate(knots)), curve_knot_off=np.asarray(koff, dtype=np.int32),
+        loop_curve_off=np.asarray(lco, dtype=np.int32), face_loop_off=np.asarray(flo, dtype=np.int32),
+        face_periodic=np.zeros(n_faces, dtype=np.uint8),
+        face_domain=np.tile(np.array([0.0, 1.0, 0.0, 1.0]), (n_faces, 1)),
+        face_id=np.concatenate(fids).astype(np.int32), uv=np.ascontiguousarray(np.concatenate(uvs)),
+        name="NURBS", eps=EPS_FP64, meta=dict(kind="NURBS"))
+
+
 CONFIGS = {"C1": gen_c1, "C2": gen_c2, "C3": gen_c3, "C4": gen_c4, "C5": gen_c5}
 
 

@@ -96,6 +96,44 @@ wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, con
                            const wn_options_t *opts, void *stream, wn_faces_t *out,
                            int32_t *face_status);
 
+/* NURBS p-curves (p-curves are "(rational) Bezier or NURBS curves"
+ * and "B-spline or NURBS curves can always be subdivided into (rational)
+ * Bezier segments").  Curve c has degree curve_degree[c] in 1..5, control
+ * points ctrl_uv[curve_ctrl_off[c] .. curve_ctrl_off[c+1]) ([.][2] float64),
+ * weights ctrl_w (NULL = polynomial B-splines) and the clamped, non-decreasing
+ * knot vector knots[curve_knot_off[c] .. curve_knot_off[c+1]) with
+ * n_knots(c) = n_ctrl(c) + p + 1 and interior multiplicities <= p.  Every
+ * interior knot span of positive length becomes one Bezier segment of the
+ * curve's degree; the curve's two end points are copied bit-exactly (the
+ * junctions of a loop of curves stay bit-continuous).  All arrays are device
+ * pointers; n_ctrl / n_knots are the lengths of ctrl_uv / knots.
+ *
+ * wn_nurbs_to_bezier: the decomposition alone, into caller buffers in the
+ * layout wn_build_faces takes: curve_seg_off [n_curves+1] (segments of curve
+ * c = [curve_seg_off[c], curve_seg_off[c+1])), bez_uv [n_pts][2], bez_w
+ * [n_pts], bez_degree [n_segs].  seg_cap / pt_cap are their capacities
+ * (enough: sum_c (n_ctrl(c) - p_c) segments, sum_c (n_ctrl(c) - p_c)(p_c + 1)
+ * points); *n_segs_out / *n_pts_out [host] receive the sizes (also when the
+ * capacity is too small: WN_ERR_ARG).  Invalid curve data: WN_ERR_GEOM with
+ * the first bad curve in wn_last_error().  Synchronises `stream` once (sizes).
+ *
+ * wn_build_faces_nurbs: wn_build_faces on NURBS loops: loop l is the curves
+ * [loop_curve_off[l], loop_curve_off[l+1]) in order; other arguments and the
+ * handle, options, status and error semantics as for wn_build_faces. */
+wn_status_t wn_nurbs_to_bezier(int32_t n_curves, int32_t n_ctrl, int32_t n_knots, const double *ctrl_uv,
+                               const double *ctrl_w, const int32_t *curve_degree, const int32_t *curve_ctrl_off,
+                               const double *knots, const int32_t *curve_knot_off, int32_t seg_cap,
+                               int32_t pt_cap, int32_t *curve_seg_off, double *bez_uv, double *bez_w,
+                               int32_t *bez_degree, int32_t *n_segs_out, int32_t *n_pts_out, void *stream);
+
+wn_status_t wn_build_faces_nurbs(int32_t n_faces, int32_t n_loops, int32_t n_curves, int32_t n_ctrl,
+                                 int32_t n_knots, const double *ctrl_uv, const double *ctrl_w,
+                                 const int32_t *curve_degree, const int32_t *curve_ctrl_off, const double *knots,
+                                 const int32_t *curve_knot_off, const int32_t *loop_curve_off,
+                                 const int32_t *face_loop_off, const uint8_t *face_periodic,
+                                 const double *face_domain, const wn_options_t *opts, void *stream,
+                                 wn_faces_t *out, int32_t *face_status);
+
 /* Batched query (hot path: bucketing K4 + query kernel K3), fully asynchronous
  * on `stream`; outputs are valid after the stream is synchronised.
  *   n        number of queries (>= 0).

@@ -29,7 +29,8 @@ STATUS = {0: "WN_OK", 1: "WN_ERR_ARG", 2: "WN_ERR_GEOM", 3: "WN_ERR_TOPOLOGY", 4
 FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5: "pairing", 6: "geom"}
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
-           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host", "wn_query_grid"]
+           "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host", "wn_query_grid",
+           "wn_nurbs_to_bezier", "wn_build_faces_nurbs"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "warp_skips", "on_boundary", "span_tests", "warp_records", "_r10", "_r11"]
 
@@ -73,6 +74,10 @@ def load():
         L.wn_query_host.restype = C.c_int
         L.wn_query_host.argtypes = [vp, C.c_int64, vp, vp, vp, vp, C.c_int64, vp]
         L.wn_query_grid.restype = C.c_int
+        L.wn_nurbs_to_bezier.restype = C.c_int
+        L.wn_nurbs_to_bezier.argtypes = [C.c_int32] * 3 + [vp] * 6 + [C.c_int32, C.c_int32] + [vp] * 7
+        L.wn_build_faces_nurbs.restype = C.c_int
+        L.wn_build_faces_nurbs.argtypes = [C.c_int32] * 5 + [vp] * 10 + [vp, vp, vp, vp]
         L.wn_query_grid.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, vp, vp]
         L.wn_faces_info.restype = C.c_int
         L.wn_faces_info.argtypes = [vp, C.POINTER(FacesInfo)]
@@ -179,6 +184,50 @@ class Faces:
                 if t is not None and t.is_cuda:
                     t.record_stream(stream)
         return cls(h, device, nf, opts)
+
+    @classmethod
+    def build_nurbs(cls, ctrl_uv, ctrl_w, curve_degree, curve_ctrl_off, knots, curve_knot_off, loop_curve_off,
+                    face_loop_off, face_periodic, face_domain, eps=0.0, max_depth=0, precision=0, rule=0,
+                    angle_mode=0, strict=True, hierarchy=True, device=None, stream=None):
+        """wn_build_faces_nurbs: faces bounded by loops of clamped NURBS curves
+        (decomposed into rational Bezier segments on the device)."""
+        torch = _torch()
+        L = load()
+        if not torch.cuda.is_available():
+            raise WNError(4, "no CUDA device (libwn has no CPU fallback)")
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        ctrl = _dev(ctrl_uv, torch.float64, device).reshape(-1, 2)
+        w = _dev(ctrl_w, torch.float64, device)
+        deg = _dev(curve_degree, torch.int32, device)
+        co = _dev(curve_ctrl_off, torch.int32, device)
+        kn = _dev(knots, torch.float64, device)
+        ko = _dev(curve_knot_off, torch.int32, device)
+        lco = _dev(loop_curve_off, torch.int32, device)
+        flo = _dev(face_loop_off, torch.int32, device)
+        per = _dev(face_periodic, torch.uint8, device)
+        dom = _dev(face_domain, torch.float64, device).reshape(-1, 4)
+        nf, nl, nc = flo.numel() - 1, lco.numel() - 1, deg.numel()
+        status = torch.zeros(max(nf, 1), dtype=torch.int32, device=device)
+        opts = Options(float(eps), int(max_depth), int(precision), int(rule), int(angle_mode), int(bool(strict)),
+                       int(bool(hierarchy)))
+        h = C.c_void_p()
+        with torch.cuda.device(device):
+            rc = L.wn_build_faces_nurbs(nf, nl, nc, ctrl.shape[0], kn.numel(), _ptr(ctrl), _ptr(w), _ptr(deg),
+                                        _ptr(co), _ptr(kn), _ptr(ko), _ptr(lco), _ptr(flo), _ptr(per), _ptr(dom),
+                                        C.byref(opts), _stream(stream, device), C.byref(h), _ptr(status))
+        if rc != WN_OK:
+            raise WNError(rc, last_error(), status[:nf].cpu().numpy())
+        if stream is not None and hasattr(stream, "cuda_stream"):
+            for t in (ctrl, w, deg, co, kn, ko, lco, flo, per, dom, status):
+                if t is not None and t.is_cuda:
+                    t.record_stream(stream)
+        return cls(h, device, nf, opts)
+
+    @classmethod
+    def from_nurbs_workload(cls, wl, **kw):
+        return cls.build_nurbs(wl["ctrl_uv"], wl["ctrl_w"], wl["curve_degree"], wl["curve_ctrl_off"], wl["knots"],
+                               wl["curve_knot_off"], wl["loop_curve_off"], wl["face_loop_off"],
+                               wl["face_periodic"], wl["face_domain"], **kw)
 
     @classmethod
     def from_workload(cls, wl, **kw):
@@ -343,3 +392,33 @@ def last_query_launches():
 
 def last_build_launches():
     return int(load().wn_last_build_launches())
+
+
+def nurbs_to_bezier(ctrl_uv, ctrl_w, curve_degree, curve_ctrl_off, knots, curve_knot_off, device=None):
+    """wn_nurbs_to_bezier on the device: returns (curve_seg_off, bez_uv, bez_w,
+    bez_degree) as CUDA tensors (the wn_build_faces segment layout)."""
+    torch = _torch()
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    ctrl = _dev(ctrl_uv, torch.float64, device).reshape(-1, 2)
+    w = _dev(ctrl_w, torch.float64, device)
+    deg = _dev(curve_degree, torch.int32, device)
+    co = _dev(curve_ctrl_off, torch.int32, device)
+    kn = _dev(knots, torch.float64, device)
+    ko = _dev(curve_knot_off, torch.int32, device)
+    nc = deg.numel()
+    d = np.asarray(curve_degree, dtype=np.int64)
+    nctrl = np.diff(np.asarray(curve_ctrl_off, dtype=np.int64))
+    seg_cap = int(np.sum(np.maximum(nctrl - d, 0)))
+    pt_cap = int(np.sum(np.maximum(nctrl - d, 0) * (d + 1)))
+    cso = torch.empty(nc + 1, dtype=torch.int32, device=device)
+    bz = torch.empty((max(pt_cap, 1), 2), dtype=torch.float64, device=device)
+    bw = torch.empty(max(pt_cap, 1), dtype=torch.float64, device=device)
+    bd = torch.empty(max(seg_cap, 1), dtype=torch.int32, device=device)
+    ns, npt = C.c_int32(), C.c_int32()
+    with torch.cuda.device(device):
+        rc = load().wn_nurbs_to_bezier(nc, ctrl.shape[0], kn.numel(), _ptr(ctrl), _ptr(w), _ptr(deg), _ptr(co),
+                                       _ptr(kn), _ptr(ko), seg_cap, pt_cap, _ptr(cso), _ptr(bz), _ptr(bw),
+                                       _ptr(bd), C.byref(ns), C.byref(npt), _stream(None, device))
+    if rc != WN_OK:
+        raise WNError(rc, last_error())
+    return cso, bz[:npt.value], bw[:npt.value], bd[:ns.value]

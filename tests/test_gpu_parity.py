@@ -368,3 +368,51 @@ def test_grid_query_c5_full_size_equals_explicit():
     assert torch.equal(rg.flag, re_.flag)
     assert torch.equal(rg.winding, re_.winding)
     faces.close()
+
+
+def test_nurbs_decompose_matches_oracle():
+    """wn_nurbs_to_bezier (device knot insertion) = the oracle's own
+    decomposition: same segment counts and degrees, control points and weights
+    to rounding, bit-exact curve ends and junctions."""
+    wl = G.gen_nurbs(n_faces=60)
+    cso, bz, bw, bd = wn.nurbs_to_bezier(wl["ctrl_uv"], wl["ctrl_w"], wl["curve_degree"], wl["curve_ctrl_off"],
+                                         wl["knots"], wl["curve_knot_off"])
+    torch.cuda.synchronize()
+    cso, bz, bw, bd = cso.cpu().numpy(), bz.cpu().numpy(), bw.cpu().numpy(), bd.cpu().numpy()
+    ref = oracle.nurbs_to_bezier_workload(wl)
+    assert np.array_equal(bd, ref["seg_degree"])
+    assert bz.shape == ref["ctrl_uv"].shape
+    assert np.max(np.abs(bz - ref["ctrl_uv"])) < 1e-12
+    assert np.max(np.abs(bw / ref["ctrl_w"] - 1.0)) < 1e-12
+    # curve ends exact, consecutive segments share their junction bit for bit
+    off = np.concatenate([[0], np.cumsum(bd + 1)])
+    co = wl["curve_ctrl_off"]
+    for c in range(len(wl["curve_degree"])):
+        s0, s1 = cso[c], cso[c + 1]
+        assert np.array_equal(bz[off[s0]], wl["ctrl_uv"][co[c]])
+        assert np.array_equal(bz[off[s1] - 1], wl["ctrl_uv"][co[c + 1] - 1])
+        for s in range(s0, s1 - 1):
+            assert np.array_equal(bz[off[s + 1] - 1], bz[off[s + 1]])
+
+
+@pytest.mark.parametrize("angle_mode,hierarchy", [(0, True), (1, False)])
+def test_nurbs_faces_parity(angle_mode, hierarchy):
+    """wn_build_faces_nurbs + wn_query vs the oracle on its own Bezier form."""
+    wl = G.gen_nurbs(n_faces=150)
+    faces = wn.Faces.from_nurbs_workload(wl, angle_mode=angle_mode, hierarchy=hierarchy)
+    r = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    w, fl = r.winding.cpu().numpy(), r.flag.cpu().numpy()
+    faces.close()
+    _check(oracle.nurbs_to_bezier_workload(wl), w, fl, min_cmp=0.99)
+
+
+def test_nurbs_invalid_knots_rejected():
+    wl = G.gen_nurbs(n_faces=3)
+    bad = dict(wl)
+    kn = wl["knots"].copy()
+    kn[1] = 0.5            # first curve no longer clamped / non-decreasing
+    bad["knots"] = kn
+    with pytest.raises(wn.WNError) as e:
+        wn.Faces.from_nurbs_workload(bad)
+    assert e.value.status == 2

@@ -201,6 +201,26 @@ __device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const dou
   }
 }
 
+// Control-polygon length of a (homogeneous) piece: an upper bound on its arc
+// length (rational de Casteljau cuts corners of the projected polygon).
+template <int N>
+__device__ __forceinline__ double poly_len(const double (&a)[N + 1], const double (&b)[N + 1],
+                                           const double (&c)[N + 1]) {
+  // (plain sqrt: coordinates are far from overflow; rounding ~1e-16 relative is
+  // covered by the R5 margins like every other bound)
+  double r = 1.0 / c[0];
+  double L = 0.0, x0 = a[0] * r, y0 = b[0] * r;
+#pragma unroll
+  for (int i = 1; i <= N; ++i) {
+    r = 1.0 / c[i];
+    const double x1 = a[i] * r, y1 = b[i] * r;
+    L += sqrt((x1 - x0) * (x1 - x0) + (y1 - y0) * (y1 - y0));
+    x0 = x1;
+    y0 = y1;
+  }
+  return L;
+}
+
 // One thread per segment (taken in degree-sorted order so that a warp runs one
 // degree variant): loads its control points once and computes B, S0 and the 8
 // piece bounds, written as one 80-B record prep[s] (five 16-B stores), which
@@ -227,16 +247,19 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     return;
   }
   const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
-  o2[0] = make_double2(B, fmin(B, lpoly));
+  double l8 = 0.0;   // sum of the 8 dyadic pieces' polygon lengths >= arc length (R9, tighter)
 #pragma unroll 1
   for (int q = 0; q < 8; q += 2) {
     double a[N + 1], bb[N + 1], c[N + 1];
     dyadic_piece<N>(X, Y, W, q, a, bb, c);
     const double b0 = 8.0 * hodo_bound<N>(a, bb, c);
+    l8 += poly_len<N>(a, bb, c);
     dyadic_piece<N>(X, Y, W, q + 1, a, bb, c);
     const double b1 = 8.0 * hodo_bound<N>(a, bb, c);
+    l8 += poly_len<N>(a, bb, c);
     o2[1 + q / 2] = make_double2(b0, b1);
   }
+  o2[0] = make_double2(B, fmin(B, fmin(lpoly, l8)));
 }
 
 __global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
@@ -511,7 +534,7 @@ __device__ void put_group<double>(Hot<double> *H, int r, double xmin, double ymi
   h.fy = f_dn(ymin);
   h.fs = f_up(xmax);
   h.meta = meta;
-  h.x = ymax;
+  h.x = __hiloint2double(0, __float_as_int(f_up(ymax)));   // fp32 ymax (rounded up) in the low word
   h.y = 0.0;
   H[r] = h;
 }
@@ -554,8 +577,11 @@ __device__ __forceinline__ void st2<float>(float *p, float a, float b) {
 // per-level SPAN emission reads shared memory instead of a chain of global loads.
 constexpr int EMIT_WARPS = 4;
 constexpr int EMIT_STAGE = 256;
+#ifndef EMIT_MINB
+#define EMIT_MINB 8
+#endif
 template <typename R>
-__global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
+__global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
                        const int32_t *__restrict__ loop_off,
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
@@ -636,22 +662,16 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
     const int n = deg[s];
     const int o = coff[s];
     const int2 k = shift[s];
-    // register-resident control points (unrolled over the maximum degree)
-    double px[6], py[6], pxn = 0.0, pyn = 0.0;
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      px[j] = py[j] = 0.0;
-      if (j <= n) {
-        px[j] = X(ctrl[2 * (o + j)], k.x);
-        py[j] = Y(ctrl[2 * (o + j) + 1], k.y);
-      }
-      if (j == n) { pxn = px[j]; pyn = py[j]; }
-    }
+    // end points (the interior control points are re-read pair by pair below,
+    // keeping few values live: occupancy of this latency-bound scatter)
+    // (scalar loads: the caller's ctrl_uv need only be 8-B aligned)
+    const double px0 = X(ctrl[2 * o], k.x), py0 = Y(ctrl[2 * o + 1], k.y);
+    const double pxn = X(ctrl[2 * (o + n)], k.x), pyn = Y(ctrl[2 * (o + n) + 1], k.y);
     int r;
     if (!tree) {
       r = r_first + idx + nb;
-      if (s == s0) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVE | fa);
-      else if (bk) put_rec<R>(hot, r - 1, px[0], py[0], 0.0, K_MOVEG | fa);
+      if (s == s0) put_rec<R>(hot, r - 1, px0, py0, 0.0, K_MOVE | fa);
+      else if (bk) put_rec<R>(hot, r - 1, px0, py0, 0.0, K_MOVEG | fa);
     } else {
       // path hierarchy: each chain of m segments becomes a pre-order
       // binary tree of 2m-1 records (SPAN nodes over segment ranges, SEG leaves);
@@ -660,8 +680,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
       const int j = idx - ch.x;
       int a = 0, bnd = ch.y - 1, off = r_first + 2 * ch.x;
       if (j == 0) {
-        if (s == s0) put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVE | fa);
-        else put_rec<R>(hot, off - 1, px[0], py[0], 0.0, K_MOVEG | fa);
+        if (s == s0) put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVE | fa);
+        else put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVEG | fa);
       }
       bool omit = omit_root && ch.y >= 2;                // closed loop: no root SPAN
       while (a < bnd) {
@@ -707,7 +727,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
     put_rec<R>(hot, r, pxn, pyn, S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
     // cold record written field pair by field pair (vector stores, no local copy)
     Cold<R> *Cp = cold + G.cold_off + idx;
-    st2<R>(&Cp->f0x, (R)px[0], (R)py[0]);
+    st2<R>(&Cp->f0x, (R)px0, (R)py0);
     st2<R>(&Cp->f1x, (R)pxn, (R)pyn);
     st2<R>(&Cp->B, Br, (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M);
     *reinterpret_cast<int2 *>(&Cp->n) = make_int2(n, 0);
@@ -718,24 +738,25 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS) k_emit(int32_t n_groups, cons
       const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.y)) * (1.0 + rel);
       st2<R>(&Cp->Bq[q], (sizeof(R) == 4) ? (R)f_up(b0) : (R)b0, (sizeof(R) == 4) ? (R)f_up(b1) : (R)b1);
     }
-    R cxv[6], cyv[6], cwv[6];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      if (j <= n) {
-        const double wj = wts ? wts[o + j] : 1.0;
-        const double cw = binom5(n, j) * wj;
-        cxv[j] = (R)(cw * px[j]);
-        cyv[j] = (R)(cw * py[j]);
-        cwv[j] = (R)cw;
-      } else {
-        cxv[j] = cyv[j] = cwv[j] = (R)0;
-      }
-    }
+    // homogeneous Horner coefficients c_j = C(n,j) w_j (x_j, y_j, 1), zero above n
 #pragma unroll
     for (int j = 0; j < 6; j += 2) {
-      st2<R>(&Cp->cx[j], cxv[j], cxv[j + 1]);
-      st2<R>(&Cp->cy[j], cyv[j], cyv[j + 1]);
-      st2<R>(&Cp->cw[j], cwv[j], cwv[j + 1]);
+      R cx2[2], cy2[2], cw2[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jj = j + h;
+        cx2[h] = cy2[h] = cw2[h] = (R)0;
+        if (jj <= n) {
+          const double wj = wts ? wts[o + jj] : 1.0;
+          const double cw = binom5(n, jj) * wj;
+          cx2[h] = (R)(cw * X(ctrl[2 * (o + jj)], k.x));
+          cy2[h] = (R)(cw * Y(ctrl[2 * (o + jj) + 1], k.y));
+          cw2[h] = (R)cw;
+        }
+      }
+      st2<R>(&Cp->cx[j], cx2[0], cx2[1]);
+      st2<R>(&Cp->cy[j], cy2[0], cy2[1]);
+      st2<R>(&Cp->cw[j], cw2[0], cw2[1]);
     }
   }
   if (lane == 0) {

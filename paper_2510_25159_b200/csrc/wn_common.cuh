@@ -22,11 +22,11 @@ namespace wn {
 // hot record kinds (meta & 0xF) and flag bits (meta bits 4..7); meta >> 8 = aux
 // ---------------------------------------------------------------------------
 enum : uint32_t {
-  K_SEG = 1,     // (a,b) = F1, c = root span S0 (Eq. 1 with R5 margin); aux = face-local cold index
-  K_SPAN = 2,    // path-hierarchy node: (x,y) = end of the run, span = sum of its S0; aux = subtree records
+  K_SEG = 0,     // (a,b) = F1, c = root span S0 (Eq. 1 with R5 margin); aux = face-local cold index
+  K_SPAN = 1,    // path-hierarchy node: (x,y) = end of the run, span = sum of its S0; aux = subtree records
   K_MOVE = 3,    // (a,b) = chain start; sets group start A and the previous point
   K_MOVEG = 4,   // (a,b) = next chain start after a gap; crossing mode adds the gap terms
-  K_GROUP = 5,   // cull header: bbox (float4 in a,b for fp64; a,b,c + next record for fp32); aux = records to skip
+  K_GROUP = 5,   // cull header: box rounded outward (fp64 records: fp32 xmin,ymin,xmax + fp32 ymax in x; fp32: half maxima in c); aux = records to skip
   K_LINE = 6,    // a = line coordinate; omega(p,L) = +-1/2
   K_XCH = 7,     // extended copy closing (crossing mode): -c(A -> Z)
   K_NCH = 8,     // extended copy closing (angle mode): -omega(p, A, Z)  (Eq. 5 chord)
@@ -34,7 +34,8 @@ enum : uint32_t {
   K_SLINE = 10   // (x,y) = point of a line along v = (p Tu, q Tv), aux = (p, q) as two signed 12-bit
                  // fields: omega(p,L) = +-1/2 for the bands of a general class (Prop. 2)
 };
-// SEG and SPAN (the records of the inner loop) are kinds 1 and 2: one compare
+// SEG and SPAN (the records of the inner loop) are kinds 0 and 1: one bit test
+// ((meta & 0xE) == 0) selects them, one more (meta & 1) tells them apart
 constexpr uint32_t F_ANGLE = 1u << 4;   // literal atan2 chord angles (angle_mode = 1)
 constexpr uint32_t F_AXISV = 1u << 5;   // LINE parallel to v: test the u coordinate
 constexpr uint32_t F_GE = 1u << 6;      // LINE: left iff q >= c (else q <= c)
@@ -53,7 +54,7 @@ template <>
 struct __align__(32) Hot<double> {
   float fx, fy, fs;   // fp32 point (nearest) and filter span (rounded up, margins included)
   uint32_t meta;
-  double x, y;        // exact point (SEG/MOVE/MOVEG), line coordinate (LINE: x), GROUP: ymax in x
+  double x, y;        // exact point (SEG/MOVE/MOVEG), line coordinate (LINE: x), GROUP: fp32 ymax (up) in x's low word
 };
 template <>
 struct __align__(16) Hot<float> {

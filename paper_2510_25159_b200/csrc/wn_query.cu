@@ -101,6 +101,7 @@ struct QParams {
   const int32_t *grid_face;
   int64_t grid_n;
   int32_t grid_nu, grid_nv;
+  int32_t grid_blk;        // > 0: warp = grid_blk x (32 / grid_blk) cell block (see k_phase1)
 };
 
 // Cell-centred grid point (iu + 1/2) * (hi - lo) / n + lo, rounded step by step
@@ -263,7 +264,10 @@ template <typename R>
 __device__ __forceinline__ bool group_out(const Hot<R> &h, double px, double py);
 template <>
 __device__ __forceinline__ bool group_out<double>(const Hot<double> &h, double px, double py) {
-  return !((double)h.fx <= px && px <= (double)h.fs && (double)h.fy <= py && py <= h.x);
+  // fp32 box rounded outward vs the fp32-rounded point: RN is monotone, so a
+  // point inside the exact box is never culled (exact-conservative)
+  const float x = (float)px, y = (float)py, ymax = __int_as_float(__double2loint(h.x));
+  return !(h.fx <= x && x <= h.fs && h.fy <= y && y <= ymax);
 }
 template <>
 __device__ __forceinline__ bool group_out<float>(const Hot<float> &h, double px, double py) {
@@ -309,13 +313,14 @@ struct HotView<float> {
   }
 };
 
-__device__ __forceinline__ bool group_out_v(const HotView<double> &h, double px, double py) {
-  return !((double)h.fx <= px && px <= (double)h.fs && (double)h.fy <= py && py <= h.x);
+__device__ __forceinline__ bool group_out_v(const HotView<double> &h, float pxf, float pyf) {
+  // as group_out<double>: fp32 comparisons, exact-conservative
+  const float ymax = __int_as_float(__double2loint(h.x));
+  return !(h.fx <= pxf && pxf <= h.fs && h.fy <= pyf && pyf <= ymax);
 }
-__device__ __forceinline__ bool group_out_v(const HotView<float> &h, double px, double py) {
+__device__ __forceinline__ bool group_out_v(const HotView<float> &h, float x, float y) {
   uint32_t c = __float_as_uint(h.fs);
   const __half2 hi = *reinterpret_cast<const __half2 *>(&c);
-  const float x = (float)px, y = (float)py;
   return !(h.fx <= x && x <= __half2float(hi.x) && h.fy <= y && y <= __half2float(hi.y));
 }
 
@@ -447,16 +452,27 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     pend &= ~4;
   };
 
+  // query of this thread within a sub-tile.  Implicit grids whose rows tile a
+  // sub-tile (grid_blk = 32 / rows-per-sub-tile > 0) give each warp a compact
+  // grid_blk x (32 / grid_blk) block of cells instead of a run of one row: the
+  // warp's queries then lie close together, so they agree more often on
+  // pruning a hierarchy span or culling a group (fewer warp-level descents).
+  int lt = t;
+  if constexpr (GRID) {
+    const int bw = P.grid_blk;
+    if (bw > 0) lt = (lane / bw) * P.grid_nu + warp * bw + lane % bw;
+  }
+
   // one unit = up to QU queries of face f, processed QT at a time
   for (int sub = 0; sub < T.qcnt; sub += QT) {
-    bool valid = sub + t < T.qcnt;
-    const int32_t pos = (int32_t)(T.qbeg + sub) + t;
+    bool valid = sub + lt < T.qcnt;
+    const int32_t pos = (int32_t)(T.qbeg + sub) + lt;
     const int32_t qi = valid ? (unsorted ? P.perm[pos] : pos) : 0;
     double px = 0.0, py = 0.0;
     if (valid) {
       double u, v;
       if constexpr (GRID) {
-        const int loc = s_gloc0 + sub + t;
+        const int loc = s_gloc0 + sub + lt;
         const int iv = loc / P.grid_nu, iu = loc - iv * P.grid_nu;
         u = __dadd_rn(s_grid[0], __dmul_rn((double)iu + 0.5, s_grid[2]));   // = grid_coord(), bit for bit
         v = __dadd_rn(s_grid[1], __dmul_rn((double)iv + 0.5, s_grid[3]));
@@ -505,14 +521,15 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         }
       }
       const int ce = cb + cn;
+      unsigned sp = sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>);   // shared address of record gr
       while (gr < ce) {
         HotView<R> h;
-        h.load(sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>));
+        h.load(sp);
         const uint32_t meta = h.meta;
         const uint32_t kind = meta & 0xFu;
         const bool act = valid && gr >= skip_end;
         if (COUNT && lane == 0) ++c_rec;
-        if (__builtin_expect(kind - K_SEG < 2u, 1)) {   // SEG or SPAN
+        if (__builtin_expect((meta & 0xEu) == 0u, 1)) {   // SEG (0) or SPAN (1)
           // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
           // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
           // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
@@ -529,7 +546,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             df = sqrtf(dx * dx + dy * dy);
           }
           const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
-          if (kind == K_SPAN) {
+          if (meta & 1u) {                                       // K_SPAN
             if (COUNT && act) ++c_span;
             // descend unless every active lane prunes the whole run
             const bool descend = act && !pr;
@@ -543,6 +560,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
               }
               if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
               gr += (int)(meta >> 8);
+              sp += (meta >> 8) * (unsigned)sizeof(Hot<R>);
               if (COUNT && lane == 0) ++c_cull;
             } else if (act && pr) {
               // this lane prunes the run: chord now, inactive for the subtree
@@ -611,10 +629,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           up = F64 ? (h.y >= py) : (h.fy >= pyf);
         } else if (kind == K_GROUP) {
           // copy-group / closed-loop cull: p outside the group's box => exactly 0
-          const bool out = !act || group_out_v(h, px, py);
+          const bool out = !act || group_out_v(h, pxf, pyf);
           const int skip = (int)(meta >> 8);
           if (__all_sync(0xffffffffu, out)) {
             gr += skip;
+            sp += (unsigned)skip * (unsigned)sizeof(Hot<R>);
             if (COUNT && lane == 0) ++c_cull;
           } else if (out && act) {
             skip_end = gr + 1 + skip;
@@ -641,6 +660,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           }
         }
         ++gr;
+        sp += (unsigned)sizeof(Hot<R>);
       }
       // all warps done with this chunk before it is overwritten (multi-chunk faces)
       if (!single && (ce < nrec || sub + QT < T.qcnt)) __syncthreads();
@@ -1193,6 +1213,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.grid_face = nullptr;
   P.grid_n = 0;
   P.grid_nu = P.grid_nv = 0;
+  P.grid_blk = 0;
   {
     const wn_status_t rc = launch_k3<R>(F, P, n, face_id, max_tiles, st, launches);
     if (rc != WN_OK) return rc;
@@ -1276,6 +1297,11 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   P.grid_n = G;
   P.grid_nu = nu;
   P.grid_nv = nv;
+  // 2-D warp blocks when a sub-tile is R whole rows (R = QT / nu) and a block
+  // of R rows x (32 / R) columns fits: units start at multiples of QT
+  P.grid_blk = 0;
+  if (nu > 0 && nu <= QT && QT % nu == 0 && QT / nu <= 32 && !(std::getenv("WN_GRID_LINEAR") && *std::getenv("WN_GRID_LINEAR")))
+    P.grid_blk = 32 / (QT / nu);
   {
     const wn_status_t rc = launch_k3<R>(F, P, n, nullptr, max_tiles, st, launches);
     if (rc != WN_OK) return rc;

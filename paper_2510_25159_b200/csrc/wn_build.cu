@@ -1150,7 +1150,8 @@ __global__ void k_plan_count(int32_t n_faces, int32_t n_loops, const int32_t *__
                              const double *__restrict__ dom, const LoopInfo *__restrict__ L, int angle, int strict,
                              int tree, int fp32, const int *__restrict__ pair_beta, const int *__restrict__ pair_s,
                              int32_t *__restrict__ status, uint8_t *__restrict__ fper, double *__restrict__ fdom,
-                             double *__restrict__ fM, int4 *__restrict__ cnt, uint32_t *__restrict__ okey,
+                             double *__restrict__ fM, float4 *__restrict__ fbox, int4 *__restrict__ cnt,
+                             uint32_t *__restrict__ okey,
                              int32_t *__restrict__ oval, BuildSummary *__restrict__ sum) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n_faces) return;
@@ -1163,6 +1164,20 @@ __global__ void k_plan_count(int32_t n_faces, int32_t n_loops, const int32_t *__
   fper[f] = C.per;
   fdom[4 * f] = C.u0; fdom[4 * f + 1] = C.Tu; fdom[4 * f + 2] = C.v0; fdom[4 * f + 3] = C.Tv;
   fM[f] = C.M;
+  {
+    // box of the queries that can be inside: the loops' boxes, the base tile
+    // on periodic axes (queries are reduced into it); only a regrouping key
+    float x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+    for (int l = l0; l < l1; ++l) {
+      if (L[l].nseg == 0) continue;
+      x0 = fminf(x0, (float)L[l].bb[0]); y0 = fminf(y0, (float)L[l].bb[1]);
+      x1 = fmaxf(x1, (float)L[l].bb[2]); y1 = fmaxf(y1, (float)L[l].bb[3]);
+    }
+    if (C.per & 1) { x0 = (float)C.u0; x1 = (float)(C.u0 + C.Tu); }
+    if (C.per & 2) { y0 = (float)C.v0; y1 = (float)(C.v0 + C.Tv); }
+    if (!(x1 > x0) || !(y1 > y0) || !isfinite(x1 - x0) || !isfinite(y1 - y0)) x0 = y0 = x1 = y1 = 0.f;
+    fbox[f] = make_float4(x0, y0, x1, y1);
+  }
   CountSink S;
   if (st) {
     atomicOr(&sum->bad, 1);
@@ -1320,7 +1335,7 @@ void free_handle(wn_faces_t F) {
   // (its build or its latest query, on whatever stream that ran)
   if (F->last_use) cudaStreamWaitEvent(0, F->last_use, 0);
   void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
-                F->face_per, F->face_ok, F->face_M, F->counters};
+                F->face_per, F->face_ok, F->face_M, F->face_box, F->counters};
   for (void *p : ps)
     if (p) cache_free(p, 0);
   if (F->last_use) cudaEventDestroy(F->last_use);
@@ -1380,6 +1395,8 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   WN_CUDA(cache_alloc((void **)&F->face_per, std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_ok, std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->face_box, sizeof(float4) * std::max(nf, 1), st));
+  WN_CUDA(cudaMemsetAsync(F->face_box, 0, sizeof(float4) * std::max(nf, 1), st));   // probes: no regrouping
   WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st));
   F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
   int32_t maxr = 0;
@@ -1557,6 +1574,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(cache_alloc((void **)&F->face_per, nf1, st2));
   WN_CUDA(cache_alloc((void **)&F->face_ok, nf1, st2));
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * nf1, st2));
+  WN_CUDA(cache_alloc((void **)&F->face_box, sizeof(float4) * nf1, st2));
   WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st2));
   int32_t *d_status = face_status;
   if (!d_status) WN_CUDA(D2.alloc(&d_status, nf1));
@@ -1585,7 +1603,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       k_plan_count<<<(n_faces + 127) / 128, 128, 0, st2>>>(
           n_faces, n_loops, face_loop_off, face_periodic, face_domain, B.info, angle ? 1 : 0, O.strict ? 1 : 0,
           O.hierarchy ? 1 : 0, fp32 ? 1 : 0, pair_beta, pair_s, d_status, F->face_per, F->face_dom, F->face_M,
-          d_cnt4, d_okey, d_oval, d_sum);
+          F->face_box, d_cnt4, d_okey, d_oval, d_sum);
       k_plan_scan<<<1, PLAN_SCAN_T, 0, st2>>>(n_faces, d_cnt4, d_off4, F->face_rec_off, F->face_cold_off, d_sum);
       WN_CUDA(cub::DeviceRadixSort::SortPairs(d_sort_tmp, sort_tmp, d_okey, d_okey2, d_oval, F->face_order, n_faces,
                                               0, 32, st2));

@@ -203,6 +203,7 @@ struct wn_faces_s {
   uint8_t *face_per = nullptr;     // [n_faces]
   uint8_t *face_ok = nullptr;      // [n_faces]
   double *face_M = nullptr;        // [n_faces] absolute margin M (R5) per face
+  float4 *face_box = nullptr;      // [n_faces] box holding every query that can be inside (query regrouping)
   unsigned long long *counters = nullptr;  // [8]
   int counters_on = 0;
   cudaEvent_t last_use = nullptr;    // recorded after the build and after every query

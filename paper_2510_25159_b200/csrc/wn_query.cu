@@ -102,6 +102,10 @@ struct QParams {
   int64_t grid_n;
   int32_t grid_nu, grid_nv;
   int32_t grid_blk;        // > 0: warp = grid_blk x (32 / grid_blk) cell block (see k_phase1)
+  const float4 *face_box;  // [n_faces] box of the face's queries that can be inside (spatial regrouping)
+  int32_t spatial;         // explicit batches: regroup each unit's queries in Morton order
+  int32_t *sorder;         // [n] regrouped query order, unit by unit (positions of the tile ranges)
+  int32_t *skey;           // [n] scratch of the regrouping (cell key << 12 | rank in cell)
 };
 
 // Cell-centred grid point (iu + 1/2) * (hi - lo) / n + lo, rounded step by step
@@ -353,6 +357,8 @@ constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classif
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
+constexpr int SP_BINS = 1024;   // Morton cells of the spatial regrouping (32 x 32)
+constexpr int SP_COHERENT = 24; // mean warp-footprint perimeter (cells) above which a unit is regrouped
 
 #ifndef WN_P1_MINB
 #define WN_P1_MINB 4
@@ -398,6 +404,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   const int cold0 = P.face_cold_off[f];
   // implicit grid: a unit lies inside one grid (units are cut per grid), so the
   // grid index, its box and the cell steps are per-CTA values
+  // spatial regrouping of explicit units (see below)
+  __shared__ uint32_t s_hist[SP_BINS / 2];   // 16-bit counters, two per word
+  __shared__ int s_wsum[NWARP];
+  __shared__ int s_coh[2];                   // coherence probe: perimeter sum, warps
+  if (t < 2) s_coh[t] = 0;
   // (kept in shared memory, not in registers across the record loop)
   __shared__ double s_grid[4];   // u_lo, v_lo, (u_hi - u_lo) / nu, (v_hi - v_lo) / nv
   __shared__ int s_gloc0;
@@ -452,6 +463,120 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     pend &= ~4;
   };
 
+  // Spatial regrouping (explicit batches): the unit's queries are put in
+  // Morton order of a 32 x 32 cell grid over the face's box (a counting sort
+  // in shared memory, once per unit), so that each warp takes 32 queries
+  // that lie close together and agrees more often on pruning a span or
+  // culling a group.  A permutation of whole queries: no value changes.  The
+  // order goes to a per-unit scratch range (L2-resident), read per sub-tile.
+  bool spatial = false;
+  if constexpr (!GRID) {
+    spatial = P.spatial && T.qcnt > 32;
+    const float4 fb = spatial ? P.face_box[f] : make_float4(0.f, 0.f, 0.f, 0.f);
+    {
+      const float sx = fb.z > fb.x ? 32.f / (fb.z - fb.x) : 0.f, sy = fb.w > fb.y ? 32.f / (fb.w - fb.y) : 0.f;
+      auto key_of = [&](int i, int32_t &qi_out) {
+        const int32_t pos = (int32_t)T.qbeg + i;
+        const int32_t qi = unsorted ? P.perm[pos] : pos;
+        qi_out = qi;
+        const double u = P.uv[2 * (int64_t)qi], v = P.uv[2 * (int64_t)qi + 1];
+        if (!isfinite(u) || !isfinite(v)) return SP_BINS - 1;
+        const double ur = (per & 1) ? reduce_coord(u, dom[0], dom[1]) : u;
+        const double vr = (per & 2) ? reduce_coord(v, dom[2], dom[3]) : v;
+        const int cx = min(max(__float2int_rd(((float)ur - fb.x) * sx), 0), 31);
+        const int cy = min(max(__float2int_rd(((float)vr - fb.y) * sy), 0), 31);
+        int mx = cx, my = cy;   // interleave 5 + 5 bits
+        mx = (mx | (mx << 4)) & 0x0F0F; mx = (mx | (mx << 2)) & 0x3333; mx = (mx | (mx << 1)) & 0x5555;
+        my = (my | (my << 4)) & 0x0F0F; my = (my | (my << 2)) & 0x3333; my = (my | (my << 1)) & 0x5555;
+        return mx | (my << 1);
+      };
+      if (spatial) {
+      // Coherence probe on the first QT queries in their given order: the
+      // mean perimeter (in cells) of a warp's footprint.  Already coherent
+      // input (e.g. row-major grids: a warp covers a short run of one row) is
+      // left in its order -- regrouping it would cost more than it saves.
+      {
+        int cx = 0, cy = 0;
+        bool ok = t < T.qcnt;
+        if (ok) {
+          int32_t q_;
+          const int k = key_of(t, q_);
+          // cell coordinates back from the Morton key
+          int a = k & 0x5555, b = (k >> 1) & 0x5555;
+          a = (a | (a >> 1)) & 0x3333; a = (a | (a >> 2)) & 0x0F0F; a = (a | (a >> 4)) & 0x00FF;
+          b = (b | (b >> 1)) & 0x3333; b = (b | (b >> 2)) & 0x0F0F; b = (b | (b >> 4)) & 0x00FF;
+          cx = a;
+          cy = b;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (m) {
+          const unsigned x0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cx : 255u);
+          const unsigned x1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cx : 0u);
+          const unsigned y0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cy : 255u);
+          const unsigned y1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cy : 0u);
+          if (lane == 0) {
+            atomicAdd(&s_coh[0], (int)((x1 - x0) + (y1 - y0)));
+            atomicAdd(&s_coh[1], 1);
+          }
+        }
+      }
+      for (int i = t; i < SP_BINS / 2; i += NTH) s_hist[i] = 0;
+      __syncthreads();
+      spatial = s_coh[0] > SP_COHERENT * s_coh[1];
+      }
+    if (spatial) {
+      // pass 1: key and rank within its cell -> scratch (key << 12 | rank)
+#pragma unroll 4
+      for (int i = t; i < T.qcnt; i += NTH) {
+        int32_t q_;
+        const int k = key_of(i, q_);
+        const uint32_t old = atomicAdd(&s_hist[k >> 1], 1u << (16 * (k & 1)));
+        P.skey[T.qbeg + i] = (k << 12) | (int)((old >> (16 * (k & 1))) & 0xFFFu);
+      }
+      __syncthreads();
+      // exclusive scan of the SP_BINS counters: each thread owns SP_BINS / NTH
+      constexpr int PER = SP_BINS / NTH;   // bins per thread (even)
+      uint32_t c[PER];
+      int tot = 0;
+#pragma unroll
+      for (int j = 0; j < PER; j += 2) {
+        const uint32_t wv = s_hist[(t * PER + j) >> 1];
+        c[j] = wv & 0xFFFFu;
+        c[j + 1] = wv >> 16;
+        tot += (int)(c[j] + c[j + 1]);
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int nb = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nb;
+      }
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int base = incl - tot;
+#pragma unroll
+      for (int w2 = 0; w2 < NWARP; ++w2) base += (w2 < warp) ? s_wsum[w2] : 0;
+#pragma unroll
+      for (int j = 0; j < PER; j += 2) {
+        const uint32_t o0 = (uint32_t)base, o1 = (uint32_t)base + c[j];
+        base += (int)(c[j] + c[j + 1]);
+        s_hist[(t * PER + j) >> 1] = o0 | (o1 << 16);      // offsets <= 4096: no carry
+      }
+      __syncthreads();
+      // pass 2: position = cell offset + rank in cell (no atomics, no reload of uv)
+#pragma unroll 4
+      for (int i = t; i < T.qcnt; i += NTH) {
+        const int32_t pos = (int32_t)T.qbeg + i;
+        const int kr = P.skey[pos];
+        const int k = kr >> 12;
+        const uint32_t off = (s_hist[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+        P.sorder[T.qbeg + (int)off + (kr & 0xFFF)] = unsorted ? P.perm[pos] : pos;
+      }
+      __syncthreads();   // the order (global, this CTA's range) is visible to the block
+    }
+    }
+  }
+
   // query of this thread within a sub-tile.  Implicit grids whose rows tile a
   // sub-tile (grid_blk = 32 / rows-per-sub-tile > 0) give each warp a compact
   // grid_blk x (32 / grid_blk) block of cells instead of a run of one row: the
@@ -467,7 +592,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   for (int sub = 0; sub < T.qcnt; sub += QT) {
     bool valid = sub + lt < T.qcnt;
     const int32_t pos = (int32_t)(T.qbeg + sub) + lt;
-    const int32_t qi = valid ? (unsorted ? P.perm[pos] : pos) : 0;
+    int32_t qi = valid ? (spatial ? P.sorder[pos] : unsorted ? P.perm[pos] : pos) : 0;
     double px = 0.0, py = 0.0;
     if (valid) {
       double u, v;
@@ -1155,6 +1280,8 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const size_t o_toff = carve(sizeof(int32_t) * (nf + 1));
   const size_t o_tiles = carve(sizeof(Tile) * (size_t)max_tiles);
   const size_t o_perm = carve(sizeof(int32_t) * (size_t)n);
+  const size_t o_sord = carve(sizeof(int32_t) * (size_t)n);
+  const size_t o_skey = carve(sizeof(int32_t) * (size_t)n);
   const size_t o_hq = carve(sizeof(HardEntry) * (size_t)hq_cap);
   const size_t o_tmp = carve(tmp);
   char *base = nullptr;
@@ -1214,6 +1341,10 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.grid_n = 0;
   P.grid_nu = P.grid_nv = 0;
   P.grid_blk = 0;
+  P.face_box = F->face_box;
+  P.spatial = (F->face_box != nullptr && !(std::getenv("WN_NO_SPATIAL") && *std::getenv("WN_NO_SPATIAL"))) ? 1 : 0;
+  P.sorder = (int32_t *)(base + o_sord);
+  P.skey = (int32_t *)(base + o_skey);
   {
     const wn_status_t rc = launch_k3<R>(F, P, n, face_id, max_tiles, st, launches);
     if (rc != WN_OK) return rc;
@@ -1297,6 +1428,10 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   P.grid_n = G;
   P.grid_nu = nu;
   P.grid_nv = nv;
+  P.face_box = F->face_box;
+  P.spatial = 0;
+  P.sorder = nullptr;
+  P.skey = nullptr;
   // 2-D warp blocks when a sub-tile is R whole rows (R = QT / nu) and a block
   // of R rows x (32 / R) columns fits: units start at multiples of QT
   P.grid_blk = 0;

@@ -416,3 +416,20 @@ def test_nurbs_invalid_knots_rejected():
     with pytest.raises(wn.WNError) as e:
         wn.Faces.from_nurbs_workload(bad)
     assert e.value.status == 2
+
+
+def test_spatial_regrouping_is_a_permutation(monkeypatch):
+    """The in-kernel Morton regrouping of a unit's queries (random-order batch:
+    it engages) permutes whole queries: results are bit-identical to the
+    given order (crossing mode: integer sums)."""
+    wl = G.gen_c2(n_queries=200_000)
+    faces = wn.Faces.from_workload(wl)
+    r1 = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    monkeypatch.setenv("WN_NO_SPATIAL", "1")
+    r2 = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    faces.close()
+    assert torch.equal(r1.flag, r2.flag)
+    same = (r1.winding == r2.winding) | (torch.isnan(r1.winding) & torch.isnan(r2.winding))
+    assert bool(same.all())

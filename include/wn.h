@@ -211,10 +211,12 @@ wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, double *
                           int64_t *k3_launches /* [host] */);
 
 /* K1 segment prep on its own (diagnostics / tests): for every segment writes
- * out[s][10] = {B, S0, Bq[0..7]}: the derivative bound of Lemma 1 (P:335-345,
- * App. A.1, reading R29), the root span S0 = min(B, control-polygon
- * length) (R9) and the bounds of the 8 dyadic pieces [q/8,(q+1)/8] (t-units),
- * without margins.  Device pointers; synchronises the stream. */
+ * out[s][18] = {B, S0, Bq[0..7], Lq[0..7]}: the derivative bound of Lemma 1
+ * (App. A.1, reading R29), the root span S0 = min(B,
+ * control-polygon length, sum of Lq) (R9), the derivative bounds of the 8
+ * dyadic pieces [q/8,(q+1)/8] (t-units) and their control-polygon lengths
+ * (arc-length bounds), without margins.  Device pointers; synchronises the
+ * stream. */
 wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, const double *ctrl_w,
                             const int32_t *seg_degree, double *out, void *stream);
 

@@ -373,13 +373,13 @@ def freed_timing():
 
 
 def segment_prep(ctrl_uv, ctrl_w, seg_degree, device=None, stream=None):
-    """K1 alone: [n_segs, 10] = (B, S0, Bq[8]) per segment (no margins)."""
+    """K1 alone: [n_segs, 18] = (B, S0, Bq[8], Lq[8]) per segment (no margins)."""
     torch = _torch()
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     ctrl = _dev(ctrl_uv, torch.float64, device).reshape(-1, 2)
     w = _dev(ctrl_w, torch.float64, device)
     deg = _dev(seg_degree, torch.int32, device)
-    out = torch.empty((deg.numel(), 10), dtype=torch.float64, device=device)
+    out = torch.empty((deg.numel(), 18), dtype=torch.float64, device=device)
     rc = load().wn_segment_prep(deg.numel(), _ptr(ctrl), _ptr(w), _ptr(deg), _ptr(out), _stream(stream, device))
     if rc != WN_OK:
         raise WNError(rc, last_error())

@@ -223,7 +223,8 @@ __device__ __forceinline__ double poly_len(const double (&a)[N + 1], const doubl
 
 // One thread per segment (taken in degree-sorted order so that a warp runs one
 // degree variant): loads its control points once and computes B, S0 and the 8
-// piece bounds, written as one 80-B record prep[s] (five 16-B stores), which
+// piece bounds and piece polygon lengths, written as one 144-B record prep[s]
+// (nine 16-B stores), which
 // k_emit then reads coalesced in segment order.
 template <int N>
 __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o,
@@ -243,7 +244,7 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
   double2 *o2 = reinterpret_cast<double2 *>(out);
   if (err) {
 #pragma unroll
-    for (int k = 0; k < 5; ++k) o2[k] = make_double2(0.0, 0.0);
+    for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
     return;
   }
   const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
@@ -253,11 +254,13 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     double a[N + 1], bb[N + 1], c[N + 1];
     dyadic_piece<N>(X, Y, W, q, a, bb, c);
     const double b0 = 8.0 * hodo_bound<N>(a, bb, c);
-    l8 += poly_len<N>(a, bb, c);
+    const double l0 = poly_len<N>(a, bb, c);
     dyadic_piece<N>(X, Y, W, q + 1, a, bb, c);
     const double b1 = 8.0 * hodo_bound<N>(a, bb, c);
-    l8 += poly_len<N>(a, bb, c);
+    const double l1 = poly_len<N>(a, bb, c);
+    l8 += l0 + l1;
     o2[1 + q / 2] = make_double2(b0, b1);
+    o2[5 + q / 2] = make_double2(l0, l1);
   }
   o2[0] = make_double2(B, fmin(B, fmin(lpoly, l8)));
 }
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__r
     default: {   // rejected on the host (k_deg flag); never read past the arrays
       serr[s] = 1;
       double2 *o2 = reinterpret_cast<double2 *>(prep + s);
-      for (int k = 0; k < 5; ++k) o2[k] = make_double2(0.0, 0.0);
+      for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
     }
   }
 }
@@ -737,6 +740,9 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
       const double b0 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.x)) * (1.0 + rel);
       const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.y)) * (1.0 + rel);
       st2<R>(&Cp->Bq[q], (sizeof(R) == 4) ? (R)f_up(b0) : (R)b0, (sizeof(R) == 4) ? (R)f_up(b1) : (R)b1);
+      const double2 lq = pr2[5 + q / 2];
+      const double l0 = lq.x * (1.0 + rel), l1 = lq.y * (1.0 + rel);
+      st2<R>(&Cp->Lq[q], (sizeof(R) == 4) ? (R)f_up(l0) : (R)l0, (sizeof(R) == 4) ? (R)f_up(l1) : (R)l1);
     }
     // homogeneous Horner coefficients c_j = C(n,j) w_j (x_j, y_j, 1), zero above n
 #pragma unroll

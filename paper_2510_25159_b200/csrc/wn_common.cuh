@@ -72,6 +72,7 @@ struct __align__(16) Cold {   // 16-B aligned; every field pair below starts on 
   R M;      // absolute margin (R5)
   R cx[6], cy[6], cw[6];
   R Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin
+  R Lq[8];  // arc-length bound (control-polygon length) of each dyadic piece, incl. margin
   int32_t n, pad;
 };
 
@@ -79,6 +80,7 @@ struct __align__(16) Cold {   // 16-B aligned; every field pair below starts on 
 struct SegPrep {
   double B, S0;
   double Bq[8];
+  double Lq[8];   // control-polygon lengths of the 8 dyadic pieces (arc-length bounds)
 };
 
 // hard-pair queue entry (shared memory): q (9 bits) | angle (1 bit) | cold local index (22 bits)

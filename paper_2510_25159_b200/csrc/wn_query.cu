@@ -209,15 +209,22 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
       if (dR < eps) { res.ob = true; break; }               // Alg. 1 line 1
       // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
       // (piece bounds for d >= 3, their max above), + margin (R5)
-      R Bn;
-      if (d >= 3) {
+      R Bn, span;
+      if (d > 3) {
         Bn = __ldg(&C->Bq[(int)(ta * 8.0)]);
+        span = ldexp(Bn, -d) + M;
       } else {
+        // nodes made of whole dyadic pieces: also the sum of their polygon
+        // lengths (arc-length bounds, R9)
         const int q0 = (int)(ta * 8.0), nq = 8 >> d;
         Bn = __ldg(&C->Bq[q0]);
-        for (int k = 1; k < nq; ++k) Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+        R Ls = __ldg(&C->Lq[q0]);
+        for (int k = 1; k < nq; ++k) {
+          Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+          Ls += __ldg(&C->Lq[q0 + k]);
+        }
+        span = min(ldexp(Bn, -d), Ls) + M;
       }
-      const R span = ldexp(Bn, -d) + M;
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     if (!split) {                                           // chord substitution
@@ -878,11 +885,20 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
       const int q0 = (int)(ta * 8.0);
       R Bn = __ldg(&C->Bq[q0]);
-      if (d < 3) {
+      R span;
+      if (d <= 3) {
+        // nodes made of whole dyadic pieces: also the sum of their polygon
+        // lengths (arc-length bounds, R9)
         const int nq = 8 >> d;
-        for (int k = 1; k < nq; ++k) Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+        R Ls = __ldg(&C->Lq[q0]);
+        for (int k = 1; k < nq; ++k) {
+          Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
+          Ls += __ldg(&C->Lq[q0 + k]);
+        }
+        span = min(ldexp(Bn, -d), Ls) + M;
+      } else {
+        span = ldexp(Bn, -d) + M;
       }
-      const R span = ldexp(Bn, -d) + M;
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     bool done = ob;

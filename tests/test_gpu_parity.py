@@ -245,9 +245,14 @@ def test_k1_derivative_bounds_sound():
             m = (ts >= q / 8) & (ts <= (q + 1) / 8)
             assert row[2 + q] >= sp[m].max() * (1 - 1e-12)
         pts = np.array([oracle.evaluate(P, w, t) for t in ts])
-        arc = np.hypot(*np.diff(pts, axis=0).T).sum()
+        seg = np.hypot(*np.diff(pts, axis=0).T)
+        arc = seg.sum()
         assert row[1] >= arc * (1 - 1e-9)
         assert row[1] <= row[0] + 1e-15
+        # piece polygon lengths bound the pieces' arc lengths (256 samples each)
+        for q in range(8):
+            assert row[10 + q] >= seg[q * 256:(q + 1) * 256].sum() * (1 - 1e-9)
+        assert row[1] <= row[10:18].sum() * (1 + 1e-12)
 
 
 def test_hard_pair_queue_overflow_path(monkeypatch):

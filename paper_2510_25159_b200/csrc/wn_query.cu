@@ -630,7 +630,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
     double zx = 0.0, zy = 0.0;
     float cdf = 0.f;
-    bool up = false, onb = false;
+    int up = 0;                    // side of the branch cut of the previous chain point (0/1)
+    bool onb = false;
     int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
     int xs = 0, halves = 0;
     pend = 0;
@@ -653,13 +654,18 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         }
       }
       const int ce = cb + cn;
-      unsigned sp = sbase + (unsigned)(gr - cb) * (unsigned)sizeof(Hot<R>);   // shared address of record gr
-      while (gr < ce) {
+      // the record cursor and the lanes' subtree ends as shared addresses
+      // within this chunk (converted back to record indices at its end)
+      constexpr int RB = (int)sizeof(Hot<R>);
+      int sp = (int)sbase + (gr - cb) * RB;                    // shared address of record gr
+      int sse = (int)sbase + (skip_end - cb) * RB;             // lane inactive while sp < sse
+      const int spe = (int)sbase + cn * RB;
+      while (sp < spe) {
         HotView<R> h;
-        h.load(sp);
+        h.load((unsigned)sp);
         const uint32_t meta = h.meta;
         const uint32_t kind = meta & 0xFu;
-        const bool act = valid && gr >= skip_end;
+        const bool act = valid && sp >= sse;
         if (COUNT && lane == 0) ++c_rec;
         if (__builtin_expect((meta & 0xEu) == 0u, 1)) {   // SEG (0) or SPAN (1)
           // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
@@ -667,13 +673,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
           // ellipse, d >= eps"; a crossing / hard / uncertain lane takes the exact
           // slow path.
-          bool u1;
+          int u1;
           float df;
           if constexpr (F64) {
-            u1 = h.y >= py;                                      // exact side of the branch cut
+            u1 = h.y >= py ? 1 : 0;                              // exact side of the branch cut
             df = fdist_ftz(h.fx - pxf, h.fy - pyf);
           } else {
-            u1 = h.fy >= pyf;
+            u1 = h.fy >= pyf ? 1 : 0;
             const float dx = h.fx - pxf, dy = h.fy - pyf;
             df = sqrtf(dx * dx + dy * dy);
           }
@@ -691,15 +697,14 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                 }
               }
               if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
-              gr += (int)(meta >> 8);
-              sp += (meta >> 8) * (unsigned)sizeof(Hot<R>);
+              sp += (int)(meta >> 8) * RB;
               if (COUNT && lane == 0) ++c_cull;
             } else if (act && pr) {
               // this lane prunes the run: chord now, inactive for the subtree
               if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
               else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
               zx = h.x; zy = h.y; cdf = df; up = u1;
-              skip_end = gr + 1 + (int)(meta >> 8);
+              sse = sp + RB + (int)(meta >> 8) * RB;
             }
           } else {
             const bool need = act && (!pr || u1 != up || ANGLE);
@@ -758,17 +763,16 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           }
           if (kind == K_MOVE) { gax = h.x; gay = h.y; }
           zx = h.x; zy = h.y; cdf = nd;
-          up = F64 ? (h.y >= py) : (h.fy >= pyf);
+          up = (F64 ? (h.y >= py) : (h.fy >= pyf)) ? 1 : 0;
         } else if (kind == K_GROUP) {
           // copy-group / closed-loop cull: p outside the group's box => exactly 0
           const bool out = !act || group_out_v(h, pxf, pyf);
           const int skip = (int)(meta >> 8);
           if (__all_sync(0xffffffffu, out)) {
-            gr += skip;
-            sp += (unsigned)skip * (unsigned)sizeof(Hot<R>);
+            sp += skip * RB;
             if (COUNT && lane == 0) ++c_cull;
           } else if (out && act) {
-            skip_end = gr + 1 + skip;
+            sse = sp + RB + skip * RB;
           }
         } else if (kind == K_LINE) {
           // omega(p,L) = +-1/2, p on L counts as left (R11)
@@ -791,9 +795,10 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             }
           }
         }
-        ++gr;
-        sp += (unsigned)sizeof(Hot<R>);
+        sp += RB;
       }
+      gr = cb + (sp - (int)sbase) / RB;
+      skip_end = cb + (sse - (int)sbase) / RB;
       // all warps done with this chunk before it is overwritten (multi-chunk faces)
       if (!single && (ce < nrec || sub + QT < T.qcnt)) __syncthreads();
     }

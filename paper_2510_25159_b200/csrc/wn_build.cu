@@ -182,6 +182,9 @@ constexpr SubTab make_subtab() {
   return T;
 }
 __constant__ SubTab c_sub = make_subtab();
+#ifndef PREP_MINB
+#define PREP_MINB 4
+#endif
 
 template <int N>
 __device__ __forceinline__ void dyadic_piece(const double (&X)[N + 1], const double (&Y)[N + 1],
@@ -265,7 +268,7 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
   o2[0] = make_double2(B, fmin(B, fmin(lpoly, l8)));
 }
 
-__global__ void __launch_bounds__(128) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
+__global__ void __launch_bounds__(128, PREP_MINB) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
                                               const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
                                               const double *__restrict__ w, SegPrep *__restrict__ prep,
                                               uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {

@@ -1550,21 +1550,22 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(D.alloc(&B.s0pre, n_segs));
   WN_CUDA(D.alloc(&B.lend, n_segs));
   WN_CUDA(D.alloc(&B.info, n_loops));
-  // K2a first: the host planner only needs the loop summaries, so their copy
-  // is waited on while K1 (derivative bounds) runs on the device
-  if (n_loops) WN_CUDA(cudaMemsetAsync(B.loop_face, 0xFF, sizeof(int32_t) * n_loops, st));
-  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st>>>(n_faces, n_loops, face_loop_off, B.loop_face);
-  if (n_loops)
-    k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_faces, n_segs, loop_seg_off, B.loop_face, face_periodic,
-                                                                      face_domain, seg_degree, B.coff, ctrl_uv, ctrl_w,
-                                                                      B.shift, B.brk, B.chain, B.lend, B.info);
-  g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
-  WN_CUDA(cudaGetLastError());
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_loop_face + k_lift"); }
-  // --- K2b on the device, on an auxiliary stream concurrent with K1 ---
+  // K2a and K2b (lifting, then the device planner) on an auxiliary stream,
+  // concurrent with K1 (derivative bounds: translation invariant, needs no
+  // lifting) on `st`; the host waits only for the planner's summary.  Both
+  // need the control offsets: the auxiliary stream starts after their scan.
   cudaStream_t st2 = g_aux[dev];
   WN_CUDA(cudaEventRecord(g_ev_lift[dev], st));
   WN_CUDA(cudaStreamWaitEvent(st2, g_ev_lift[dev], 0));
+  if (n_loops) WN_CUDA(cudaMemsetAsync(B.loop_face, 0xFF, sizeof(int32_t) * n_loops, st2));
+  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, face_loop_off, B.loop_face);
+  if (n_loops)
+    k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st2>>>(n_loops, n_faces, n_segs, loop_seg_off, B.loop_face, face_periodic,
+                                                                       face_domain, seg_degree, B.coff, ctrl_uv, ctrl_w,
+                                                                       B.shift, B.brk, B.chain, B.lend, B.info);
+  g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
+  WN_CUDA(cudaGetLastError());
+  if (tr.on) { cudaStreamSynchronize(st2); tr.mark("(trace) k_loop_face + k_lift"); }
   DevBuf D2;
   D2.st = st2;
   wn_faces_t F = new wn_faces_s();

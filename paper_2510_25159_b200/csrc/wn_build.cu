@@ -742,10 +742,10 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
       const double2 bq = pr2[1 + q / 2];
       const double b0 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.x)) * (1.0 + rel);
       const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.y)) * (1.0 + rel);
-      st2<R>(&Cp->Bq[q], (sizeof(R) == 4) ? (R)f_up(b0) : (R)b0, (sizeof(R) == 4) ? (R)f_up(b1) : (R)b1);
+      st2<float>(&Cp->Bq[q], f_up(b0), f_up(b1));   // fp32 rounded up: still upper bounds
       const double2 lq = pr2[5 + q / 2];
       const double l0 = lq.x * (1.0 + rel), l1 = lq.y * (1.0 + rel);
-      st2<R>(&Cp->Lq[q], (sizeof(R) == 4) ? (R)f_up(l0) : (R)l0, (sizeof(R) == 4) ? (R)f_up(l1) : (R)l1);
+      st2<float>(&Cp->Lq[q], f_up(l0), f_up(l1));
     }
     // homogeneous Horner coefficients c_j = C(n,j) w_j (x_j, y_j, 1), zero above n
 #pragma unroll

@@ -71,8 +71,8 @@ struct __align__(16) Cold {   // 16-B aligned; every field pair below starts on 
   R B;      // derivative bound (A.1; R29) incl. relative margin
   R M;      // absolute margin (R5)
   R cx[6], cy[6], cw[6];
-  R Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin
-  R Lq[8];  // arc-length bound (control-polygon length) of each dyadic piece, incl. margin
+  float Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin, rounded up
+  float Lq[8];  // arc-length bound (control-polygon length) of each dyadic piece, incl. margin, rounded up
   int32_t n, pad;
 };
 

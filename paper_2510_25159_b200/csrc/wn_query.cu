@@ -211,17 +211,17 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
       // (piece bounds for d >= 3, their max above), + margin (R5)
       R Bn, span;
       if (d > 3) {
-        Bn = __ldg(&C->Bq[(int)(ta * 8.0)]);
+        Bn = (R)__ldg(&C->Bq[(int)(ta * 8.0)]);
         span = ldexp(Bn, -d) + M;
       } else {
         // nodes made of whole dyadic pieces: also the sum of their polygon
         // lengths (arc-length bounds, R9)
         const int q0 = (int)(ta * 8.0), nq = 8 >> d;
-        Bn = __ldg(&C->Bq[q0]);
-        R Ls = __ldg(&C->Lq[q0]);
+        Bn = (R)__ldg(&C->Bq[q0]);
+        R Ls = (R)__ldg(&C->Lq[q0]);
         for (int k = 1; k < nq; ++k) {
-          Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
-          Ls += __ldg(&C->Lq[q0 + k]);
+          Bn = max(Bn, (R)__ldg(&C->Bq[q0 + k]));
+          Ls += (R)__ldg(&C->Lq[q0 + k]);
         }
         span = min(ldexp(Bn, -d), Ls) + M;
       }
@@ -889,16 +889,16 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       ob = dR < eps;                                        // Alg. 1 line 1
       // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
       const int q0 = (int)(ta * 8.0);
-      R Bn = __ldg(&C->Bq[q0]);
+      R Bn = (R)__ldg(&C->Bq[q0]);
       R span;
       if (d <= 3) {
         // nodes made of whole dyadic pieces: also the sum of their polygon
         // lengths (arc-length bounds, R9)
         const int nq = 8 >> d;
-        R Ls = __ldg(&C->Lq[q0]);
+        R Ls = (R)__ldg(&C->Lq[q0]);
         for (int k = 1; k < nq; ++k) {
-          Bn = max(Bn, __ldg(&C->Bq[q0 + k]));
-          Ls += __ldg(&C->Lq[q0 + k]);
+          Bn = max(Bn, (R)__ldg(&C->Bq[q0 + k]));
+          Ls += (R)__ldg(&C->Lq[q0 + k]);
         }
         span = min(ldexp(Bn, -d), Ls) + M;
       } else {

@@ -556,13 +556,23 @@ __device__ void put_group<float>(Hot<float> *H, int r, double xmin, double ymin,
   H[r] = h;
 }
 
-// C(n, j) for n <= 5, exact (no per-call local table)
+// C(n, j) for 0 <= j <= n <= 5, exact: 4-bit entries of a packed table indexed
+// by 6 n + j (no divisions, no local or constant-memory table)
 __device__ __forceinline__ double binom5(int n, int j) {
-  double c = 1.0;
-#pragma unroll
-  for (int i = 0; i < 5; ++i)
-    if (i < j) c = c * (double)(n - i) / (double)(i + 1);   // integer quotients: exact
-  return c;
+  constexpr unsigned long long T0 = 0x0000000000000000ull   // n = 0, 1, 2 (idx 0..15)
+      | 1ull << 0                                            // C(0,0)
+      | 1ull << 24 | 1ull << 28                              // C(1,0..1)
+      | 1ull << 48 | 2ull << 52 | 1ull << 56;                // C(2,0..2)
+  constexpr unsigned long long T1 = 0x0000000000000000ull   // n = 3, 4, 5 (idx 18..35, minus 18)
+      | 1ull << 0 | 3ull << 4 | 3ull << 8 | 1ull << 12        // C(3,0..3)
+      | 1ull << 24 | 4ull << 28 | 6ull << 32 | 4ull << 36 | 1ull << 40   // C(4,0..4)
+      | 1ull << 48 | 5ull << 52 | 10ull << 56 | 10ull << 60;           // C(5,0..3)
+  const int idx = 6 * n + j;
+  unsigned v;
+  if (idx < 18) v = (unsigned)(T0 >> (4 * idx)) & 15u;
+  else if (idx < 34) v = (unsigned)(T1 >> (4 * (idx - 18))) & 15u;
+  else v = idx == 34 ? 5u : 1u;                              // C(5,4), C(5,5)
+  return (double)v;
 }
 
 template <typename R>

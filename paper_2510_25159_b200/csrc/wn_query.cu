@@ -1049,10 +1049,14 @@ __global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t 
       uint4 v = fv[i];
       if (((v.x | v.y | v.z | v.w) & 0x80808080u) == 0) continue;   // final flags are 0..3
       // all 16 windings in flight at once (a pending group has several)
+      // the windings of the pending entries only (predicated loads, all in flight)
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
       double wv[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) wv[k] = winding[16 * i + k];
-      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+      for (int k = 0; k < 16; ++k) {
+        const bool pk = ((w[k >> 2] >> (8 * (k & 3))) & 0xFFu) == FLAG_PENDING;
+        wv[k] = pk ? winding[16 * i + k] : 0.0;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint32_t o = 0;

@@ -109,6 +109,28 @@ def test_c5_full_size_sampled():
     _check(wl, w, fl, idx=idx, min_cmp=0.97)
 
 
+def test_c3_full_size_sampled():
+    """BASELINE configs[2] at full size (1M queries on the bi-periodic torus),
+    sampled oracle check."""
+    wl = G.gen_c3()
+    w, fl = _gpu(wl)
+    assert np.all(fl != 3)
+    idx = np.random.default_rng(2).choice(len(w), 20_000, replace=False)
+    _check(wl, w, fl, idx=idx, min_cmp=0.99)
+
+
+@pytest.mark.parametrize("fp32", [False, True])
+def test_c4_full_size_sampled(fp32):
+    """BASELINE configs[3] at full size (1,000 gapped / open loops, 256k
+    queries), fp64 and fp32 (oracle on the fp32-rounded inputs, R19), sampled."""
+    wl = G.gen_c4()
+    if fp32:
+        wl = G.to_fp32_inputs(wl)
+    w, fl = _gpu(wl, precision=1 if fp32 else 0)
+    idx = np.random.default_rng(3).choice(len(w), 30_000, replace=False)
+    _check(wl, w, fl, idx=idx, fp32=fp32, min_cmp=0.95)
+
+
 # ----------------------------------------------------------------------------
 # edge cases
 # ----------------------------------------------------------------------------

@@ -415,7 +415,10 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   __shared__ uint32_t s_hist[SP_BINS / 2];   // 16-bit counters, two per word
   __shared__ int s_wsum[NWARP];
   __shared__ int s_coh[2];                   // coherence probe: perimeter sum, warps
+  __shared__ double s_v0;                    // row probe: v of the unit's first query
+  __shared__ int s_nu;                       // row probe: first index with another v
   if (t < 2) s_coh[t] = 0;
+  if (t == 0) s_nu = QT;
   // (kept in shared memory, not in registers across the record loop)
   __shared__ double s_grid[4];   // u_lo, v_lo, (u_hi - u_lo) / nu, (v_hi - v_lo) / nv
   __shared__ int s_gloc0;
@@ -477,6 +480,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   // culling a group.  A permutation of whole queries: no value changes.  The
   // order goes to a per-unit scratch range (L2-resident), read per sub-tile.
   bool spatial = false;
+  int lt = t;                    // query of this thread within a sub-tile (see below)
   if constexpr (!GRID) {
     spatial = P.spatial && T.qcnt > 32;
     const float4 fb = spatial ? P.face_box[f] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -527,9 +531,27 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           }
         }
       }
+      // Row probe: a unit that starts with whole rows of length nu (v constant
+      // along a row; nu dividing QT) -- a row-major tessellation grid -- is
+      // mapped to 2-D warp tiles like wn_query_grid, without sorting
+      double vt = 0.0;
+      if (t < T.qcnt) {
+        const int32_t pos = (int32_t)T.qbeg + t;
+        vt = P.uv[2 * (int64_t)(unsorted ? P.perm[pos] : pos) + 1];
+        if (t == 0) s_v0 = vt;
+      }
       for (int i = t; i < SP_BINS / 2; i += NTH) s_hist[i] = 0;
       __syncthreads();
-      spatial = s_coh[0] > SP_COHERENT * s_coh[1];
+      if (t > 0 && t < T.qcnt && !(vt == s_v0)) atomicMin(&s_nu, t);
+      __syncthreads();
+      const int nu = s_nu;
+      if (T.qcnt >= QT && nu >= 8 && nu < QT && QT % nu == 0 && QT / nu <= 32) {
+        const int bw = 32 / (QT / nu);   // row-major unit: the same 2-D tiles as a grid
+        lt = (lane / bw) * nu + warp * bw + lane % bw;
+        spatial = false;
+      } else {
+        spatial = s_coh[0] > SP_COHERENT * s_coh[1];
+      }
       }
     if (spatial) {
       // pass 1: key and rank within its cell -> scratch (key << 12 | rank)
@@ -589,7 +611,6 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   // grid_blk x (32 / grid_blk) block of cells instead of a run of one row: the
   // warp's queries then lie close together, so they agree more often on
   // pruning a hierarchy span or culling a group (fewer warp-level descents).
-  int lt = t;
   if constexpr (GRID) {
     const int bw = P.grid_blk;
     if (bw > 0) lt = (lane / bw) * P.grid_nu + warp * bw + lane % bw;

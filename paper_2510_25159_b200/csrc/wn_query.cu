@@ -1122,7 +1122,7 @@ __device__ __forceinline__ int hist_key(int f, int n_faces) { return (f >= 0 && 
 __global__ void k_hist(int64_t n, const int32_t *__restrict__ face_id, int32_t n_faces,
                        int32_t *__restrict__ cnt, int32_t *__restrict__ unsorted,
                        double *__restrict__ winding, uint8_t *__restrict__ flag) {
-  constexpr int G = 8;   // ids per thread (two 16-B loads in flight)
+  constexpr int G = 16;  // ids per thread (four 16-B loads in flight)
   const bool vec = ((uintptr_t)face_id & 15) == 0;
   const int64_t ng = (n + G - 1) / G;
   const int lane = threadIdx.x & 31;
@@ -1132,10 +1132,11 @@ __global__ void k_hist(int64_t n, const int32_t *__restrict__ face_id, int32_t n
     const int64_t i0 = g * G;
     int id[G];
     if (g < ng && vec && i0 + G - 1 < n) {
-      const int4 v0 = *reinterpret_cast<const int4 *>(face_id + i0);
-      const int4 v1 = *reinterpret_cast<const int4 *>(face_id + i0 + 4);
-      id[0] = v0.x; id[1] = v0.y; id[2] = v0.z; id[3] = v0.w;
-      id[4] = v1.x; id[5] = v1.y; id[6] = v1.z; id[7] = v1.w;
+#pragma unroll
+      for (int k = 0; k < G; k += 4) {
+        const int4 v = *reinterpret_cast<const int4 *>(face_id + i0 + k);
+        id[k] = v.x; id[k + 1] = v.y; id[k + 2] = v.z; id[k + 3] = v.w;
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < G; ++k) id[k] = (g < ng && i0 + k < n) ? face_id[i0 + k] : INT32_MIN;
@@ -1345,7 +1346,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   const int TB = 256;
   const int64_t nb64 = (n + TB - 1) / TB;
   const int nb = (int)(nb64 < 148 * 32 ? nb64 : 148 * 32);
-  const int64_t nbh64 = ((n + 7) / 8 + TB - 1) / TB;
+  const int64_t nbh64 = ((n + 15) / 16 + TB - 1) / TB;
   const int nbh = (int)(nbh64 < 148 * 16 ? nbh64 : 148 * 16);
   k_hist<<<nbh, TB, 0, st>>>(n, face_id, nf, cnt, flags, winding, flag);
   ++launches;

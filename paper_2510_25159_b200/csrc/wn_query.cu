@@ -502,56 +502,56 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         return mx | (my << 1);
       };
       if (spatial) {
-      // Coherence probe on the first QT queries in their given order: the
-      // mean perimeter (in cells) of a warp's footprint.  Already coherent
-      // input (e.g. row-major grids: a warp covers a short run of one row) is
-      // left in its order -- regrouping it would cost more than it saves.
-      {
-        int cx = 0, cy = 0;
-        bool ok = t < T.qcnt;
-        if (ok) {
-          int32_t q_;
-          const int k = key_of(t, q_);
-          // cell coordinates back from the Morton key
-          int a = k & 0x5555, b = (k >> 1) & 0x5555;
-          a = (a | (a >> 1)) & 0x3333; a = (a | (a >> 2)) & 0x0F0F; a = (a | (a >> 4)) & 0x00FF;
-          b = (b | (b >> 1)) & 0x3333; b = (b | (b >> 2)) & 0x0F0F; b = (b | (b >> 4)) & 0x00FF;
-          cx = a;
-          cy = b;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (m) {
-          const unsigned x0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cx : 255u);
-          const unsigned x1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cx : 0u);
-          const unsigned y0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cy : 255u);
-          const unsigned y1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cy : 0u);
-          if (lane == 0) {
-            atomicAdd(&s_coh[0], (int)((x1 - x0) + (y1 - y0)));
-            atomicAdd(&s_coh[1], 1);
+        // Coherence probe on the first QT queries in their given order: the
+        // mean perimeter (in cells) of a warp's footprint.  Already coherent
+        // input (e.g. row-major grids: a warp covers a short run of one row) is
+        // left in its order -- regrouping it would cost more than it saves.
+        {
+          int cx = 0, cy = 0;
+          bool ok = t < T.qcnt;
+          if (ok) {
+            int32_t q_;
+            const int k = key_of(t, q_);
+            // cell coordinates back from the Morton key
+            int a = k & 0x5555, b = (k >> 1) & 0x5555;
+            a = (a | (a >> 1)) & 0x3333; a = (a | (a >> 2)) & 0x0F0F; a = (a | (a >> 4)) & 0x00FF;
+            b = (b | (b >> 1)) & 0x3333; b = (b | (b >> 2)) & 0x0F0F; b = (b | (b >> 4)) & 0x00FF;
+            cx = a;
+            cy = b;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (m) {
+            const unsigned x0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cx : 255u);
+            const unsigned x1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cx : 0u);
+            const unsigned y0 = __reduce_min_sync(0xffffffffu, ok ? (unsigned)cy : 255u);
+            const unsigned y1 = __reduce_max_sync(0xffffffffu, ok ? (unsigned)cy : 0u);
+            if (lane == 0) {
+              atomicAdd(&s_coh[0], (int)((x1 - x0) + (y1 - y0)));
+              atomicAdd(&s_coh[1], 1);
+            }
           }
         }
-      }
-      // Row probe: a unit that starts with whole rows of length nu (v constant
-      // along a row; nu dividing QT) -- a row-major tessellation grid -- is
-      // mapped to 2-D warp tiles like wn_query_grid, without sorting
-      double vt = 0.0;
-      if (t < T.qcnt) {
-        const int32_t pos = (int32_t)T.qbeg + t;
-        vt = P.uv[2 * (int64_t)(unsorted ? P.perm[pos] : pos) + 1];
-        if (t == 0) s_v0 = vt;
-      }
-      for (int i = t; i < SP_BINS / 2; i += NTH) s_hist[i] = 0;
-      __syncthreads();
-      if (t > 0 && t < T.qcnt && !(vt == s_v0)) atomicMin(&s_nu, t);
-      __syncthreads();
-      const int nu = s_nu;
-      if (T.qcnt >= QT && nu >= 8 && nu < QT && QT % nu == 0 && QT / nu <= 32) {
-        const int bw = 32 / (QT / nu);   // row-major unit: the same 2-D tiles as a grid
-        lt = (lane / bw) * nu + warp * bw + lane % bw;
-        spatial = false;
-      } else {
-        spatial = s_coh[0] > SP_COHERENT * s_coh[1];
-      }
+        // Row probe: a unit that starts with whole rows of length nu (v constant
+        // along a row; nu dividing QT) -- a row-major tessellation grid -- is
+        // mapped to 2-D warp tiles like wn_query_grid, without sorting
+        double vt = 0.0;
+        if (t < T.qcnt) {
+          const int32_t pos = (int32_t)T.qbeg + t;
+          vt = P.uv[2 * (int64_t)(unsorted ? P.perm[pos] : pos) + 1];
+          if (t == 0) s_v0 = vt;
+        }
+        for (int i = t; i < SP_BINS / 2; i += NTH) s_hist[i] = 0;
+        __syncthreads();
+        if (t > 0 && t < T.qcnt && !(vt == s_v0)) atomicMin(&s_nu, t);
+        __syncthreads();
+        const int nu = s_nu;
+        if (T.qcnt >= QT && nu >= 8 && nu < QT && QT % nu == 0 && QT / nu <= 32) {
+          const int bw = 32 / (QT / nu);   // row-major unit: the same 2-D tiles as a grid
+          lt = (lane / bw) * nu + warp * bw + lane % bw;
+          spatial = false;
+        } else {
+          spatial = s_coh[0] > SP_COHERENT * s_coh[1];
+        }
       }
     if (spatial) {
       // pass 1: key and rank within its cell -> scratch (key << 12 | rank)

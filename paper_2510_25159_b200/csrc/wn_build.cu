@@ -902,8 +902,10 @@ __host__ __device__ inline double tile_margin(const FaceCtx &C) {
 
 // contractible loop in a (uni/bi/non-)periodic face: every translate meeting the tile
 template <class S>
-__host__ __device__ void plan_contractible(S &P, int l, const LoopInfo &I, const FaceCtx &C, bool tree) {
-  const int fl = loop_flags(I, C.angle, false, tree);
+__host__ __device__ void plan_contractible(S &P, int l, const LoopInfo &I, const FaceCtx &C, bool tree,
+                                           bool no_cull = false) {
+  int fl = loop_flags(I, C.angle, false, tree);
+  if (no_cull) fl &= ~PF_CULL;
   int i0 = 0, i1 = 0, j0 = 0, j1 = 0;
   const double m = tile_margin(C);
   if (C.per & 1) k_range(I.bb[0], I.bb[2], C.u0, C.Tu, m, i0, i1);
@@ -1026,11 +1028,26 @@ __host__ __device__ void plan_general_pair(S &P, int l, const LoopInfo &I, int l
 template <class S>
 __host__ __device__ void plan_face(S &P, const LoopInfo *L, int l0, int l1, const FaceCtx &C,
                                    const int *pair_beta, const int *pair_s, bool tree) {
+  // Non-periodic face: the loop whose box holds every other loop's box (the
+  // outer boundary) gets no cull header -- its box is the face's query box, so
+  // the header would pass for (nearly) every query and only cost an iteration
+  // (a query outside it prunes at the loop's first hierarchy level instead)
+  int outer = -1;
+  if (C.per == 0) {
+    double x0 = INFINITY, y0 = INFINITY, x1 = -INFINITY, y1 = -INFINITY;
+    for (int l = l0; l < l1; ++l) {
+      if (L[l].nseg == 0) continue;
+      x0 = fmin(x0, L[l].bb[0]); y0 = fmin(y0, L[l].bb[1]);
+      x1 = fmax(x1, L[l].bb[2]); y1 = fmax(y1, L[l].bb[3]);
+    }
+    for (int l = l0; l < l1 && outer < 0; ++l)
+      if (L[l].nseg && L[l].bb[0] == x0 && L[l].bb[1] == y0 && L[l].bb[2] == x1 && L[l].bb[3] == y1) outer = l;
+  }
   for (int l = l0; l < l1; ++l) {
     const LoopInfo &I = L[l];
     if (I.nseg == 0) continue;
     if (C.per == 0 || (I.cu == 0 && I.cv == 0)) {
-      plan_contractible(P, l, I, C, tree);
+      plan_contractible(P, l, I, C, tree, l == outer);
       continue;
     }
     const int axis = (I.cu != 0) ? 0 : 1;

@@ -500,6 +500,28 @@ __global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, 
 // ---------------------------------------------------------------------------
 // K2c: record emission, one thread per planned group.
 // ---------------------------------------------------------------------------
+// Path-hierarchy trees of closed single-chain loops omit their top OMIT_LEVELS
+// levels of SPAN nodes: the half-loop ellipses of a closed loop contain
+// (nearly) the whole loop interior, so those nodes almost never prune and a
+// warp would only spend an iteration descending them.  Value-neutral (an
+// omitted node = always descend).  Split rule of every tree: [a, b] ->
+// [a, mid], [mid + 1, b], mid = (a + b) >> 1.
+constexpr int OMIT_LEVELS = 2;
+static_assert(OMIT_LEVELS <= 2, "tree_internal_top is written out for k <= 2");
+__host__ __device__ inline int tree_internal_top(int n, int k) {   // internal nodes at depth < k
+  int c = 0;
+  if (k >= 1 && n >= 2) {
+    ++c;
+    if (k >= 2) {
+      const int left = (n + 1) >> 1, right = n - left;   // left = mid - a + 1 for any [a, b]
+      c += (left >= 2 ? 1 : 0) + (right >= 2 ? 1 : 0);
+    }
+  }
+  return c;
+}
+// records of the pre-order tree over n leaves with its top k levels omitted
+__host__ __device__ inline int tree_recs(int n, int k) { return 2 * n - 1 - tree_internal_top(n, k); }
+
 template <typename R>
 struct Emit;
 
@@ -699,15 +721,17 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
         if (s == s0) put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVE | fa);
         else put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVEG | fa);
       }
-      bool omit = omit_root && ch.y >= 2;                // closed loop: no root SPAN
+      int depth = 0;
+      const int omit_k = omit_root ? OMIT_LEVELS : 0;    // closed loop: no top SPAN levels
       while (a < bnd) {
         const int mid = (a + bnd) >> 1;
-        if (omit) {                                      // root level without its record
-          omit = false;
+        if (depth < omit_k) {                            // omitted level: no record
           if (j <= mid) bnd = mid;
-          else { off += 2 * (mid - a + 1) - 1; a = mid + 1; }
+          else { off += tree_recs(mid - a + 1, omit_k - depth - 1); a = mid + 1; }
+          ++depth;
           continue;
         }
+        ++depth;
         if (j == a) {
           // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
           const int se = s0 + ch.x + bnd;                // last segment of the run
@@ -779,7 +803,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     }
   }
   if (lane == 0) {
-    int r = tree ? G.rec_off + cull + 2 * (s1 - s0) - (omit_root && s1 - s0 >= 2 ? 1 : 0)
+    int r = tree ? G.rec_off + cull + 1 + tree_recs(s1 - s0, omit_root ? OMIT_LEVELS : 0)
                  : r_first + (s1 - s0) + carry;
     if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
     if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
@@ -790,6 +814,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
 // ---------------------------------------------------------------------------
 // host planner
 // ---------------------------------------------------------------------------
+__host__ __device__ inline int group_nrec(int kind, int flags, const LoopInfo &I);
+
 struct Plan {
   std::vector<PlanGroup> groups;
   std::vector<int32_t> rec_off;   // per target face + 1
@@ -834,8 +860,7 @@ struct Plan {
       ++n_lines;
     } else {
       // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg
-      nrec = ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) +
-             ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
+      nrec = group_nrec(kind, flags, I);
       colds += I.nseg;
       if (flags & PF_CULL) ++n_cull;
     }
@@ -872,9 +897,9 @@ struct FaceCtx {
 __host__ __device__ inline int group_nrec(int kind, int flags, const LoopInfo &I) {
   if (kind == G_LINE) return 1;
   // flat: MOVE + nseg SEG + nbrk MOVEG; tree: MOVE + sum_c (2 m_c - 1) + nbrk = 2 nseg,
-  // minus the omitted root SPAN of a closed single-chain loop
+  // minus the omitted top SPAN levels of a closed single-chain loop
   return ((flags & PF_CULL) ? 1 : 0) + ((flags & PF_TREE) ? 2 * I.nseg : 1 + I.nseg + I.nbrk) -
-         ((flags & PF_OMIT_ROOT) && I.nseg >= 2 ? 1 : 0) +
+         ((flags & PF_OMIT_ROOT) ? tree_internal_top(I.nseg, OMIT_LEVELS) : 0) +
          ((flags & (PF_TAIL_CLOSEG | PF_TAIL_XCH | PF_TAIL_NCH)) ? 1 : 0);
 }
 

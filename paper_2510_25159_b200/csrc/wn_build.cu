@@ -614,7 +614,8 @@ __device__ __forceinline__ void st2<float>(float *p, float a, float b) {
 // EMIT_STAGE segments the warp first stages them in shared memory, so the
 // per-level SPAN emission reads shared memory instead of a chain of global loads.
 constexpr int EMIT_WARPS = 4;
-constexpr int EMIT_STAGE = 256;
+constexpr int EMIT_STAGE = 128;
+constexpr int PREP_D2 = (int)(sizeof(SegPrep) / 16);   // 16-B words per K1 record
 #ifndef EMIT_MINB
 #define EMIT_MINB 8
 #endif
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
   const int r_first = G.rec_off + cull + 1;              // first record after GROUP? and MOVE
   const bool tree = (G.flags & PF_TREE) != 0;
   const bool omit_root = tree && (G.flags & PF_OMIT_ROOT) != 0;
+  __shared__ double2 s_prep[EMIT_WARPS][32 * PREP_D2];  // the chunk's K1 records
   __shared__ double2 s_end[EMIT_WARPS][EMIT_STAGE];      // translated lifted end points
   __shared__ double s_pre[EMIT_WARPS][EMIT_STAGE];       // S0 prefix sums
   const int wib = (threadIdx.x >> 5);
@@ -695,6 +697,14 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     const unsigned bm = __ballot_sync(0xffffffffu, bk);
     const int nb = carry + __popc(bm & ((2u << lane) - 1u));   // breaks in (s0, s]
     carry += __popc(bm);
+    // this chunk's K1 records (contiguous: 144 B per segment) staged with
+    // coalesced 16-B loads instead of one strided record per lane
+    {
+      const int cnt = min(32, s1 - base);
+      const double2 *src = reinterpret_cast<const double2 *>(prep + base);
+      for (int i = lane; i < cnt * PREP_D2; i += 32) s_prep[wib][i] = src[i];
+      __syncwarp();
+    }
     if (!in) continue;
     const int idx = s - s0;
     const int n = deg[s];
@@ -754,7 +764,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
       }
       r = off;
     }
-    const double2 *pr2 = reinterpret_cast<const double2 *>(prep + s);
+    const double2 *pr2 = &s_prep[wib][lane * PREP_D2];   // this segment's K1 record (staged)
     const double2 bs = pr2[0];                            // (B, S0)
     const double bpB = bs.x, bpS0 = bs.y;
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the

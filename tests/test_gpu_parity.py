@@ -460,3 +460,61 @@ def test_spatial_regrouping_is_a_permutation(monkeypatch):
     assert torch.equal(r1.flag, r2.flag)
     same = (r1.winding == r2.winding) | (torch.isnan(r1.winding) & torch.isnan(r2.winding))
     assert bool(same.all())
+
+
+# ----------------------------------------------------------------------------
+# degenerate geometry and large faces
+# ----------------------------------------------------------------------------
+
+def test_degenerate_segments_and_loops():
+    """Zero-length segments (all control points equal), collinear control
+    points, a closed loop of ONE segment (coincident end points: its root
+    ellipse foci coincide), a two-segment lens, faces with no loops and a loop
+    of degree-1 segments only: parity with the oracle, and the loop-free face
+    is 0 everywhere."""
+    rng = np.random.default_rng(11)
+    c = np.array([0.5, 0.5])
+    # square with a zero-length and a collinear cubic inserted on its edges
+    sq = [(np.array([[0.2, 0.2], [0.8, 0.2]]), None),
+          (np.array([[0.8, 0.2], [0.8, 0.2], [0.8, 0.2], [0.8, 0.2]]), None),       # zero length
+          (np.array([[0.8, 0.2], [0.8, 0.4], [0.8, 0.6], [0.8, 0.8]]), None),       # collinear cubic
+          (np.array([[0.8, 0.8], [0.2, 0.8]]), None),
+          (np.array([[0.2, 0.8], [0.2, 0.2]]), None)]
+    # one-segment closed loop (quintic teardrop), rational weights
+    P = np.array([[0.5, 0.3], [0.9, 0.1], [0.9, 0.9], [0.1, 0.9], [0.1, 0.1], [0.5, 0.3]])
+    drop = [(P, rng.uniform(0.5, 2.0, 6))]
+    # two-segment lens
+    lens = [(np.array([[0.3, 0.5], [0.5, 0.8], [0.7, 0.5]]), None), (np.array([[0.7, 0.5], [0.5, 0.2], [0.3, 0.5]]), None)]
+    faces = [([sq], 0, (0, 1, 0, 1)), ([drop], 0, (0, 1, 0, 1)), ([lens], 0, (0, 1, 0, 1)), ([], 0, (0, 1, 0, 1))]
+    nq = 4000
+    q = rng.uniform(0, 1, size=(len(faces) * nq, 2))
+    fid = np.repeat(np.arange(len(faces)), nq).astype(np.int32)
+    wl = H.make_wl(faces, q, fid)
+    w, fl = _gpu(wl)
+    _check(wl, w, fl, min_cmp=0.99)
+    assert np.all(w[fid == 3] == 0.0) and np.all(fl[fid == 3] == 0)
+
+
+def test_large_face_multichunk():
+    """One face whose record program spans many 32-KB shared-memory chunks
+    (an 8,000-segment rational star loop plus 50 holes): staging chunk by
+    chunk, hierarchy subtrees and skips that cross chunk boundaries."""
+    rng = np.random.default_rng(12)
+    from wn_workloads.configs import _star_segments, _star_vertices
+    outer = _star_segments(rng, _star_vertices(rng, (0.5, 0.5), 0.42, 0.02, 8000, False),
+                           rng.integers(1, 6, 8000), 0.05, True)
+    loops = [outer]
+    for k in range(50):
+        cc = (0.2 + 0.6 * ((k % 10) + 0.5) / 10, 0.3 + 0.4 * ((k // 10) + 0.5) / 5)
+        loops.append(_star_segments(rng, _star_vertices(rng, cc, 0.02, 0.002, 12, True),
+                                    rng.integers(1, 6, 12), 0.05, True))
+    q = rng.uniform(0.05, 0.95, size=(30_000, 2))
+    wl = H.make_wl([(loops, 0, (0, 1, 0, 1))], q)
+    faces = wn.Faces.from_workload(wl)
+    assert faces.info()["max_face_records"] > 3 * 1024
+    r = faces.query(wl["face_id"], wl["uv"])
+    torch.cuda.synchronize()
+    w, fl = r.winding.cpu().numpy(), r.flag.cpu().numpy()
+    faces.close()
+    idx = np.random.default_rng(0).choice(len(w), 3000, replace=False)
+    _check(wl, w, fl, idx=idx, min_cmp=0.95)

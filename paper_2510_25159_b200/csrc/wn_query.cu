@@ -632,6 +632,10 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       } else {
         u = P.uv[2 * (int64_t)qi];
         v = P.uv[2 * (int64_t)qi + 1];
+        // the next sub-tile's point to L2 while this one is swept (given order
+        // or row tiles: the position is the query index)
+        if (!spatial && !unsorted && sub + QT + lt < T.qcnt)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.uv + 2 * (int64_t)(pos + QT)));
       }
       if (!isfinite(u) || !isfinite(v)) {
         P.winding[qi] = nan_d();

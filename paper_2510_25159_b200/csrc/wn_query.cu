@@ -880,6 +880,8 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
     if (!live) {
       if (i >= total) break;
       const HardEntry H = P.hq[i];
+      if (i + stride < total)   // this lane's next pair, to L2 while this one recurses
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.hq + i + stride));
       angle = H.c >> 31;
       C = P.cold + (H.c & 0x7fffffffu);
       qx = (R)H.px;

@@ -1152,6 +1152,12 @@ __global__ void k_hist(int64_t n, const int32_t *__restrict__ face_id, int32_t n
     int nxt = __shfl_down_sync(0xffffffffu, id[0], 1);
     if (lane == 0) prv = (g < ng && i0 > 0) ? face_id[i0 - 1] : INT32_MIN;
     if (lane == 31 || g + 1 >= ng) nxt = (g < ng && i0 + G < n) ? face_id[i0 + G] : INT32_MIN;
+    // fast path: a whole group inside one run of a valid face id (the common
+    // case, runs are a face's queries) -- no boundary, no atomic, sorted
+    int dif = (prv ^ id[0]) | (nxt ^ id[0]);
+#pragma unroll
+    for (int k = 1; k < G; ++k) dif |= id[k] ^ id[0];
+    if (dif == 0 && g < ng && i0 > 0 && i0 + G < n && hist_key(id[0], n_faces) >= 0) continue;
     if (g < ng) {
 #pragma unroll
       for (int k = 0; k < G; ++k) {

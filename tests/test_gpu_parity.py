@@ -518,3 +518,47 @@ def test_large_face_multichunk():
     faces.close()
     idx = np.random.default_rng(0).choice(len(w), 3000, replace=False)
     _check(wl, w, fl, idx=idx, min_cmp=0.95)
+
+
+def test_bucketing_runs_and_group_boundaries():
+    """K4 (a3) on batches built to stress the histogram's 16-id groups: runs of
+    a face's queries of length 1, 15, 16, 17, 31, 32, 33, 48 and 1,000+ placed
+    at and off group boundaries, invalid ids (-1, n_faces) inside long runs and
+    at group edges, a descending face id exactly at a group boundary after a
+    long sorted prefix (the batch must be detected unsorted) and a repeated
+    face after other faces.  Valid queries match the oracle; invalid ids are
+    flagged 3."""
+    wl = G.gen_c4(n_faces=40, q_per_face=200, n_deleted=4)
+    rng = np.random.default_rng(21)
+    pool = {f: np.nonzero(wl["face_id"] == f)[0] for f in range(40)}
+    lens = [1, 15, 16, 17, 31, 32, 33, 48, 1024, 1040, 7, 16, 16, 64]
+    fids, src = [], []
+    for k, L in enumerate(lens):
+        f = k % 40 if k != 9 else 3          # face 3 again after others
+        fids.append(np.full(L, f, np.int32))
+        src.append(rng.choice(pool[f], L))
+    # a descending step exactly at a group boundary (prefix length is a multiple of 16)
+    pre = sum(len(a) for a in fids)
+    pad = (-pre) % 16
+    fids.append(np.full(pad + 32, 39, np.int32))
+    src.append(rng.choice(pool[39], pad + 32))
+    fids.append(np.full(48, 2, np.int32))
+    src.append(rng.choice(pool[2], 48))
+    fid = np.concatenate(fids)
+    idx = np.concatenate(src)
+    assert (pre + pad + 32) % 16 == 0
+    uv = wl["uv"][idx].copy()
+    bad = [int(np.cumsum(lens)[8]) - 500, int(np.cumsum(lens)[8]) - 512, 0, len(fid) - 1, pre + pad + 16]
+    fid[bad[0]] = -1
+    fid[bad[1]] = 40
+    fid[bad[2]] = 41
+    fid[bad[3]] = -7
+    fid[bad[4]] = 40
+    w, fl = _gpu(wl, face_id=fid, uv=uv)
+    assert np.all(fl[bad] == 3) and np.all(np.isnan(w[bad]))
+    ok = np.ones(len(fid), bool)
+    ok[bad] = False
+    assert np.all(fl[ok] != 3)
+    wl2 = dict(wl)
+    wl2["face_id"], wl2["uv"] = fid[ok], uv[ok]
+    _check(wl2, w[ok], fl[ok], min_cmp=0.95)

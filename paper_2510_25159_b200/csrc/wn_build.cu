@@ -614,7 +614,9 @@ __device__ __forceinline__ void st2<float>(float *p, float a, float b) {
 // EMIT_STAGE segments the warp first stages them in shared memory, so the
 // per-level SPAN emission reads shared memory instead of a chain of global loads.
 constexpr int EMIT_WARPS = 4;
-constexpr int EMIT_STAGE = 128;
+#ifndef EMIT_STAGE
+#define EMIT_STAGE 128
+#endif
 constexpr int PREP_D2 = (int)(sizeof(SegPrep) / 16);   // 16-B words per K1 record
 #ifndef EMIT_MINB
 #define EMIT_MINB 8

@@ -613,7 +613,9 @@ __device__ __forceinline__ void st2<float>(float *p, float a, float b) {
 // prefix of segments handled by other lanes (or chunks): for groups of up to
 // EMIT_STAGE segments the warp first stages them in shared memory, so the
 // per-level SPAN emission reads shared memory instead of a chain of global loads.
-constexpr int EMIT_WARPS = 4;
+#ifndef EMIT_WARPS
+#define EMIT_WARPS 4
+#endif
 #ifndef EMIT_STAGE
 #define EMIT_STAGE 128
 #endif

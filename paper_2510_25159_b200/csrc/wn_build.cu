@@ -291,6 +291,54 @@ __global__ void __launch_bounds__(128, PREP_MINB) k_prep(int32_t n_segs, const i
   }
 }
 
+#ifndef PREP_SPLIT
+#define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels; 0: one k_prep for all degrees
+#endif
+// Per-degree K1: the degree-sorted segments split into the ranges of the sort
+// key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with
+// its own register budget (degree 1-3 need far fewer than degree 5).  bnd[k] =
+// first sorted position with key >= k, k = 0..8.
+__global__ void k_deg_bounds(int32_t n, const int32_t *__restrict__ sdeg, int32_t *__restrict__ bnd) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > n) return;
+  const int prev = p ? (sdeg[p - 1] & 7) : -1;
+  const int cur = p < n ? (sdeg[p] & 7) : 8;
+  for (int k = prev + 1; k <= cur; ++k) bnd[k] = p;
+}
+
+#ifndef PREP_DEG_MINB
+#define PREP_DEG_MINB 1
+#endif
+template <int N>
+__global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *__restrict__ bnd, const int32_t *__restrict__ deg,
+                                                  const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
+                                                  const double *__restrict__ w, SegPrep *__restrict__ prep,
+                                                  uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
+  const int lo = bnd[N], hi = bnd[N + 1];
+  for (int p = lo + blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += gridDim.x * blockDim.x) {
+    const int s = order[p];
+    if (deg[s] == N) {
+      prep_n<N>(ctrl, w, coff[s], prep + s, serr + s);
+    } else {   // a degree outside 1..5 with these low bits (rejected on the host)
+      serr[s] = 1;
+      double2 *o2 = reinterpret_cast<double2 *>(prep + s);
+      for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// keys 0, 6, 7: degrees outside 1..5 only
+__global__ void k_prep_bad(const int32_t *__restrict__ bnd, SegPrep *__restrict__ prep, uint8_t *__restrict__ serr,
+                           const int32_t *__restrict__ order) {
+  const int n0 = bnd[1] - bnd[0], n1 = bnd[8] - bnd[6];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1; i += gridDim.x * blockDim.x) {
+    const int s = order[i < n0 ? bnd[0] + i : bnd[6] + (i - n0)];
+    serr[s] = 1;
+    double2 *o2 = reinterpret_cast<double2 *>(prep + s);
+    for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+  }
+}
+
 __global__ void k_iota(int32_t n, int32_t *__restrict__ a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
@@ -1711,9 +1759,23 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(D.alloc(&dt, tmp));
     cub::DeviceRadixSort::SortPairs(dt, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
     g_build_launches += 4;
+#if PREP_SPLIT
+    int32_t *d_bnd = nullptr;
+    WN_CUDA(D.alloc(&d_bnd, 9));
+    k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
+    const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
+    k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+    k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+    k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+    k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+    k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
+    k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, B.prep, d_serr, d_order);
+    g_build_launches += 7;
+#else
     k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr,
                                                  d_order);
     ++g_build_launches;
+#endif
   }
   if (n_loops) {
     k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, loop_seg_off, B.prep, B.s0pre);

@@ -82,12 +82,14 @@ typedef struct {                 /* [host] */
  *   stream        cudaStream_t (0 = legacy default stream).
  *   out           [host] receives the handle on WN_OK; untouched otherwise.
  *   face_status   [n_faces] DEVICE int32 or NULL: WN_FACE_* per face.
- * The host waits only for the per-loop summaries (topology validation and
- * planning need them); derivative bounds and record emission stay asynchronous
- * on `stream` after the call returns.  The input buffers must therefore stay
- * valid until that work completes: free them in stream order on `stream` (a
- * caching allocator on the same stream) or after synchronising it.  Queries
- * may be issued at once on any stream (wn_query waits for the build's event);
+ * Synchronisation and input lifetime: the call waits on the host
+ * for the device planner's summary (topology validation and the record counts;
+ * errors are returned synchronously) and for the segment-prep kernel, the last
+ * reader of the caller's arrays -- every later step reads library-owned copies
+ * (the lifted control points, CSR copies).  So ALL input buffers may be freed or
+ * overwritten, on any stream, as soon as wn_build_faces returns.  The record
+ * emission itself stays asynchronous on `stream` after the return; queries may
+ * be issued at once on any stream (wn_query waits for the build's event);
  * wn_free_faces orders its frees after the handle's last build/query. */
 wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, const double *ctrl_uv,
                            const double *ctrl_w, const int32_t *seg_degree,
@@ -101,7 +103,8 @@ wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t n_segs, con
  * Bezier segments").  Curve c has degree curve_degree[c] in 1..5, control
  * points ctrl_uv[curve_ctrl_off[c] .. curve_ctrl_off[c+1]) ([.][2] float64),
  * weights ctrl_w (NULL = polynomial B-splines) and the clamped, non-decreasing
- * knot vector knots[curve_knot_off[c] .. curve_knot_off[c+1]) with
+ * knot vector knots[curve_knot_off[c] .. curve_knot_off[c+1]) (exactly p+1
+ * equal knots at each end) with
  * n_knots(c) = n_ctrl(c) + p + 1 and interior multiplicities <= p.  Every
  * interior knot span of positive length becomes one Bezier segment of the
  * curve's degree; the curve's two end points are copied bit-exactly (the
@@ -186,6 +189,8 @@ typedef struct {
   int64_t bytes;         /* device bytes owned by the handle */
   int32_t precision;     /* 0 fp64, 1 fp32 */
   int32_t max_face_records;
+  int64_t n_copy_groups; /* extended-copy groups (Eq. 5 copies of non-contractible loops) */
+  int64_t n_bands;       /* Eq. 8 bands emitted for bi-periodic pairs: line pairs */
 } wn_faces_info_t;
 
 wn_status_t wn_faces_info(wn_faces_t faces, wn_faces_info_t *out /* [host] */);

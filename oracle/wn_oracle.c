@@ -659,6 +659,10 @@ int orc_nurbs_decompose(int p, int n_ctrl, const double *P, const double *w, con
   for (int i = 0; i + 1 < nk; i++) if (!(U[i] <= U[i + 1])) return -1;
   for (int i = 1; i <= p; i++) if (U[i] != U[0] || U[nk - 1 - i] != U[nk - 1]) return -1;
   if (!(U[p] < U[nk - 1 - p])) return -1;
+  /* clamped means EXACTLY p+1 equal end knots (a (p+2)-fold end knot is not a
+   * clamped knot vector of this degree: the Bezier form's end points would no
+   * longer be P_0 / P_n) */
+  if (U[p + 1] == U[p] || U[nk - 2 - p] == U[nk - 1 - p]) return -1;
   for (int i = p + 1; i < nk - 1 - p; i++) {        /* interior multiplicity <= p */
     int s = 1;
     while (i + s < nk - 1 - p && U[i + s] == U[i]) s++;

@@ -50,7 +50,7 @@ class Options(C.Structure):
 class FacesInfo(C.Structure):
     _fields_ = [("n_records", C.c_int64), ("n_seg_records", C.c_int64), ("n_groups", C.c_int64),
                 ("n_lines", C.c_int64), ("bytes", C.c_int64), ("precision", C.c_int32),
-                ("max_face_records", C.c_int32)]
+                ("max_face_records", C.c_int32), ("n_copy_groups", C.c_int64), ("n_bands", C.c_int64)]
 
 
 def lib_path():

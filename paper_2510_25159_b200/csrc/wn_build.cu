@@ -367,7 +367,8 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
                                               const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
                                               const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
                                               const double *__restrict__ ctrl, const double *__restrict__ wts,
-                                              int2 *__restrict__ shift, uint8_t *__restrict__ brk,
+                                              double *__restrict__ lctrl, double *__restrict__ lw,
+                                              uint8_t *__restrict__ brk,
                                               int2 *__restrict__ chain, double2 *__restrict__ lend,
                                               LoopInfo *__restrict__ info) {
   // one warp per loop; lanes take its segments 32 at a time.  The lattice
@@ -469,7 +470,17 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
     cxr = __shfl_sync(0xffffffffu, xe, cnt - 1);
     cyr = __shfl_sync(0xffffffffu, ye, cnt - 1);
     if (in) {
-      shift[s] = make_int2(ku, kv);
+      // the lifted control points and weights: library-owned copies that the
+      // record emission reads (the caller's arrays are not read after the
+      // build returns, include/wn.h)
+      const int n = deg[s], o = coff[s];
+      if (n >= 1 && n <= 5)
+        for (int j = 0; j <= n; ++j) {
+          const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1];
+          lctrl[2 * (o + j)] = pu ? lat(x, ku, Tu) : x;
+          lctrl[2 * (o + j) + 1] = pv ? lat(y, kv, Tv) : y;
+          if (wts) lw[o + j] = wts[o + j];
+        }
       brk[s] = bk;
       // lifted box and end point: lat() is monotone, so it commutes with min/max
       bx0 = pu ? lat(bx0, ku, Tu) : bx0; bx1 = pu ? lat(bx1, ku, Tu) : bx1;
@@ -678,7 +689,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
                        const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
                        const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
                        const double *__restrict__ wts, const SegPrep *__restrict__ prep,
-                       const int2 *__restrict__ shift, const uint8_t *__restrict__ brk,
+                       const uint8_t *__restrict__ brk,
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const double2 *__restrict__ lend,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
@@ -693,9 +704,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
   const double Tu = face_dom[4 * f + 1], Tv = face_dom[4 * f + 3];
   const LoopInfo I = info[l];
   const uint32_t fa = (G.flags & PF_ANGLE) ? F_ANGLE : 0u;
-  // lifted + translated coordinate (two exact-op steps: lift, then translate)
-  auto X = [&](double x, int ks) { return pu ? lat(lat(x, ks, Tu), G.ku, Tu) : x; };
-  auto Y = [&](double y, int ks) { return pv ? lat(lat(y, ks, Tv), G.kv, Tv) : y; };
+  // `ctrl` / `wts` are the LIFTED control points written by k_lift (lat(x,
+  // k_s, T) per segment); translated coordinate of this group's copy:
   auto TX = [&](double x) { return pu ? lat(x, G.ku, Tu) : x; };
   auto TY = [&](double y) { return pv ? lat(y, G.kv, Tv) : y; };
   if (G.kind == G_LINE) {
@@ -761,12 +771,10 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     const int idx = s - s0;
     const int n = deg[s];
     const int o = coff[s];
-    const int2 k = shift[s];
     // end points (the interior control points are re-read pair by pair below,
     // keeping few values live: occupancy of this latency-bound scatter)
-    // (scalar loads: the caller's ctrl_uv need only be 8-B aligned)
-    const double px0 = X(ctrl[2 * o], k.x), py0 = Y(ctrl[2 * o + 1], k.y);
-    const double pxn = X(ctrl[2 * (o + n)], k.x), pyn = Y(ctrl[2 * (o + n) + 1], k.y);
+    const double px0 = TX(ctrl[2 * o]), py0 = TY(ctrl[2 * o + 1]);
+    const double pxn = TX(ctrl[2 * (o + n)]), pyn = TY(ctrl[2 * (o + n) + 1]);
     int r;
     if (!tree) {
       r = r_first + idx + nb;
@@ -854,8 +862,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
         if (jj <= n) {
           const double wj = wts ? wts[o + jj] : 1.0;
           const double cw = binom5(n, jj) * wj;
-          cx2[h] = (R)(cw * X(ctrl[2 * (o + jj)], k.x));
-          cy2[h] = (R)(cw * Y(ctrl[2 * (o + jj) + 1], k.y));
+          cx2[h] = (R)(cw * TX(ctrl[2 * (o + jj)]));
+          cy2[h] = (R)(cw * TY(ctrl[2 * (o + jj) + 1]));
           cw2[h] = (R)cw;
         }
       }
@@ -1231,15 +1239,17 @@ struct BuildSummary {
   unsigned long long first_bad;   // (face << 32) | code, minimum over bad faces
   int tot_g, tot_r, tot_c, pad;
   unsigned long long lines, cull;
+  unsigned long long copies, bands;   // extended-copy groups; Eq. 8 bands (line pairs of bi-periodic faces)
 };
 
 struct CountSink {
-  int ng = 0, recs = 0, colds = 0, lines = 0, cull = 0;
+  int ng = 0, recs = 0, colds = 0, lines = 0, cull = 0, copies = 0;
   __device__ void add(int kind, int flags, int, int, int, const LoopInfo &I, double) {
     ++ng;
     recs += group_nrec(kind, flags, I);
     if (kind == G_LINE) ++lines;
     else {
+      if (kind == G_COPY) ++copies;
       colds += I.nseg;
       if (flags & PF_CULL) ++cull;
     }
@@ -1313,6 +1323,8 @@ __global__ void k_plan_count(int32_t n_faces, int32_t n_loops, const int32_t *__
     plan_face(S, L, l0, l1, C, pair_beta, pair_s, tree != 0);
     if (S.lines) atomicAdd(&sum->lines, (unsigned long long)S.lines);
     if (S.cull) atomicAdd(&sum->cull, (unsigned long long)S.cull);
+    if (S.copies) atomicAdd(&sum->copies, (unsigned long long)S.copies);
+    if (C.per == 3 && S.lines) atomicAdd(&sum->bands, (unsigned long long)(S.lines / 2));
     if (S.recs >= (1 << 24) || S.colds >= (1 << 22)) atomicOr(&sum->toobig, 1);
     atomicMax(&sum->maxr, S.recs);
   }
@@ -1414,7 +1426,7 @@ cudaEvent_t g_pin_ev[64] = {};
 bool g_pin_pending[64] = {};
 // per device: the auxiliary stream of the device planner and its fork/join events
 cudaStream_t g_aux[64] = {};
-cudaEvent_t g_ev_lift[64] = {}, g_ev_plan[64] = {}, g_ev_fill[64] = {};
+cudaEvent_t g_ev_lift[64] = {}, g_ev_plan[64] = {}, g_ev_fill[64] = {}, g_ev_k1[64] = {};
 struct PinRelease {
   cudaEvent_t ev;
   bool *pending;
@@ -1466,6 +1478,10 @@ void free_handle(wn_faces_t F) {
   delete F;
 }
 
+// Everything the emission (and the pairing probes) reads is library-owned:
+// ctrl / w are the lifted copies written by k_lift, deg / lso / flo copies of
+// the caller's arrays, per / dom the handle's face arrays.  The caller's
+// buffers are read only by work that completes before wn_build_faces returns.
 struct BuildCtx {
   int32_t n_faces, n_loops, n_segs;
   const double *ctrl, *w;
@@ -1474,7 +1490,6 @@ struct BuildCtx {
   const double *dom;
   int32_t *coff, *loop_face;
   SegPrep *prep;
-  int2 *shift;
   uint8_t *brk;
   int2 *chain;      // per segment: (chain start index within its loop, chain length)
   double *s0pre;    // per segment: prefix sum of root spans S0 along its loop
@@ -1483,6 +1498,43 @@ struct BuildCtx {
   cudaStream_t st;
 };
 
+// K1 launch, shared by wn_build_faces and wn_segment_prep: segments sorted by
+// degree (3-bit radix sort), then one kernel per degree over its range of the
+// sorted order, each with its own register budget (PREP_SPLIT; 0 = one k_prep).
+cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, const double *ctrl, const double *w,
+                      SegPrep *prep, uint8_t *serr, DevBuf &D, cudaStream_t st) {
+  if (n_segs <= 0) return cudaSuccess;
+  int32_t *d_iota = nullptr, *d_order = nullptr, *d_degs = nullptr;
+  cudaError_t e;
+  if ((e = D.alloc(&d_iota, n_segs)) != cudaSuccess) return e;
+  if ((e = D.alloc(&d_order, n_segs)) != cudaSuccess) return e;
+  if ((e = D.alloc(&d_degs, n_segs)) != cudaSuccess) return e;
+  k_iota<<<(n_segs + 255) / 256, 256, 0, st>>>(n_segs, d_iota);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, deg, d_degs, d_iota, d_order, n_segs, 0, 3, st);
+  char *dt = nullptr;
+  if ((e = D.alloc(&dt, tmp)) != cudaSuccess) return e;
+  cub::DeviceRadixSort::SortPairs(dt, tmp, deg, d_degs, d_iota, d_order, n_segs, 0, 3, st);
+  g_build_launches += 4;
+#if PREP_SPLIT
+  int32_t *d_bnd = nullptr;
+  if ((e = D.alloc(&d_bnd, 9)) != cudaSuccess) return e;
+  k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
+  const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
+  k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
+  k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
+  k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
+  k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
+  k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
+  k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, prep, serr, d_order);
+  g_build_launches += 7;
+#else
+  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, deg, coff, ctrl, w, prep, serr, d_order);
+  ++g_build_launches;
+#endif
+  return cudaGetLastError();
+}
+
 // K2c launch over `ng` device PlanGroups into F's record buffers
 template <typename R>
 cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces_t F) {
@@ -1490,7 +1542,7 @@ cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces
   const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
   ++g_build_launches;
   k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, B.st>>>(
-      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl, B.w, B.prep, B.shift, B.brk, B.chain,
+      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl, B.w, B.prep, B.brk, B.chain,
       B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, (Cold<R> *)F->cold,
       std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
   return cudaGetLastError();
@@ -1610,6 +1662,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(cudaEventCreateWithFlags(&g_ev_lift[dev], cudaEventDisableTiming));
     WN_CUDA(cudaEventCreateWithFlags(&g_ev_plan[dev], cudaEventDisableTiming));
     WN_CUDA(cudaEventCreateWithFlags(&g_ev_fill[dev], cudaEventDisableTiming));
+    WN_CUDA(cudaEventCreateWithFlags(&g_ev_k1[dev], cudaEventDisableTiming));
     WN_CUDA(cudaStreamCreateWithFlags(&g_aux[dev], cudaStreamNonBlocking));
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -1632,17 +1685,27 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(cudaMemcpyAsync(h_per, face_periodic, n_faces, cudaMemcpyDeviceToHost, st));
     WN_CUDA(cudaMemcpyAsync(h_dom, face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st));
   }
+  // --- library copies of the caller's CSR / degree arrays (the caller may free
+  // or overwrite every input as soon as this call returns, include/wn.h) ---
+  BuildCtx B{};
+  B.n_faces = n_faces; B.n_loops = n_loops; B.n_segs = n_segs; B.st = st;
+  {
+    int32_t *c_deg = nullptr, *c_lso = nullptr, *c_flo = nullptr;
+    WN_CUDA(D.alloc(&c_deg, n_segs));
+    WN_CUDA(D.alloc(&c_lso, n_loops + 1));
+    WN_CUDA(D.alloc(&c_flo, n_faces + 1));
+    if (n_segs) WN_CUDA(cudaMemcpyAsync(c_deg, seg_degree, sizeof(int32_t) * n_segs, cudaMemcpyDeviceToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(c_lso, loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToDevice, st));
+    WN_CUDA(cudaMemcpyAsync(c_flo, face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToDevice, st));
+    B.deg = c_deg; B.lso = c_lso; B.flo = c_flo;
+  }
   // --- K0: degrees -> control offsets ---
   int32_t *d_cnt = nullptr, *d_bad = nullptr;
-  BuildCtx B{};
-  B.n_faces = n_faces; B.n_loops = n_loops; B.n_segs = n_segs;
-  B.ctrl = ctrl_uv; B.w = ctrl_w; B.deg = seg_degree; B.lso = loop_seg_off; B.flo = face_loop_off;
-  B.per = face_periodic; B.dom = face_domain; B.st = st;
   WN_CUDA(D.alloc(&d_cnt, n_segs + 1));
   WN_CUDA(D.alloc(&d_bad, 1));
   WN_CUDA(D.alloc(&B.coff, n_segs + 1));
   WN_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), st));
-  k_deg<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, seg_degree, d_cnt, d_bad);
+  k_deg<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, B.deg, d_cnt, d_bad);
   g_build_launches += 3;   // k_deg + cub scan (init + scan)
   {
     size_t tmp = 0;
@@ -1655,10 +1718,14 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   tr.mark("csr copies + degree scan (async)");
   // --- K1 prep, loop->face, K2a lift ---
   uint8_t *d_serr = nullptr;
+  double *d_lctrl = nullptr, *d_lw = nullptr;   // lifted control points / weights (k_lift): <= 6 per segment
   WN_CUDA(D.alloc(&B.prep, n_segs));
   WN_CUDA(D.alloc(&d_serr, n_segs));
   WN_CUDA(D.alloc(&B.loop_face, n_loops));
-  WN_CUDA(D.alloc(&B.shift, n_segs));
+  WN_CUDA(D.alloc(&d_lctrl, 12 * (size_t)n_segs));
+  if (ctrl_w) WN_CUDA(D.alloc(&d_lw, 6 * (size_t)n_segs));
+  B.ctrl = d_lctrl;
+  B.w = d_lw;
   WN_CUDA(D.alloc(&B.brk, n_segs));
   WN_CUDA(D.alloc(&B.chain, n_segs));
   WN_CUDA(D.alloc(&B.s0pre, n_segs));
@@ -1672,11 +1739,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(cudaEventRecord(g_ev_lift[dev], st));
   WN_CUDA(cudaStreamWaitEvent(st2, g_ev_lift[dev], 0));
   if (n_loops) WN_CUDA(cudaMemsetAsync(B.loop_face, 0xFF, sizeof(int32_t) * n_loops, st2));
-  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, face_loop_off, B.loop_face);
+  if (n_faces) k_loop_face<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, B.flo, B.loop_face);
   if (n_loops)
-    k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st2>>>(n_loops, n_faces, n_segs, loop_seg_off, B.loop_face, face_periodic,
-                                                                       face_domain, seg_degree, B.coff, ctrl_uv, ctrl_w,
-                                                                       B.shift, B.brk, B.chain, B.lend, B.info);
+    k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st2>>>(n_loops, n_faces, n_segs, B.lso, B.loop_face, face_periodic,
+                                                                       face_domain, B.deg, B.coff, ctrl_uv, ctrl_w,
+                                                                       d_lctrl, d_lw, B.brk, B.chain, B.lend, B.info);
   g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st2); tr.mark("(trace) k_loop_face + k_lift"); }
@@ -1699,7 +1766,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(cache_alloc((void **)&F->face_ok, nf1, st2));
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * nf1, st2));
   WN_CUDA(cache_alloc((void **)&F->face_box, sizeof(float4) * nf1, st2));
-  WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st2));
+  WN_CUDA(cache_alloc((void **)&F->counters, 16 * sizeof(unsigned long long), st2));
+  // the emission reads the handle's face arrays (written by k_plan_count:
+  // periodicity bits, domain with non-periodic axes zeroed) -- library-owned
+  B.per = F->face_per;
+  B.dom = F->face_dom;
   int32_t *d_status = face_status;
   if (!d_status) WN_CUDA(D2.alloc(&d_status, nf1));
   int4 *d_cnt4 = nullptr, *d_off4 = nullptr;
@@ -1725,7 +1796,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     WN_CUDA(cudaMemsetAsync(&d_sum->first_bad, 0xFF, sizeof(unsigned long long), st2));
     if (n_faces) {
       k_plan_count<<<(n_faces + 127) / 128, 128, 0, st2>>>(
-          n_faces, n_loops, face_loop_off, face_periodic, face_domain, B.info, angle ? 1 : 0, O.strict ? 1 : 0,
+          n_faces, n_loops, B.flo, face_periodic, face_domain, B.info, angle ? 1 : 0, O.strict ? 1 : 0,
           O.hierarchy ? 1 : 0, fp32 ? 1 : 0, pair_beta, pair_s, d_status, F->face_per, F->face_dom, F->face_M,
           F->face_box, d_cnt4, d_okey, d_oval, d_sum);
       k_plan_scan<<<1, PLAN_SCAN_T, 0, st2>>>(n_faces, d_cnt4, d_off4, F->face_rec_off, F->face_cold_off, d_sum);
@@ -1745,50 +1816,23 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     wn_status_t rc = plan_pass(nullptr, nullptr);
     if (rc != WN_OK) return rc;
   }
-  // segments sorted by degree so that k_prep's warps run one degree variant
-  int32_t *d_order = nullptr;
-  if (n_segs) {
-    int32_t *d_iota = nullptr, *d_degs = nullptr;
-    WN_CUDA(D.alloc(&d_iota, n_segs));
-    WN_CUDA(D.alloc(&d_order, n_segs));
-    WN_CUDA(D.alloc(&d_degs, n_segs));
-    k_iota<<<(n_segs + 255) / 256, 256, 0, st>>>(n_segs, d_iota);
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
-    char *dt = nullptr;
-    WN_CUDA(D.alloc(&dt, tmp));
-    cub::DeviceRadixSort::SortPairs(dt, tmp, seg_degree, d_degs, d_iota, d_order, n_segs, 0, 3, st);
-    g_build_launches += 4;
-#if PREP_SPLIT
-    int32_t *d_bnd = nullptr;
-    WN_CUDA(D.alloc(&d_bnd, 9));
-    k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
-    const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
-    k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-    k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-    k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-    k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-    k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, d_order);
-    k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, B.prep, d_serr, d_order);
-    g_build_launches += 7;
-#else
-    k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr,
-                                                 d_order);
-    ++g_build_launches;
-#endif
-  }
+  // K1 (reads the caller's control points: the host waits for g_ev_k1 before returning)
+  WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, D, st));
   if (n_loops) {
-    k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, loop_seg_off, B.prep, B.s0pre);
+    k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, B.lso, B.prep, B.s0pre);
     ++g_build_launches;
   }
   WN_CUDA(cudaGetLastError());
+  WN_CUDA(cudaEventRecord(g_ev_k1[dev], st));
   if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep + k_s0pre"); }
   WN_CUDA(cudaEventSynchronize(g_ev_plan[dev]));
   tr.mark("device plan summary");
   // CSR / domain checks on the host (the kernels above clamp every CSR index,
-  // so a bad input is reported here without any out-of-bounds access)
+  // so a bad input is reported here without any out-of-bounds access).  An
+  // error return also waits for K1 (it reads the caller's arrays).
   auto fail = [&](wn_status_t rc) {
     cudaStreamSynchronize(st2);
+    cudaEventSynchronize(g_ev_k1[dev]);
     return rc;
   };
   bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
@@ -2046,16 +2090,25 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   F->n_seg = h_sum->tot_c;
   F->n_lines = (int64_t)h_sum->lines;
   F->n_groups = (int64_t)h_sum->cull;
+  F->n_copy_groups = (int64_t)h_sum->copies;
+  F->n_bands = (int64_t)h_sum->bands;
   F->max_face_records = h_sum->maxr;
   WN_CUDA(cache_alloc(&F->hot, (fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * (size_t)std::max(h_sum->tot_r, 1), st));
   WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * (size_t)std::max(h_sum->tot_c, 1), st));
   F->bytes = (int64_t)(fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * h_sum->tot_r +
              (int64_t)(fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * h_sum->tot_c + (int64_t)n_faces * 50;
   const int ng = h_sum->tot_g;
+  // the plan groups: written by k_plan_fill on st2, read by k_emit on st --
+  // released on st (after k_emit), not with the auxiliary stream's buffers
   PlanGroup *d_groups = nullptr;
-  WN_CUDA(D2.alloc(&d_groups, std::max(ng, 1)));
+  WN_CUDA(cache_alloc((void **)&d_groups, sizeof(PlanGroup) * (size_t)std::max(ng, 1), st2));
+  struct GroupsRelease {
+    void *p;
+    cudaStream_t st;
+    ~GroupsRelease() { cache_free(p, st); }
+  } groups_release{d_groups, st};
   if (ng) {
-    k_plan_fill<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, face_loop_off, F->face_per, F->face_dom,
+    k_plan_fill<<<(n_faces + 127) / 128, 128, 0, st2>>>(n_faces, n_loops, B.flo, F->face_per, F->face_dom,
                                                         F->face_M, B.info, angle ? 1 : 0, O.hierarchy ? 1 : 0,
                                                         d_pair_beta, d_pair_s, d_off4, d_groups);
     ++g_build_launches;
@@ -2065,6 +2118,10 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   WN_CUDA(cudaStreamWaitEvent(st, g_ev_fill[dev], 0));   // join: K2c after the plan and after K1
   WN_CUDA(fp32 ? launch_emit<float>(B, ng, d_groups, F) : launch_emit<double>(B, ng, d_groups, F));
   tr.mark("device plan fill + emit (enqueued)");
+  // K1 is the last reader of the caller's buffers (k_emit reads the library's
+  // lifted copies): once it is done the inputs may be freed (include/wn.h).
+  // The emission is already queued behind it, so this wait leaves no gap.
+  WN_CUDA(cudaEventSynchronize(g_ev_k1[dev]));
   // no final synchronisation: the handle's records are complete in stream
   // order, so queries enqueued on `stream` after this call see them
   {
@@ -2110,10 +2167,12 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
   WN_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   WN_CUDA(cudaStreamSynchronize(st));
   if (h_bad) { set_error("wn_segment_prep: segment degree outside 1..5"); return WN_ERR_ARG; }
-  // k_prep writes 16-B vectors: stage through an aligned buffer if needed
+  // K1 writes 16-B vectors: stage through an aligned buffer if needed.  The
+  // same launch sequence as wn_build_faces (launch_k1), so the bound tests
+  // through this entry point cover the shipped K1 code.
   SegPrep *dst = (SegPrep *)out;
   if ((uintptr_t)out & 15) WN_CUDA(D.alloc(&dst, n_segs));
-  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, dst, serr, nullptr);
+  WN_CUDA(launch_k1(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, dst, serr, D, st));
   if ((void *)dst != (void *)out)
     WN_CUDA(cudaMemcpyAsync(out, dst, sizeof(SegPrep) * (size_t)n_segs, cudaMemcpyDeviceToDevice, st));
   WN_CUDA(cudaGetLastError());
@@ -2130,6 +2189,8 @@ extern "C" wn_status_t wn_faces_info(wn_faces_t F, wn_faces_info_t *out) {
   out->bytes = F->bytes;
   out->precision = F->precision;
   out->max_face_records = F->max_face_records;
+  out->n_copy_groups = F->n_copy_groups;
+  out->n_bands = F->n_bands;
   return WN_OK;
 }
 

@@ -213,7 +213,7 @@ struct wn_faces_s {
   int timing_on = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k3_events;
   std::vector<cudaEvent_t> k3_mid;   // after phase 1 (k_phase1) of each timed query
-  int64_t n_records = 0, n_seg = 0, n_groups = 0, n_lines = 0, bytes = 0;
+  int64_t n_records = 0, n_seg = 0, n_groups = 0, n_lines = 0, bytes = 0, n_copy_groups = 0, n_bands = 0;
   int32_t max_face_records = 0;
 };
 

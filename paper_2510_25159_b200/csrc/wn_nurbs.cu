@@ -20,7 +20,7 @@ namespace wn {
 
 namespace {
 
-// Validation + segment count of one curve: clamped (p+1 equal end knots),
+// Validation + segment count of one curve: clamped (exactly p+1 equal end knots),
 // non-decreasing, U[p] < U[m-p], interior multiplicity <= p, finite data,
 // positive weights.  Segments = distinct interior knot values + 1.
 __global__ void k_nurbs_count(int32_t n_curves, int32_t n_ctrl_total, int32_t n_knots_total,
@@ -43,6 +43,9 @@ __global__ void k_nurbs_count(int32_t n_curves, int32_t n_ctrl_total, int32_t n_
   for (int i = 0; i < nk; ++i) ok &= isfinite(U[i]) && (i == 0 || U[i - 1] <= U[i]);
   for (int i = 1; i <= p && ok; ++i) ok &= U[i] == U[0] && U[nk - 1 - i] == U[nk - 1];
   ok &= U[p] < U[nk - 1 - p];
+  // exactly p+1 equal end knots: a (p+2)-fold end knot would be counted as an
+  // interior knot here while the fill sweep runs into the end knots
+  ok &= U[p + 1] != U[p] && U[nk - 2 - p] != U[nk - 1 - p];
   int count = 1;
   for (int i = p + 1; i < nk - 1 - p && ok;) {
     int s = 1;

@@ -456,7 +456,17 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   auto flush = [&]() {
     __syncwarp();
     int b = 0;
-    if (lane == 0) b = atomicAdd(P.hq_count, hn_);
+    if (lane == 0) {
+      // saturating reservation: once the queue is full the counter only
+      // moves to cap + 1 (marks the overflow for k_overflow), so it can never
+      // wrap however many pairs a batch attempts
+      if (*reinterpret_cast<volatile int32_t *>(P.hq_count) >= P.hq_cap) {
+        b = P.hq_cap;
+        atomicMax(P.hq_count, P.hq_cap + 1);
+      } else {
+        b = atomicAdd(P.hq_count, hn_);
+      }
+    }
     b = __shfl_sync(0xffffffffu, b, 0);
     bool ovf = false;
     for (int i = lane; i < hn_; i += 32) {
@@ -1317,7 +1327,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   // amortise the CTA prologue and the record staging over several sub-tiles,
   // small ones keep >= ~4 waves of CTAs
   int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
-  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(64, atoi(s)));
+  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(16, atoi(s)));   // <= 16: a unit <= 4096 queries (12-bit rank in the regrouping key)
   const int qu = QT * sub;
   const int64_t max_tiles64 = (n + qu - 1) / qu + nf;
   if (n > INT32_MAX - 1 || max_tiles64 > INT32_MAX) {
@@ -1426,7 +1436,7 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
     return WN_ERR_ARG;
   }
   int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
-  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(64, atoi(s)));
+  if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(16, atoi(s)));   // <= 16: a unit <= 4096 queries (12-bit rank in the regrouping key)
   const int qu = QT * sub;
   const int tpg = (int)((G + qu - 1) / qu);
   const int64_t max_tiles64 = (int64_t)n_grid * tpg;

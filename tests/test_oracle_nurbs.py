@@ -114,3 +114,18 @@ def test_generated_nurbs_faces_closed_integral():
     assert set(np.round(r["w"][cm]).astype(int)) <= {0, 1}
     centre = oracle.query(bz, face_id=np.arange(12, dtype=np.int32), uv=np.tile([[0.5, 0.5]], (12, 1)))
     assert np.all(centre["w"].round() == 1)
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_overclamped_end_knot_rejected(p):
+    """A (p+2)-fold end knot is not a clamped knot vector of degree p (the
+    curve's end points would not be P_0 / P_n): rejected, not decomposed into
+    a bogus extra segment (e.g. p=1, U=[0,0,1,1,1])."""
+    if p == 1:
+        P = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0]])
+        U = np.array([0.0, 0.0, 1.0, 1.0, 1.0])
+    else:
+        P = np.random.default_rng(3).uniform(-1, 1, size=(6, 2))
+        U = np.array([0.0, 0.0, 0.0, 0.0, 0.0, 0.5, 1.0, 1.0, 1.0, 1.0])   # 5-fold start knot
+    with pytest.raises(ValueError):
+        oracle.nurbs_decompose(p, P, None, U)

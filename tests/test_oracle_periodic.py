@@ -87,8 +87,14 @@ def test_bi_periodic_strip(case, shift_beta):
     assert r["w"][0] == pytest.approx(case["omega"], abs=1e-12)
 
 
-def test_eq5_N_vs_2N_and_tile_periodicity():
-    wl = G.gen_c5(n_faces=30, grid=6)
+@pytest.mark.parametrize("exact", [True, False])
+def test_eq5_N_vs_2N_and_tile_periodicity(exact):
+    """exact=False: generic fp64 periodic data (T = 2 pi as a plain double,
+    segments stored at random lattice translates): lifted junctions at seam
+    crossings are not bit-continuous, the loops' closures carry ulp-size
+    defects; Eq. 5 still converges and values stay integers to ~1e-12 away
+    from the curves."""
+    wl = G.gen_c5(n_faces=30, grid=6, exact=exact, store_jitter=0 if exact else 2)
     per = np.nonzero(wl["face_periodic"])[0]
     assert len(per) >= 3
     m = np.isin(wl["face_id"], per)
@@ -97,14 +103,14 @@ def test_eq5_N_vs_2N_and_tile_periodicity():
     r2 = oracle.query(wl, face_id=fid, uv=q, N5=8)
     ok = r1["comparable"] & r2["comparable"]
     assert ok.mean() > 0.9
-    assert np.max(np.abs(r1["w"][ok] - r2["w"][ok])) < 1e-13
+    assert np.max(np.abs(r1["w"][ok] - r2["w"][ok])) < (1e-13 if exact else 1e-11)
     # tile periodicity: the unreduced point one period away gives the same value
     T = wl["face_domain"][fid, 1]
     r3 = oracle.query(wl, face_id=fid, uv=q + np.stack([T, 0 * T], 1), reduce=False)
     ok &= r3["comparable"]
     assert np.max(np.abs(r1["w"][ok] - r3["w"][ok])) < 1e-9
     # and every comparable value is an integer (closed / balanced loops)
-    assert np.max(np.abs(r1["w"][ok] - np.round(r1["w"][ok]))) < 1e-12
+    assert np.max(np.abs(r1["w"][ok] - np.round(r1["w"][ok]))) < (1e-12 if exact else 1e-10)
 
 
 def test_c3_pairing_finds_proper_translate():
@@ -134,11 +140,16 @@ def _graph_v(segs, u, T):
     raise RuntimeError
 
 
-def test_c3_torus_closed_form():
+@pytest.mark.parametrize("exact", [True, False])
+def test_c3_torus_closed_form(exact):
     """C3 analytic classification: inside iff in the band between
     alpha (v = f_a(u)) and the proper translate of beta (v = f_b(u) + T),
-    modulo the lattice, minus the two CW holes, plus the CCW island."""
-    wl = G.gen_c3(n_queries=600)
+    modulo the lattice, minus the two CW holes, plus the CCW island.
+    exact=False: generic fp64 data (T = 2 pi plain, random storage translates;
+    lifted junctions not bit-continuous): the ulp-size gaps perturb the value
+    by at most ~defect / (2 pi distance), so the pin uses a 1e-5 margin and a
+    1e-9 tolerance there."""
+    wl = G.gen_c3(n_queries=600, exact=exact, store_jitter=0 if exact else 2)
     meta = wl["meta"]
     T = meta["T"]
     rng = np.random.default_rng(5)
@@ -159,8 +170,8 @@ def test_c3_torus_closed_form():
             marg = min(marg, abs(d - rad))
             if d < rad:
                 total += orient
-        if marg > 1e-7 and r["comparable"][i]:
-            assert abs(r["w"][i] - total) < 1e-12, (p, r["w"][i], total)
+        if marg > (1e-7 if exact else 1e-5) and r["comparable"][i]:
+            assert abs(r["w"][i] - total) < (1e-12 if exact else 1e-9), (p, r["w"][i], total)
             n_ok += 1
     assert n_ok > 550
 
@@ -196,8 +207,10 @@ def _band_f(segs, tau, a0, v, nu0):
     raise RuntimeError(tau)
 
 
-@pytest.mark.parametrize("pq,T", [((2, 1), None), ((3, 2), None), ((1, -2), None), ((2, 3), (2 * math.pi, math.pi))])
-def test_c3pq_general_class_closed_form(pq, T):
+@pytest.mark.parametrize("pq,T,exact", [((2, 1), None, True), ((3, 2), None, True), ((1, -2), None, True),
+                                        ((2, 3), (2 * math.pi, math.pi), True), ((3, -2), None, False),
+                                        ((2, 3), (2 * math.pi, math.pi), False)])
+def test_c3pq_general_class_closed_form(pq, T, exact):
     """General bi-periodic class (p,q) (Prop. 2, Eq. 8):
     the face interior is the band between alpha and the proper translate of
     beta, modulo the lattice, minus two CW holes plus one CCW island.  Band
@@ -205,7 +218,7 @@ def test_c3pq_general_class_closed_form(pq, T):
     the loops as graphs over tau -- independent of the oracle's Eq. 5/8 sums."""
     p, q = pq
     kw = {} if T is None else dict(Tu=T[0], Tv=T[1])
-    wl = G.gen_c3pq(p=p, q=q, n_queries=250, **kw)
+    wl = G.gen_c3pq(p=p, q=q, n_queries=250, exact=exact, store_jitter=0 if exact else 2, **kw)
     meta = wl["meta"]
     Tu, Tv, v, a0 = meta["Tu"], meta["Tv"], meta["v"], meta["a0"]
     s = float(np.linalg.norm(meta["w"]))
@@ -237,8 +250,8 @@ def test_c3pq_general_class_closed_form(pq, T):
             marg = min(marg, abs(d - rad))
             if d < rad:
                 total += orient
-        if marg > 1e-7 and r["comparable"][k]:
-            assert abs(r["w"][k] - total) < 1e-12, (x, r["w"][k], total)
+        if marg > (1e-7 if exact else 1e-5) and r["comparable"][k]:
+            assert abs(r["w"][k] - total) < (1e-12 if exact else 1e-9), (x, r["w"][k], total)
             n_ok += 1
     assert n_ok > 230
 

@@ -20,12 +20,19 @@ Layout of a workload dict (all numpy, C-contiguous):
   uv            float64 [nq, 2]
   meta          dict    generator-side facts used by analytic pins
 
-Periodic faces: every control point and the periods are quantised to the
-dyadic grid 2^-40 (Q40).  All lattice translates x + k*T are then exact in
-double arithmetic, so lifting and copy emission reproduce junction points
-bit-for-bit on every side (reading R25).  Loops are stored
-seam-discontinuously: each segment is translated by the lattice
-vector that puts its first control point into the fundamental domain.
+Periodic faces (C3, C3pq, the periodic C5 faces) come in two storage modes:
+  exact=True  (default) every control point and the periods are quantised to
+              the dyadic grid 2^-40 (Q40).  All lattice translates x + k*T are
+              then exact in double arithmetic, so lifting and copy emission
+              reproduce junction points bit-for-bit (reading R25).
+  exact=False generic fp64 data: T = 2*pi (and pi) as plain doubles, control
+              points unquantised.  Storing a segment translated by -k*T and
+              lifting it back by +k*T rounds, so the junctions at seam
+              crossings are NOT bit-continuous after lifting (the chain-break
+              path of the library, reading R25).
+Loops are stored seam-discontinuously: each segment is translated
+by the lattice vector that puts its first control point into the fundamental
+domain.
 """
 from __future__ import annotations
 
@@ -43,6 +50,18 @@ def quant(x):
 
 TWO_PI_Q = float(quant(2.0 * math.pi))   # quantised period used for "2*pi" domains
 PI_Q = float(quant(math.pi))
+
+
+def _qz(exact):
+    """Coordinate rounding of a periodic generator: Q40 (exact=True) or none."""
+    if exact:
+        return quant
+    return lambda x: np.asarray(x, dtype=np.float64)
+
+
+def _periods(exact):
+    """(2*pi, pi): Q40-quantised (exact=True) or the plain doubles."""
+    return (TWO_PI_Q, PI_Q) if exact else (2.0 * math.pi, math.pi)
 
 EPS_FP64 = 1e-10   # SURVEY R1
 EPS_FP32 = 1e-6
@@ -160,35 +179,48 @@ def _circle_arcs(c, r, ccw=True):
     return [(a, w.copy()) for a in arcs]
 
 
-def _wrap_store(P, T_u, T_v, per_u, per_v, u0=0.0, v0=0.0):
+def _wrap_store(P, T_u, T_v, per_u, per_v, u0=0.0, v0=0.0, jit=None):
     """Store a lifted segment seam-discontinuously (R18): translate by the lattice
-    vector that puts its first control point into [u0,u0+T) on periodic axes.
-    Exact for Q40-quantised coordinates and periods."""
+    vector that puts its first control point into [u0,u0+T) on periodic axes,
+    plus (jit = (rng, K)) a random extra lattice vector in [-K, K]^2 -- any
+    translate is valid storage (R18).  Exact for Q40-quantised coordinates and
+    periods; rounds once per coordinate otherwise."""
     P = P.copy()
     if per_u:
         k = math.floor((P[0, 0] - u0) / T_u)
+        if jit is not None:
+            k += int(jit[0].integers(-jit[1], jit[1] + 1))
         P[:, 0] = P[:, 0] - k * T_u
     if per_v:
         k = math.floor((P[0, 1] - v0) / T_v)
+        if jit is not None:
+            k += int(jit[0].integers(-jit[1], jit[1] + 1))
         P[:, 1] = P[:, 1] - k * T_v
     return P
 
 
-def _graph_loop(rng, f, u_start, T, direction, n_seg, degs, rational):
+def _jit(seed, store_jitter):
+    """Storage-translate jitter source (its own stream: the geometry stays the
+    same whatever the jitter)."""
+    return None if not store_jitter else (np.random.Generator(np.random.PCG64(10_000 + seed)), int(store_jitter))
+
+
+def _graph_loop(rng, f, u_start, T, direction, n_seg, degs, rational, qz=quant):
     """Non-contractible loop following v = f(u) over one period, as Bezier segments
     whose control points sample the graph (monotone u => a graph).  direction=+1
-    rightward (class (1,0)), -1 leftward (class (-1,0)).  All points Q40-quantised;
-    the loop end equals start + direction*T exactly."""
-    knots_u = quant(u_start + direction * T * np.arange(n_seg + 1) / n_seg)
-    knots_u[-1] = quant(u_start) + direction * T          # exact closure (Q40 arithmetic)
-    knots_v = quant(f(knots_u))
+    rightward (class (1,0)), -1 leftward (class (-1,0)).  qz = quant: all points
+    Q40-quantised, the loop end equals start + direction*T exactly; otherwise
+    the end is start + direction*T rounded once."""
+    knots_u = qz(u_start + direction * T * np.arange(n_seg + 1) / n_seg)
+    knots_u[-1] = qz(u_start) + direction * T          # closure (exact in Q40 arithmetic)
+    knots_v = qz(f(knots_u))
     knots_v[-1] = knots_v[0]
     segs = []
     for k in range(n_seg):
         d = int(degs[k])
         ua, ub = knots_u[k], knots_u[k + 1]
         us = ua + (ub - ua) * np.arange(d + 1) / d
-        P = np.stack([quant(us), quant(f(us))], 1)
+        P = np.stack([qz(us), qz(f(us))], 1)
         P[0] = (ua, knots_v[k])
         P[d] = (ub, knots_v[k + 1])
         w = rng.uniform(0.5, 2.0, size=d + 1) if rational else np.ones(d + 1)
@@ -196,11 +228,11 @@ def _graph_loop(rng, f, u_start, T, direction, n_seg, degs, rational):
     return segs
 
 
-def _hermite_graph_loop(f, fp, u_start, T, direction, n_seg):
+def _hermite_graph_loop(f, fp, u_start, T, direction, n_seg, qz=quant):
     """Cubic Hermite fit to v = f(u) over one period (C3 separation loops)."""
-    knots_u = quant(u_start + direction * T * np.arange(n_seg + 1) / n_seg)
-    knots_u[-1] = quant(u_start) + direction * T
-    knots_v = quant(f(knots_u))
+    knots_u = qz(u_start + direction * T * np.arange(n_seg + 1) / n_seg)
+    knots_u[-1] = qz(u_start) + direction * T
+    knots_v = qz(f(knots_u))
     knots_v[-1] = knots_v[0]
     segs = []
     for k in range(n_seg):
@@ -208,8 +240,8 @@ def _hermite_graph_loop(f, fp, u_start, T, direction, n_seg):
         h = ub - ua
         P0 = np.array([ua, knots_v[k]])
         P3 = np.array([ub, knots_v[k + 1]])
-        P1 = quant(P0 + (h / 3.0) * np.array([1.0, fp(ua)]))
-        P2 = quant(P3 - (h / 3.0) * np.array([1.0, fp(ub)]))
+        P1 = qz(P0 + (h / 3.0) * np.array([1.0, fp(ua)]))
+        P2 = qz(P3 - (h / 3.0) * np.array([1.0, fp(ub)]))
         segs.append((np.stack([P0, P1, P2, P3]), np.ones(4)))
     return segs
 
@@ -317,35 +349,37 @@ def gen_c2(seed=2, n_queries=1_000_000, near_frac=0.10, near_off=1e-6):
 # C3 — bi-periodic torus face (BASELINE configs[2]); layout = SURVEY R21
 # ----------------------------------------------------------------------------
 
-def gen_c3(seed=3, n_queries=1_000_000):
+def gen_c3(seed=3, n_queries=1_000_000, exact=True, store_jitter=0):
     rng = np.random.Generator(np.random.PCG64(seed))
-    T = TWO_PI_Q
+    T, PI_ = _periods(exact)
+    qz = _qz(exact)
     b = _Builder()
     ph_a, ph_b = rng.uniform(0, 2 * math.pi, size=2)
     fa = lambda u: 4.6 + 0.3 * np.sin(u + ph_a)
     fpa = lambda u: 0.3 * math.cos(u + ph_a)
     fb = lambda u: T + 1.7 + 0.3 * np.sin(u + ph_b)      # lifted above alpha
     fpb = lambda u: 0.3 * math.cos(u + ph_b)
-    ua = float(quant(rng.uniform(math.pi, 2 * math.pi)))
-    ub = float(quant(rng.uniform(math.pi, 2 * math.pi)))
+    ua = float(qz(rng.uniform(math.pi, 2 * math.pi)))
+    ub = float(qz(rng.uniform(math.pi, 2 * math.pi)))
     loops = []
-    loops.append(("alpha", _hermite_graph_loop(fa, fpa, ua, T, +1, 24)))
-    loops.append(("beta", _hermite_graph_loop(fb, fpb, ub, T, -1, 24)))
-    loops.append(("H1", [(quant(P), w) for P, w in _circle_arcs(quant([0.0, 0.0]), float(quant(0.6)), ccw=False)]))
-    loops.append(("H2", [(quant(P), w) for P, w in _circle_arcs(quant([PI_Q, 0.0]), float(quant(0.6)), ccw=False)]))
-    loops.append(("I3", [(quant(P), w) for P, w in _circle_arcs(quant([0.0, 3.0]), float(quant(0.5)), ccw=True)]))
+    loops.append(("alpha", _hermite_graph_loop(fa, fpa, ua, T, +1, 24, qz)))
+    loops.append(("beta", _hermite_graph_loop(fb, fpb, ub, T, -1, 24, qz)))
+    loops.append(("H1", [(qz(P), w) for P, w in _circle_arcs(qz([0.0, 0.0]), float(qz(0.6)), ccw=False)]))
+    loops.append(("H2", [(qz(P), w) for P, w in _circle_arcs(qz([PI_, 0.0]), float(qz(0.6)), ccw=False)]))
+    loops.append(("I3", [(qz(P), w) for P, w in _circle_arcs(qz([0.0, 3.0]), float(qz(0.5)), ccw=True)]))
+    jit = _jit(seed, store_jitter)
     for _, segs in loops:
         for P, w in segs:
-            b.seg(_wrap_store(P, T, T, True, True), w)
+            b.seg(_wrap_store(P, T, T, True, True, jit=jit), w)
         b.end_loop()
     b.end_face(periodic=3, domain=(0.0, T, 0.0, T))
     uv = rng.uniform(0.0, 1.0, size=(n_queries, 2)) * T
     uv = np.minimum(uv, np.nextafter(T, 0.0))
-    meta = dict(kind="C3", T=T, ph_a=ph_a, ph_b=ph_b, alpha_v=4.6, beta_v=1.7, amp=0.3,
-                circles=[((0.0, 0.0), float(quant(0.6)), -1), ((PI_Q, 0.0), float(quant(0.6)), -1),
-                         ((0.0, 3.0), float(quant(0.5)), +1)],
+    meta = dict(kind="C3", T=T, ph_a=ph_a, ph_b=ph_b, alpha_v=4.6, beta_v=1.7, amp=0.3, exact=exact,
+                circles=[((0.0, 0.0), float(qz(0.6)), -1), ((PI_, 0.0), float(qz(0.6)), -1),
+                         ((0.0, 3.0), float(qz(0.5)), +1)],
                 alpha_knots=loops[0][1], beta_knots=loops[1][1])
-    return _finish(b, np.zeros(n_queries), uv, True, "C3", meta)
+    return _finish(b, np.zeros(n_queries), uv, True, "C3" if exact else "C3-generic", meta)
 
 
 # ----------------------------------------------------------------------------
@@ -364,26 +398,28 @@ def _band_frame(p, q, Tu, Tv):
     return v, w
 
 
-def _hermite_band_loop(a0, v, w, f, fp, tau0, direction, n_seg):
+def _hermite_band_loop(a0, v, w, f, fp, tau0, direction, n_seg, qz=quant):
     """x(tau) = a0 + tau v + f(tau) w over one period of tau (direction +1: tau0 ->
     tau0+1, class (p,q); -1: class -(p,q)), as cubic Hermite segments with
-    Q40-quantised control points; the end is the start + direction*v exactly."""
+    control points rounded by qz; the end is the start + direction*v (exact in
+    Q40 arithmetic, rounded once otherwise)."""
     taus = tau0 + direction * np.arange(n_seg + 1) / n_seg
     X = lambda t: a0 + t * v + f(t) * w
     dX = lambda t: v + fp(t) * w
-    K = [quant(X(t)) for t in taus]
-    K[-1] = K[0] + direction * v                     # exact closure (Q40 arithmetic)
+    K = [qz(X(t)) for t in taus]
+    K[-1] = K[0] + direction * v                     # closure
     segs = []
     for k in range(n_seg):
         h = taus[k + 1] - taus[k]
         P0, P3 = K[k], K[k + 1]
-        P1 = quant(P0 + (h / 3.0) * dX(taus[k]))
-        P2 = quant(P3 - (h / 3.0) * dX(taus[k + 1]))
+        P1 = qz(P0 + (h / 3.0) * dX(taus[k]))
+        P2 = qz(P3 - (h / 3.0) * dX(taus[k + 1]))
         segs.append((np.stack([P0, P1, P2, P3]), np.ones(4)))
     return segs
 
 
-def gen_c3pq(seed=6, p=2, q=1, n_queries=100_000, Tu=None, Tv=None, n_seg=None, beta_shift=(0, 1)):
+def gen_c3pq(seed=6, p=2, q=1, n_queries=100_000, Tu=None, Tv=None, n_seg=None, beta_shift=(0, 1), exact=True,
+             store_jitter=0):
     """Bi-periodic face whose separation loops alpha / beta have classes (p,q) /
     -(p,q): alpha at band coordinate nu = 0.2 + 0.05 sin(2 pi (2 tau) + phi_a),
     beta at nu = 0.6 + 0.05 sin(...) (the band between them is the interior),
@@ -392,14 +428,16 @@ def gen_c3pq(seed=6, p=2, q=1, n_queries=100_000, Tu=None, Tv=None, n_seg=None, 
     that pairing must find its proper translate.  All loops stored
     seam-discontinuous (R18); queries uniform in the fundamental domain."""
     rng = np.random.Generator(np.random.PCG64(seed))
-    Tu = TWO_PI_Q if Tu is None else float(quant(Tu))
-    Tv = TWO_PI_Q if Tv is None else float(quant(Tv))
+    qz = _qz(exact)
+    T2, _ = _periods(exact)
+    Tu = T2 if Tu is None else float(qz(Tu))
+    Tv = T2 if Tv is None else float(qz(Tv))
     assert math.gcd(abs(p), abs(q)) == 1
     if n_seg is None:
         n_seg = 12 * max(abs(p), abs(q), 1)
     v, w = _band_frame(p, q, Tu, Tv)
     s = float(np.linalg.norm(w))                     # distance per unit nu
-    a0 = quant(rng.uniform(0, 1, size=2) * [Tu, Tv])
+    a0 = qz(rng.uniform(0, 1, size=2) * [Tu, Tv])
     ph_a, ph_b = rng.uniform(0, 2 * math.pi, size=2)
     A = 0.05
     fa = lambda t: 0.2 + A * np.sin(4 * math.pi * t + ph_a)
@@ -407,28 +445,29 @@ def gen_c3pq(seed=6, p=2, q=1, n_queries=100_000, Tu=None, Tv=None, n_seg=None, 
     fb = lambda t: 0.6 + A * np.sin(4 * math.pi * t + ph_b)
     fpb = lambda t: 4 * math.pi * A * math.cos(4 * math.pi * t + ph_b)
     tb = float(rng.uniform(0, 1))
-    alpha = _hermite_band_loop(a0, v, w, fa, fpa, 0.0, +1, n_seg)
-    beta = _hermite_band_loop(a0, v, w, fb, fpb, tb, -1, n_seg)
+    alpha = _hermite_band_loop(a0, v, w, fa, fpa, 0.0, +1, n_seg, qz)
+    beta = _hermite_band_loop(a0, v, w, fb, fpb, tb, -1, n_seg, qz)
     shift = np.array([beta_shift[0] * Tu, beta_shift[1] * Tv])
     beta_stored = [(P + shift, wt) for P, wt in beta]
-    r = float(quant(0.075 * s))
+    r = float(qz(0.075 * s))
     circles = []
     for tau_c, nu_c, orient in ((0.3, 0.4, -1), (0.75, 0.4, -1), (0.5, 0.9, +1)):
-        c = quant(a0 + tau_c * v + nu_c * w)
+        c = qz(a0 + tau_c * v + nu_c * w)
         circles.append((c, r, orient))
     b = _Builder()
-    loops = [alpha, beta_stored] + [[(quant(P), wt) for P, wt in _circle_arcs(c, r, ccw=(o > 0))]
+    loops = [alpha, beta_stored] + [[(qz(P), wt) for P, wt in _circle_arcs(c, r, ccw=(o > 0))]
                                      for c, r, o in circles]
+    jit = _jit(seed, store_jitter)
     for segs in loops:
         for P, wt in segs:
-            b.seg(_wrap_store(P, Tu, Tv, True, True), wt)
+            b.seg(_wrap_store(P, Tu, Tv, True, True, jit=jit), wt)
         b.end_loop()
     b.end_face(periodic=3, domain=(0.0, Tu, 0.0, Tv))
     uv = rng.uniform(0.0, 1.0, size=(n_queries, 2)) * [Tu, Tv]
     uv = np.minimum(uv, np.nextafter(np.array([Tu, Tv]), 0.0))
-    meta = dict(kind="C3pq", p=p, q=q, Tu=Tu, Tv=Tv, a0=a0, v=v, w=w, alpha=alpha, beta=beta,
+    meta = dict(kind="C3pq", p=p, q=q, Tu=Tu, Tv=Tv, a0=a0, v=v, w=w, alpha=alpha, beta=beta, exact=exact,
                 circles=[(tuple(c), r, o) for c, r, o in circles])
-    return _finish(b, np.zeros(n_queries), uv, False, "C3pq(%d,%d)" % (p, q), meta)
+    return _finish(b, np.zeros(n_queries), uv, False, "C3pq(%d,%d)%s" % (p, q, "" if exact else "-generic"), meta)
 
 
 # ----------------------------------------------------------------------------
@@ -492,9 +531,11 @@ def _n_segs(rng):
     return int(round(math.exp(rng.uniform(math.log(4.0), math.log(128.0)))))
 
 
-def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
+def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30, exact=True, store_jitter=0):
     rng = np.random.Generator(np.random.PCG64(seed))
-    T = TWO_PI_Q
+    jit = _jit(seed, store_jitter)
+    T, _ = _periods(exact)
+    qz = _qz(exact)
     b = _Builder()
     uvs = []
     boxes = []   # per-face grid box (u_lo, v_lo, u_hi, v_hi): the implicit-grid form of the batch
@@ -534,35 +575,35 @@ def gen_c5(seed=5, n_faces=20_000, grid=64, periodic_frac=0.30):
                 fa = lambda u, kf=kf, pa=pa: 0.25 + 0.05 * np.sin(kf * u + pa)
                 fb = lambda u, kf=kf, pb=pb: 0.75 + 0.05 * np.sin(kf * u + pb)
                 na, nb = _n_segs(rng), _n_segs(rng)
-                loops.append(_graph_loop(rng, fa, float(quant(rng.uniform(0, T))), T, +1, na,
-                                         rng.integers(1, 6, size=na), True))
-                loops.append(_graph_loop(rng, fb, float(quant(rng.uniform(0, T))), T, -1, nb,
-                                         rng.integers(1, 6, size=nb), True))
+                loops.append(_graph_loop(rng, fa, float(qz(rng.uniform(0, T))), T, +1, na,
+                                         rng.integers(1, 6, size=na), True, qz))
+                loops.append(_graph_loop(rng, fb, float(qz(rng.uniform(0, T))), T, -1, nb,
+                                         rng.integers(1, 6, size=nb), True, qz))
                 nh = L - 2
                 for j in range(nh):
                     hu = 0.0 if j == 0 else j * T / nh + rng.uniform(-0.05, 0.05)
-                    hc = quant([hu, 0.5 + rng.uniform(-0.1, 0.1)])
+                    hc = qz([hu, 0.5 + rng.uniform(-0.1, 0.1)])
                     n = _n_segs(rng)
-                    V = quant(_star_vertices(rng, hc, 0.06, 0.005, n, cw=True))
+                    V = qz(_star_vertices(rng, hc, 0.06, 0.005, n, cw=True))
                     segs = _star_segments(rng, V, rng.integers(1, 6, size=n), 0.05, True)
-                    loops.append([(quant(P), w) for P, w in segs])
+                    loops.append([(qz(P), w) for P, w in segs])
             else:
-                hc = quant([0.0, 0.5])
+                hc = qz([0.0, 0.5])
                 n = _n_segs(rng)
-                V = quant(_star_vertices(rng, hc, 0.3, 0.02, n, cw=False))
+                V = qz(_star_vertices(rng, hc, 0.3, 0.02, n, cw=False))
                 segs = _star_segments(rng, V, rng.integers(1, 6, size=n), 0.05, True)
-                loops.append([(quant(P), w) for P, w in segs])
+                loops.append([(qz(P), w) for P, w in segs])
             for segs in loops:
                 for P, w in segs:
-                    b.seg(_wrap_store(P, T, 1.0, True, False), w)
+                    b.seg(_wrap_store(P, T, 1.0, True, False, jit=jit), w)
                 b.end_loop()
             b.end_face(periodic=1, domain=(0.0, T, 0.0, 1.0))
             boxes.append((0.0, 0.0, T, 1.0))
             uvs.append(_grid((0.0, 0.0), (T, 1.0), grid))
         fids.append(np.full(grid * grid, f))
-    meta = dict(kind="C5", n_periodic=n_periodic, grid=grid,
+    meta = dict(kind="C5", n_periodic=n_periodic, grid=grid, exact=exact,
                 grid_box=np.ascontiguousarray(np.asarray(boxes, dtype=np.float64).reshape(-1, 4)))
-    return _finish(b, np.concatenate(fids), np.concatenate(uvs), True, "C5", meta)
+    return _finish(b, np.concatenate(fids), np.concatenate(uvs), True, "C5" if exact else "C5-generic", meta)
 
 
 # ----------------------------------------------------------------------------

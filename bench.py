@@ -40,25 +40,25 @@ WORKLOAD = ("C5 synthetic B-Rep batch / tessellation: 20000 faces, loops 1-8 (ge
             "segments/loop 4-128 (log-uniform), degree 1-5 rational Bezier, 30% periodic in u, "
             "64x64 uv grid per face (81,920,000 queries), fp64")
 
-# Roofline of the dominant kernel, k_phase1 (DESIGN.md 6 "Roofline"): after the
-# fp32 filter, the telescoped crossings and the path hierarchy it is bound by
-# SM instruction issue (ncu: FP64 / FMA pipes far from busy, issue slots the
-# limiter), so the roofline is the issue rate: 148 SMs x 4 schedulers x 1
-# warp-instruction per clock at the 1965 MHz max SM clock.
-ISSUE_PEAK = 148 * 4 * 1.965e9 / 1e9          # G warp-instructions / s
-# Work per unit (warp-record iteration) of THIS implementation and the DRAM
-# traffic per launch come from the committed ncu --set full capture of the
-# same bench command (scripts/ncu_k3_metrics.py writes the JSON); the unit
-# count (warp_records) is measured live by the device counters below.
-K3_METRICS = os.path.join(ROOT, "profiles", "round1", "k_phase1_metrics.json")
+# Roofline of the query kernel (DESIGN.md 6 "Roofline and algorithmic work"):
+# ALGORITHMIC work = SURVEY 8(d)'s per-unit FP64-pipe instruction costs of the
+# paper's literal Alg. 1 (the work the method as printed performs for the
+# tests this run made) x the live unit counts of the same workload, divided by
+# the kernel's CUDA-event time and by the FP64 pipe peak MEASURED in this run
+# (wn_measure_fp_peak: DFMA chains, lane instructions / s).  Unit costs:
+U_PRUNE = 71   # pruned (query, record) test: two distances, ellipse test, atan2 chord
+U_TEST = 26    # test without a chord: hard root test, hierarchy node that descends, recursion node
+U_EVAL = 22    # midpoint evaluation, 3 (n + 1) + 10 at the mean degree n = 3
+U_LEAF = 45    # recursion leaf: chord + atan2
 
 
-def _k3_metrics():
-    try:
-        with open(K3_METRICS) as fh:
-            return json.load(fh)
-    except (OSError, ValueError):
-        return None
+def algorithmic_work(cnt):
+    """(phase-1 work, phase-2 work) in FP64-pipe lane instructions from the
+    device counters (wn_get_counters) of one query launch."""
+    span_pruned = cnt["span_tests"] - cnt["span_descended"]
+    w1 = U_PRUNE * (cnt["seg_pruned"] + span_pruned) + U_TEST * (cnt["hard_pairs"] + cnt["span_descended"])
+    w2 = U_TEST * cnt["nodes"] + U_EVAL * cnt["evals"] + U_LEAF * cnt["leaves"]
+    return float(w1), float(w2)
 
 
 def _env_int(k, d):
@@ -139,7 +139,7 @@ def _oracle_rate(wl, rng, cores, nq):
     return per_q, max(t0 - per_q * m0, 0.0)
 
 
-def _cpu_baseline(wl, target_s, rank_seed=0):
+def _cpu_baseline(wl, target_s, rank_seed=0, one_thread_frac=0.0):
     """Oracle (as it stands) on a bounded random sample of the same workload."""
     import oracle
     cores = os.cpu_count() or 1
@@ -151,12 +151,97 @@ def _cpu_baseline(wl, target_s, rank_seed=0):
     t = time.perf_counter()
     oracle.query(wl, face_id=wl["face_id"][idx], uv=wl["uv"][idx], nthreads=cores)
     dt = time.perf_counter() - t
-    return {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": "%d random queries of the C5 batch (all faces eligible), one oracle call incl. its "
-                      "own lifting/pairing of all faces, %.1f s wall" % (m, dt)}, dt
+    out = {"value": m / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
+           "sample": "%d random queries of the C5 batch (all faces eligible), one oracle call incl. its "
+                     "own lifting/pairing of all faces, %.1f s wall" % (m, dt)}
+    if one_thread_frac > 0:
+        # fixed subsample (every k-th query) on ONE thread: the paper's single-threaded C++ 
+        k = max(1, int(round(1.0 / one_thread_frac)))
+        idx1 = np.arange(0, nq, k)
+        t = time.perf_counter()
+        oracle.query(wl, face_id=wl["face_id"][idx1], uv=wl["uv"][idx1], nthreads=1)
+        d1 = time.perf_counter() - t
+        out["single_thread"] = {"value": len(idx1) / d1, "unit": UNIT, "threads": 1,
+                                "sample": "fixed %.2f%% subsample (every %d-th query of C5, %d queries), %.1f s wall"
+                                          % (100.0 / k, k, len(idx1), d1)}
+    return out, dt
+
+
+
+def config_rates(wn, wl, precision, dev, st, fp64_peak, fp32_peak, nrep=10):
+    """Build + query timing of one (smaller) BASELINE config on the device, its
+    counters and its algorithmic roofline fraction (FP32 peak for fp32)."""
+    import torch
+    from wn_workloads import configs as G
+    nq = len(wl["face_id"])
+    T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
+    geo = [T(wl["ctrl_uv"], torch.float64), T(wl["ctrl_w"], torch.float64) if wl["ctrl_w"] is not None else None,
+           T(wl["seg_degree"], torch.int32), T(wl["loop_seg_off"], torch.int32), T(wl["face_loop_off"], torch.int32),
+           T(wl["face_periodic"], torch.uint8), T(wl["face_domain"], torch.float64)]
+    fid, uv = T(wl["face_id"], torch.int32), T(wl["uv"], torch.float64)
+    wnd = torch.empty(nq, dtype=torch.float64, device=dev)
+    flg = torch.empty(nq, dtype=torch.uint8, device=dev)
+
+    def q(faces):
+        faces.query_raw(nq, fid.data_ptr(), uv.data_ptr(), wnd.data_ptr(), flg.data_ptr(), st.cuda_stream)
+
+    for _ in range(3):
+        f = wn.Faces.build(*geo, precision=precision, device=dev)
+        q(f)
+        f.close()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(nrep):
+        f = wn.Faces.build(*geo, precision=precision, device=dev)
+        q(f)
+        f.close()
+    e1.record(st)
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / nrep
+    faces = wn.Faces.build(*geo, precision=precision, device=dev)
+    q(faces)
+    torch.cuda.synchronize()
+    faces.set_timing(True)
+    e0.record(st)
+    for _ in range(nrep):
+        q(faces)
+    e1.record(st)
+    torch.cuda.synchronize()
+    q_ms = e0.elapsed_time(e1) / nrep
+    k3_ms, p1_ms, k3_n = faces.timing()
+    faces.set_timing(False)
+    faces.set_counters(True)
+    q(faces)
+    cnt = faces.counters()
+    faces.set_counters(False)
+    faces.close()
+    k3_avg, p1_avg = k3_ms / max(k3_n, 1), p1_ms / max(k3_n, 1)
+    w1, w2 = algorithmic_work(cnt)
+    peak = fp32_peak if precision else fp64_peak
+    pairs = G.n_input_pairs(wl)
+    return {"queries": nq, "precision": "fp32" if precision else "fp64", "step_ms": step_ms, "query_ms": q_ms,
+            "queries_per_s": nq / (q_ms / 1e3), "pairs_per_s": pairs / (q_ms / 1e3),
+            "k3_ms": k3_avg, "phase1_ms": p1_avg,
+            "roofline_frac": (w1 + w2) / (k3_avg / 1e3) / peak if k3_avg > 0 else None,
+            "roofline_peak": "measured %s pipe" % ("FP32" if precision else "FP64"),
+            "counters": {k: cnt[k] for k in ("pairs_tested", "span_tests", "hard_pairs", "nodes", "warp_records")}}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or platform.machine()
 
 
 def run_reference(args, rank, world):
+
     if rank != 0:
         return 0
     from wn_workloads import configs as G
@@ -181,7 +266,7 @@ def run_reference(args, rank, world):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": WORKLOAD, "sample_per_step": per_step},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
                              "sample": "%d random C5 queries per step, %d steps" % (per_step, args.steps)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -197,6 +282,8 @@ def main():
     ap.add_argument("--angle-mode", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 extra keys")
+    ap.add_argument("--cpu-1t-frac", type=float, default=0.01, help="fixed subsample of the 1-thread oracle rate")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     args = ap.parse_args()
@@ -418,30 +505,47 @@ def main():
                        "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in h_geo) + h_gb.numel() * 8),
                        "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
-    # ---- roofline of the dominant kernel (k_phase1) ----
-    k3_avg = k3_ms / max(k3_n, 1)
-    p1_avg = p1_ms / max(k3_n, 1)      # measured live in the timed region (CUDA events on the stream)
-    met = _k3_metrics()
-    if met:
-        ipr = met["inst_executed"] / met["warp_records"]
-        work = ipr * cnt["warp_records"] / 1e9          # G warp-instructions per launch
-        achieved = work / (p1_avg / 1e3)
-        traffic = met["dram_bytes"]
-    else:
-        ipr, achieved, traffic = None, None, None
-    roofline = {"bound": "alu", "achieved": achieved, "peak": ISSUE_PEAK, "unit": "Gwarp-inst/s",
-                "frac": (achieved / ISSUE_PEAK) if achieved else None, "traffic": traffic,
+    # ---- roofline of the query kernel (algorithmic work / live time / measured peak) ----
+    k3_avg = k3_ms / max(k3_n, 1)      # K3 (phase 1 + hard pairs + overflow + finish), CUDA events on the stream
+    p1_avg = p1_ms / max(k3_n, 1)      # k_phase1 alone, same events, timed region
+    fp64_peak, fp64_mhz = wn.measure_fp_peak(False, 0.05)
+    fp32_peak, fp32_mhz = wn.measure_fp_peak(True, 0.05)
+    w1, w2 = algorithmic_work(cnt)
+    ach1 = w1 / (p1_avg / 1e3) / 1e9
+    ach3 = (w1 + w2) / (k3_avg / 1e3) / 1e9
+    lane_tests = cnt["pairs_tested"] + cnt["span_tests"]
+    roofline = {"bound": "alu", "achieved": ach1, "peak": fp64_peak / 1e9, "unit": "G FP64-pipe lane-inst/s",
+                "frac": ach1 / (fp64_peak / 1e9), "traffic": None,
                 "kernel": "wn::k_phase1<double>", "kernel_ms": p1_avg, "kernel_share_of_step": p1_avg / ms_step,
-                "k3_ms": k3_avg,
-                "peak_source": "derived: 148 SMs x 4 schedulers x 1 warp-inst/clk x 1.965 GHz (max SM clock)",
-                "units": {"warp_records": cnt["warp_records"], "instr_per_warp_record": ipr,
-                          "src": os.path.relpath(K3_METRICS, ROOT) if met else None},
-                "pipes_ncu": ({k: met[k] for k in ("fp64_pct", "fma_pct", "alu_pct", "xu_pct", "issue_active_pct")
-                               if k in met} if met else None)}
+                "peak_source": "measured in this run: wn_measure_fp_peak (DFMA chains, lane inst/s) at %.0f MHz"
+                               % fp64_mhz,
+                "work": "SURVEY 8(d) unit costs x live counters: %d x pruned tests (seg %d + span %d) + %d x "
+                        "(hard root tests %d + descending span tests %d)" % (
+                            U_PRUNE, cnt["seg_pruned"], cnt["span_tests"] - cnt["span_descended"], U_TEST,
+                            cnt["hard_pairs"], cnt["span_descended"]),
+                "algorithmic_inst_per_launch": w1,
+                "k3": {"ms": k3_avg, "achieved": ach3, "frac": ach3 / (fp64_peak / 1e9),
+                       "algorithmic_inst_per_launch": w1 + w2,
+                       "phase2": "%d x nodes %d + %d x evals %d + %d x leaves %d" % (
+                           U_TEST, cnt["nodes"], U_EVAL, cnt["evals"], U_LEAF, cnt["leaves"])},
+                "units": {"warp_records": cnt["warp_records"], "lane_tests": lane_tests,
+                          "lane_utilisation": lane_tests / max(32 * cnt["warp_records"], 1),
+                          "hbm_bytes_algorithmic": 29 * nq,
+                          "hbm_gbs_algorithmic": 29 * nq / (p1_avg / 1e3) / 1e9},
+                "peaks_measured": {"fp64_lane_fma_per_s": fp64_peak, "fp64_sm_mhz": fp64_mhz,
+                                   "fp32_lane_fma_per_s": fp32_peak, "fp32_sm_mhz": fp32_mhz}}
+
+    # ---- the other BASELINE configs (parity-test cases, reported as extra keys) ----
+    others = None
+    if rank == 0 and not args.no_configs:
+        others = {}
+        for name, gen, prec in (("C1", G.gen_c1, 0), ("C2", G.gen_c2, 0), ("C3", G.gen_c3, 0), ("C4", G.gen_c4, 0),
+                                ("C4-fp32", lambda: G.to_fp32_inputs(G.gen_c4()), 1)):
+            others[name] = config_rates(wn, gen(), prec, dev, st, fp64_peak, fp32_peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, _ = _cpu_baseline(wl, args.cpu_seconds)
+        cpu, _ = _cpu_baseline(wl, args.cpu_seconds, one_thread_frac=args.cpu_1t_frac)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -455,7 +559,7 @@ def main():
                 "pairs_per_s": pairs_s,
                 "query_only": {"ms": q_ms, "queries_per_s": nq / (q_ms / 1e3), "pairs_per_s": pairs / (q_ms / 1e3)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-                "grid": grid,
+                "grid": grid, "configs": others,
                 "clocks": clocks, "counters": cnt, "faces_info": info, "flags": flags}
         print(json.dumps(line), flush=True)
     if dist:

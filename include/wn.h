@@ -201,7 +201,9 @@ wn_status_t wn_faces_info(wn_faces_t faces, wn_faces_info_t *out /* [host] */);
  *                  split-point evaluations, leaves, max depth, warp-level skips
  *                  (culled groups + pruned hierarchy subtrees), on-boundary,
  *                  (query, hierarchy node) tests, phase-1 warp-record
- *                  iterations, 0, 0}. */
+ *                  iterations, hierarchy-node tests that descend (the others
+ *                  substitute the run's chord), segment tests that substitute
+ *                  the chord}. */
 wn_status_t wn_set_counters(wn_faces_t faces, int enable);
 wn_status_t wn_get_counters(wn_faces_t faces, void *stream, int64_t *out /* [host][12] */);
 
@@ -224,6 +226,15 @@ wn_status_t wn_get_timing(wn_faces_t faces, double *k3_ms /* [host] */, double *
  * stream. */
 wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, const double *ctrl_w,
                             const int32_t *seg_degree, double *out, void *stream);
+
+/* Diagnostics: the device's measured FMA pipe peak (the roofline denominator of
+ * the query kernel): dependent-FMA chains, 8 independent per
+ * thread, 4 CTAs of 256 threads per SM, launches of ~`seconds` each, best of
+ * three.  fp32 = 0: DFMA, 1: FFMA.  *lane_fma_per_s [host] = lane FMA
+ * instructions per second (FLOP/s = 2x); *sm_mhz [host, or NULL] = the SM
+ * clock during the best launch (clock64 cycles / globaltimer ns of CTA 0).
+ * Synchronous; uses the current device. */
+wn_status_t wn_measure_fp_peak(int fp32, double seconds, double *lane_fma_per_s, double *sm_mhz);
 
 /* libwn keeps freed device buffers (records, query scratch) in a per-device
  * cache for reuse; wn_trim_memory returns them to the driver. */

@@ -30,9 +30,10 @@ FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
            "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host", "wn_query_grid",
-           "wn_nurbs_to_bezier", "wn_build_faces_nurbs"]
+           "wn_nurbs_to_bezier", "wn_build_faces_nurbs", "wn_measure_fp_peak"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
-                 "warp_skips", "on_boundary", "span_tests", "warp_records", "_r10", "_r11"]
+                 "warp_skips", "on_boundary", "span_tests", "warp_records", "span_descended",
+                 "seg_pruned"]
 
 
 class WNError(RuntimeError):
@@ -99,6 +100,8 @@ def load():
         L.wn_free_faces.argtypes = [vp]
         L.wn_last_error.restype = C.c_char_p
         L.wn_last_error.argtypes = []
+        L.wn_measure_fp_peak.restype = C.c_int
+        L.wn_measure_fp_peak.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.wn_last_query_launches.restype = C.c_int32
         L.wn_last_query_launches.argtypes = []
         _lib = L
@@ -384,6 +387,16 @@ def segment_prep(ctrl_uv, ctrl_w, seg_degree, device=None, stream=None):
     if rc != WN_OK:
         raise WNError(rc, last_error())
     return out
+
+
+def measure_fp_peak(fp32=False, seconds=0.05):
+    """(lane FMA instructions / s, SM MHz during the run) of the device's FP64
+    (fp32=False) or FP32 pipe: wn_measure_fp_peak."""
+    r, m = C.c_double(), C.c_double()
+    rc = load().wn_measure_fp_peak(int(bool(fp32)), float(seconds), C.byref(r), C.byref(m))
+    if rc != WN_OK:
+        raise WNError(rc, last_error())
+    return r.value, m.value
 
 
 def last_query_launches():

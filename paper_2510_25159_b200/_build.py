@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libwn.so")
-SOURCES = ["wn_build.cu", "wn_query.cu", "wn_alloc.cu", "wn_nurbs.cu"]
+SOURCES = ["wn_build.cu", "wn_query.cu", "wn_alloc.cu", "wn_nurbs.cu", "wn_peak.cu"]
 HEADERS = ["wn_common.cuh", os.path.join("..", "..", "include", "wn.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

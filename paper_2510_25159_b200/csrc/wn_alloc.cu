@@ -7,6 +7,7 @@
 // an event recorded on the stream that last used it; a later allocation on a
 // different stream waits on that event (cudaStreamWaitEvent) before reuse, so
 // reuse is stream-ordered exactly like cudaMallocAsync.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -39,10 +40,19 @@ size_t size_class(size_t b) {
 }
 }  // namespace
 
+// WN_ALLOC_EXACT=1 (sanitizer runs): every block is a fresh cudaMalloc of the
+// exact size, freed with cudaFree -- no size-class slack and no reuse, so
+// compute-sanitizer's memcheck sees every out-of-bounds access.
+static bool alloc_exact() {
+  static const int v = [] { const char *s = std::getenv("WN_ALLOC_EXACT"); return (s && *s && *s != '0') ? 1 : 0; }();
+  return v != 0;
+}
+
 cudaError_t cache_alloc(void **out, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  if (alloc_exact()) return cudaMalloc(out, bytes ? bytes : 1);
   const size_t sz = size_class(bytes ? bytes : 1);
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -78,6 +88,11 @@ cudaError_t cache_alloc(void **out, size_t bytes, cudaStream_t st) {
 
 void cache_free(void *p, cudaStream_t st) {
   if (!p) return;
+  if (alloc_exact()) {
+    cudaStreamSynchronize(st);
+    cudaFree(p);
+    return;
+  }
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_live.find(p);
   if (it == g_live.end()) return;

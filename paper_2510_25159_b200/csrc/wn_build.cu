@@ -224,14 +224,120 @@ __device__ __forceinline__ double poly_len(const double (&a)[N + 1], const doubl
   return L;
 }
 
+// K1 output sinks.  PrepSink: the diagnostics record of wn_segment_prep
+// (unmargined doubles).  ColdSink<R>: the build's base cold record of the
+// segment (margins applied, piece bounds rounded up to fp32: still upper
+// bounds) plus its root span S0 (unmargined) for the hierarchy prefix sums and
+// the hot SEG record.  Both are fed by the same bound code (prep_n).
+struct PrepSink {
+  SegPrep *out;
+  __device__ void zero(int s) const {
+    double2 *o2 = reinterpret_cast<double2 *>(out + s);
+    for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+  }
+  __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) const {
+    double2 *o2 = reinterpret_cast<double2 *>(out + s);
+    o2[1 + q / 2] = make_double2(b0, b1);
+    o2[5 + q / 2] = make_double2(l0, l1);
+  }
+  template <int N>
+  __device__ void root(int s, double B, double S0, const double *, const double *, const double *, int) const {
+    reinterpret_cast<double2 *>(out + s)[0] = make_double2(B, S0);
+  }
+};
+
+__device__ __forceinline__ float f_dn(double x) { return __double2float_rd(x); }
+__device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
+
+// C(n, j) for 0 <= j <= n <= 5, exact: 4-bit entries of a packed table indexed
+// by 6 n + j (no divisions, no local or constant-memory table)
+__device__ __forceinline__ double binom5(int n, int j) {
+  constexpr unsigned long long T0 = 0x0000000000000000ull   // n = 0, 1, 2 (idx 0..15)
+      | 1ull << 0                                            // C(0,0)
+      | 1ull << 24 | 1ull << 28                              // C(1,0..1)
+      | 1ull << 48 | 2ull << 52 | 1ull << 56;                // C(2,0..2)
+  constexpr unsigned long long T1 = 0x0000000000000000ull   // n = 3, 4, 5 (idx 18..35, minus 18)
+      | 1ull << 0 | 3ull << 4 | 3ull << 8 | 1ull << 12        // C(3,0..3)
+      | 1ull << 24 | 4ull << 28 | 6ull << 32 | 4ull << 36 | 1ull << 40   // C(4,0..4)
+      | 1ull << 48 | 5ull << 52 | 10ull << 56 | 10ull << 60;           // C(5,0..3)
+  const int idx = 6 * n + j;
+  unsigned v;
+  if (idx < 18) v = (unsigned)(T0 >> (4 * idx)) & 15u;
+  else if (idx < 34) v = (unsigned)(T1 >> (4 * (idx - 18))) & 15u;
+  else v = idx == 34 ? 5u : 1u;                              // C(5,4), C(5,5)
+  return (double)v;
+}
+
+template <typename R>
+struct ColdSink {
+  BaseCold<R> *out;
+  double *s0;
+  double rel;   // relative margin (R5): 2^-40 fp64, 2^-17 fp32
+  __device__ void zero(int s) const {
+    uint4 *o = reinterpret_cast<uint4 *>(out + s);
+    for (int k = 0; k < (int)(sizeof(BaseCold<R>) / 16); ++k) o[k] = make_uint4(0, 0, 0, 0);
+    s0[s] = 0.0;
+  }
+  __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) const {
+    BaseCold<R> *C = out + s;
+    *reinterpret_cast<float2 *>(&C->Bq[q]) = make_float2(f_up(fmin(B, b0) * (1.0 + rel)), f_up(fmin(B, b1) * (1.0 + rel)));
+    *reinterpret_cast<float2 *>(&C->Lq[q]) = make_float2(f_up(l0 * (1.0 + rel)), f_up(l1 * (1.0 + rel)));
+  }
+  // end points (exact, stored coordinates), bound, degree, homogeneous Horner
+  // coefficients c_j = (C(n,j) w_j) (x_j, y_j, 1), zero above the degree
+  template <int N>
+  __device__ void root(int s, double B, double S0, const double *px, const double *py, const double *W, int) const {
+    BaseCold<R> *C = out + s;
+    s0[s] = S0;
+    *reinterpret_cast<double2 *>(&C->x0) = make_double2(px[0], py[0]);
+    *reinterpret_cast<double2 *>(&C->xn) = make_double2(px[N], py[N]);
+    const double Bm = B * (1.0 + rel);
+    if constexpr (sizeof(R) == 8) {
+      *reinterpret_cast<double2 *>(&C->B) = make_double2(Bm, __longlong_as_double((long long)N));
+#pragma unroll
+      for (int j = 0; j < 6; j += 2) {
+        double cx2[2], cy2[2], cw2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int jj = j + h;
+          cx2[h] = cy2[h] = cw2[h] = 0.0;
+          if (jj <= N) {
+            const double cw = binom5(N, jj) * W[jj];
+            cx2[h] = cw * px[jj];
+            cy2[h] = cw * py[jj];
+            cw2[h] = cw;
+          }
+        }
+        *reinterpret_cast<double2 *>(&C->cx[j]) = make_double2(cx2[0], cx2[1]);
+        *reinterpret_cast<double2 *>(&C->cy[j]) = make_double2(cy2[0], cy2[1]);
+        *reinterpret_cast<double2 *>(&C->cw[j]) = make_double2(cw2[0], cw2[1]);
+      }
+    } else {
+      C->B = f_up(Bm);
+      C->n = N;
+#pragma unroll
+      for (int jj = 0; jj < 6; ++jj) {
+        float cx = 0.f, cy = 0.f, cwf = 0.f;
+        if (jj <= N) {
+          const double cw = binom5(N, jj) * W[jj];
+          cx = (float)(cw * px[jj]);
+          cy = (float)(cw * py[jj]);
+          cwf = (float)cw;
+        }
+        C->cx[jj] = cx;
+        C->cy[jj] = cy;
+        C->cw[jj] = cwf;
+      }
+    }
+  }
+};
+
 // One thread per segment (taken in degree-sorted order so that a warp runs one
 // degree variant): loads its control points once and computes B, S0 and the 8
-// piece bounds and piece polygon lengths, written as one 144-B record prep[s]
-// (nine 16-B stores), which
-// k_emit then reads coalesced in segment order.
-template <int N>
-__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o,
-                                       SegPrep *__restrict__ out, uint8_t *__restrict__ err_out) {
+// piece bounds and piece polygon lengths, written through the sink.
+template <int N, class Sink>
+__device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o, int s,
+                                       const Sink &sink, uint8_t *__restrict__ err_out) {
   double X[N + 1], Y[N + 1], W[N + 1], px[N + 1], py[N + 1];
   bool err = false;
   double lpoly = 0.0;
@@ -243,11 +349,9 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     px[j] = x; py[j] = y;
     if (j) lpoly += hypot(x - px[j - 1], y - py[j - 1]);
   }
-  *err_out = err ? 1 : 0;
-  double2 *o2 = reinterpret_cast<double2 *>(out);
+  err_out[s] = err ? 1 : 0;
   if (err) {
-#pragma unroll
-    for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+    sink.zero(s);
     return;
   }
   const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
@@ -262,37 +366,13 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     const double b1 = 8.0 * hodo_bound<N>(a, bb, c);
     const double l1 = poly_len<N>(a, bb, c);
     l8 += l0 + l1;
-    o2[1 + q / 2] = make_double2(b0, b1);
-    o2[5 + q / 2] = make_double2(l0, l1);
+    sink.pieces(s, q, B, b0, b1, l0, l1);
   }
-  o2[0] = make_double2(B, fmin(B, fmin(lpoly, l8)));
-}
-
-__global__ void __launch_bounds__(128, PREP_MINB) k_prep(int32_t n_segs, const int32_t *__restrict__ deg,
-                                              const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                                              const double *__restrict__ w, SegPrep *__restrict__ prep,
-                                              uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n_segs) return;
-  const int s = order ? order[p] : p;   // degree-sorted: warp-uniform N
-  const int o = coff[s];
-  const int n = deg[s];
-  switch (n) {
-    case 1: prep_n<1>(ctrl, w, o, prep + s, serr + s); break;
-    case 2: prep_n<2>(ctrl, w, o, prep + s, serr + s); break;
-    case 3: prep_n<3>(ctrl, w, o, prep + s, serr + s); break;
-    case 4: prep_n<4>(ctrl, w, o, prep + s, serr + s); break;
-    case 5: prep_n<5>(ctrl, w, o, prep + s, serr + s); break;
-    default: {   // rejected on the host (k_deg flag); never read past the arrays
-      serr[s] = 1;
-      double2 *o2 = reinterpret_cast<double2 *>(prep + s);
-      for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
-    }
-  }
+  sink.template root<N>(s, B, fmin(B, fmin(lpoly, l8)), px, py, W, 0);
 }
 
 #ifndef PREP_SPLIT
-#define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels; 0: one k_prep for all degrees
+#define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels
 #endif
 // Per-degree K1: the degree-sorted segments split into the ranges of the sort
 // key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with
@@ -309,33 +389,32 @@ __global__ void k_deg_bounds(int32_t n, const int32_t *__restrict__ sdeg, int32_
 #ifndef PREP_DEG_MINB
 #define PREP_DEG_MINB 1
 #endif
-template <int N>
+template <int N, class Sink>
 __global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *__restrict__ bnd, const int32_t *__restrict__ deg,
                                                   const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                                                  const double *__restrict__ w, SegPrep *__restrict__ prep,
+                                                  const double *__restrict__ w, Sink sink,
                                                   uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
   const int lo = bnd[N], hi = bnd[N + 1];
   for (int p = lo + blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += gridDim.x * blockDim.x) {
     const int s = order[p];
     if (deg[s] == N) {
-      prep_n<N>(ctrl, w, coff[s], prep + s, serr + s);
+      prep_n<N>(ctrl, w, coff[s], s, sink, serr);
     } else {   // a degree outside 1..5 with these low bits (rejected on the host)
       serr[s] = 1;
-      double2 *o2 = reinterpret_cast<double2 *>(prep + s);
-      for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+      sink.zero(s);
     }
   }
 }
 
 // keys 0, 6, 7: degrees outside 1..5 only
-__global__ void k_prep_bad(const int32_t *__restrict__ bnd, SegPrep *__restrict__ prep, uint8_t *__restrict__ serr,
+template <class Sink>
+__global__ void k_prep_bad(const int32_t *__restrict__ bnd, Sink sink, uint8_t *__restrict__ serr,
                            const int32_t *__restrict__ order) {
   const int n0 = bnd[1] - bnd[0], n1 = bnd[8] - bnd[6];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1; i += gridDim.x * blockDim.x) {
     const int s = order[i < n0 ? bnd[0] + i : bnd[6] + (i - n0)];
     serr[s] = 1;
-    double2 *o2 = reinterpret_cast<double2 *>(prep + s);
-    for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
+    sink.zero(s);
   }
 }
 
@@ -352,7 +431,6 @@ __global__ void k_loop_face(int32_t n_faces, int32_t n_loops, const int32_t *__r
   for (int l = l0; l < l1; ++l) loop_face[l] = f;
 }
 
-__device__ __forceinline__ double lat(double x, int k, double T) { return __dadd_rn(x, __dmul_rn((double)k, T)); }
 
 // ---------------------------------------------------------------------------
 // K2a: lifting to the universal covering space (Sec. 4.3).  Loops
@@ -367,9 +445,9 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
                                               const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,
                                               const int32_t *__restrict__ deg, const int32_t *__restrict__ coff,
                                               const double *__restrict__ ctrl, const double *__restrict__ wts,
-                                              double *__restrict__ lctrl, double *__restrict__ lw,
-                                              uint8_t *__restrict__ brk,
-                                              int2 *__restrict__ chain, double2 *__restrict__ lend,
+                                              int2 *__restrict__ shift, uint8_t *__restrict__ brk,
+                                              int2 *__restrict__ chain, double2 *__restrict__ lsta,
+                                              double2 *__restrict__ lend,
                                               LoopInfo *__restrict__ info) {
   // one warp per loop; lanes take its segments 32 at a time.  The lattice
   // shifts are a sequential recurrence (each segment continues from the
@@ -470,18 +548,9 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
     cxr = __shfl_sync(0xffffffffu, xe, cnt - 1);
     cyr = __shfl_sync(0xffffffffu, ye, cnt - 1);
     if (in) {
-      // the lifted control points and weights: library-owned copies that the
-      // record emission reads (the caller's arrays are not read after the
-      // build returns, include/wn.h)
-      const int n = deg[s], o = coff[s];
-      if (n >= 1 && n <= 5)
-        for (int j = 0; j <= n; ++j) {
-          const double x = ctrl[2 * (o + j)], y = ctrl[2 * (o + j) + 1];
-          lctrl[2 * (o + j)] = pu ? lat(x, ku, Tu) : x;
-          lctrl[2 * (o + j) + 1] = pv ? lat(y, kv, Tv) : y;
-          if (wts) lw[o + j] = wts[o + j];
-        }
+      shift[s] = make_int2(ku, kv);
       brk[s] = bk;
+      lsta[s] = make_double2(lx0, ly0);     // lifted start / end: the emission's chain points
       // lifted box and end point: lat() is monotone, so it commutes with min/max
       bx0 = pu ? lat(bx0, ku, Tu) : bx0; bx1 = pu ? lat(bx1, ku, Tu) : bx1;
       by0 = pv ? lat(by0, kv, Tv) : by0; by1 = pv ? lat(by1, kv, Tv) : by1;
@@ -536,7 +605,7 @@ __global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, 
 // the path-hierarchy spans are differences of them.  Summation
 // order differs from a serial sum by a few ulps, far inside the R5 margin.
 __global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, const int32_t *__restrict__ loop_off,
-                                               const SegPrep *__restrict__ prep, double *__restrict__ s0pre) {
+                                               const double *__restrict__ seg_s0, double *__restrict__ s0pre) {
   const int l = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (l >= n_loops) return;
@@ -544,7 +613,7 @@ __global__ void __launch_bounds__(256) k_s0pre(int32_t n_loops, int32_t n_segs, 
   double carry = 0.0;
   for (int base = s0; base < s1; base += 32) {
     const int s = base + lane;
-    double v = s < s1 ? prep[s].S0 : 0.0;
+    double v = s < s1 ? seg_s0[s] : 0.0;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double u = __shfl_up_sync(0xffffffffu, v, o);
@@ -583,9 +652,6 @@ __host__ __device__ inline int tree_recs(int n, int k) { return 2 * n - 1 - tree
 
 template <typename R>
 struct Emit;
-
-__device__ __forceinline__ float f_dn(double x) { return __double2float_rd(x); }
-__device__ __forceinline__ float f_up(double x) { return __double2float_ru(x); }
 
 // write a point-like record: (x, y) exact, s = span of the conservative filter
 template <typename R>
@@ -637,48 +703,20 @@ __device__ void put_group<float>(Hot<float> *H, int r, double xmin, double ymin,
   H[r] = h;
 }
 
-// C(n, j) for 0 <= j <= n <= 5, exact: 4-bit entries of a packed table indexed
-// by 6 n + j (no divisions, no local or constant-memory table)
-__device__ __forceinline__ double binom5(int n, int j) {
-  constexpr unsigned long long T0 = 0x0000000000000000ull   // n = 0, 1, 2 (idx 0..15)
-      | 1ull << 0                                            // C(0,0)
-      | 1ull << 24 | 1ull << 28                              // C(1,0..1)
-      | 1ull << 48 | 2ull << 52 | 1ull << 56;                // C(2,0..2)
-  constexpr unsigned long long T1 = 0x0000000000000000ull   // n = 3, 4, 5 (idx 18..35, minus 18)
-      | 1ull << 0 | 3ull << 4 | 3ull << 8 | 1ull << 12        // C(3,0..3)
-      | 1ull << 24 | 4ull << 28 | 6ull << 32 | 4ull << 36 | 1ull << 40   // C(4,0..4)
-      | 1ull << 48 | 5ull << 52 | 10ull << 56 | 10ull << 60;           // C(5,0..3)
-  const int idx = 6 * n + j;
-  unsigned v;
-  if (idx < 18) v = (unsigned)(T0 >> (4 * idx)) & 15u;
-  else if (idx < 34) v = (unsigned)(T1 >> (4 * (idx - 18))) & 15u;
-  else v = idx == 34 ? 5u : 1u;                              // C(5,4), C(5,5)
-  return (double)v;
-}
-
-template <typename R>
-__device__ __forceinline__ void st2(R *p, R a, R b);
-template <>
-__device__ __forceinline__ void st2<double>(double *p, double a, double b) {
-  *reinterpret_cast<double2 *>(p) = make_double2(a, b);
-}
-template <>
-__device__ __forceinline__ void st2<float>(float *p, float a, float b) {
-  *reinterpret_cast<float2 *>(p) = make_float2(a, b);
-}
-
 // one warp per planned group; lanes take the group's segments in parallel.
 // The path-hierarchy SPAN records of a chain need the end point and the S0
 // prefix of segments handled by other lanes (or chunks): for groups of up to
 // EMIT_STAGE segments the warp first stages them in shared memory, so the
 // per-level SPAN emission reads shared memory instead of a chain of global loads.
+// Per emitted segment the warp writes its hot records and one 24-B CopyRec
+// (consecutive lanes: coalesced); the translation-invariant cold data of the
+// segment was written once by K1 (BaseCold), whatever the number of copies.
 #ifndef EMIT_WARPS
 #define EMIT_WARPS 4
 #endif
 #ifndef EMIT_STAGE
 #define EMIT_STAGE 128
 #endif
-constexpr int PREP_D2 = (int)(sizeof(SegPrep) / 16);   // 16-B words per K1 record
 #ifndef EMIT_MINB
 #define EMIT_MINB 8
 #endif
@@ -686,14 +724,13 @@ template <typename R>
 __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_groups, const PlanGroup *__restrict__ groups,
                        const int32_t *__restrict__ loop_off,
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
-                       const double *__restrict__ face_dom, const int32_t *__restrict__ deg,
-                       const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                       const double *__restrict__ wts, const SegPrep *__restrict__ prep,
+                       const double *__restrict__ face_dom, const double2 *__restrict__ lsta,
+                       const double *__restrict__ s0, const int2 *__restrict__ shift,
                        const uint8_t *__restrict__ brk,
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const double2 *__restrict__ lend,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
-                       Cold<R> *__restrict__ cold, int dbg_flags) {
+                       CopyRec *__restrict__ copy) {
   const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (g >= n_groups) return;
@@ -704,8 +741,8 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
   const double Tu = face_dom[4 * f + 1], Tv = face_dom[4 * f + 3];
   const LoopInfo I = info[l];
   const uint32_t fa = (G.flags & PF_ANGLE) ? F_ANGLE : 0u;
-  // `ctrl` / `wts` are the LIFTED control points written by k_lift (lat(x,
-  // k_s, T) per segment); translated coordinate of this group's copy:
+  // lsta / lend hold the LIFTED end points written by k_lift (lat(x, k_s, T)
+  // per segment); translated coordinate of this group's copy:
   auto TX = [&](double x) { return pu ? lat(x, G.ku, Tu) : x; };
   auto TY = [&](double y) { return pv ? lat(y, G.kv, Tv) : y; };
   if (G.kind == G_LINE) {
@@ -730,20 +767,19 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     const double ymin = TY(I.bb[1]) - G.M, ymax = TY(I.bb[3]) + G.M;
     put_group<R>(hot, G.rec_off, xmin, ymin, xmax, ymax, K_GROUP | ((uint32_t)(G.nrec - 1) << 8));
   }
-  const int s0 = loop_off[l], s1 = loop_off[l + 1];
+  const int s0_ = loop_off[l], s1 = loop_off[l + 1];
   const int r_first = G.rec_off + cull + 1;              // first record after GROUP? and MOVE
   const bool tree = (G.flags & PF_TREE) != 0;
   const bool omit_root = tree && (G.flags & PF_OMIT_ROOT) != 0;
-  __shared__ double2 s_prep[EMIT_WARPS][32 * PREP_D2];  // the chunk's K1 records
   __shared__ double2 s_end[EMIT_WARPS][EMIT_STAGE];      // translated lifted end points
   __shared__ double s_pre[EMIT_WARPS][EMIT_STAGE];       // S0 prefix sums
   const int wib = (threadIdx.x >> 5);
-  const bool staged = tree && (s1 - s0) <= EMIT_STAGE;
+  const bool staged = tree && (s1 - s0_) <= EMIT_STAGE;
   if (staged) {
-    for (int s = s0 + lane; s < s1; s += 32) {
+    for (int s = s0_ + lane; s < s1; s += 32) {
       const double2 le = lend[s];
-      s_end[wib][s - s0] = make_double2(TX(le.x), TY(le.y));
-      s_pre[wib][s - s0] = s0pre[s];
+      s_end[wib][s - s0_] = make_double2(TX(le.x), TY(le.y));
+      s_pre[wib][s - s0_] = s0pre[s];
     }
     __syncwarp();
   }
@@ -752,33 +788,21 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     return (sizeof(R) == 8) ? (S * (1.0 + 0x1p-17) + G.M * 0x1p24) * (1.0 + 0x1p-17) : S * (1.0 + rel) + G.M;
   };
   int carry = 0;                                         // breaks before this chunk
-  for (int base = s0; base < s1; base += 32) {
+  for (int base = s0_; base < s1; base += 32) {
     const int s = base + lane;
     const bool in = s < s1;
-    const bool bk = in && s > s0 && brk[s];
+    const bool bk = in && s > s0_ && brk[s];
     const unsigned bm = __ballot_sync(0xffffffffu, bk);
     const int nb = carry + __popc(bm & ((2u << lane) - 1u));   // breaks in (s0, s]
     carry += __popc(bm);
-    // this chunk's K1 records (contiguous: 144 B per segment) staged with
-    // coalesced 16-B loads instead of one strided record per lane
-    {
-      const int cnt = min(32, s1 - base);
-      const double2 *src = reinterpret_cast<const double2 *>(prep + base);
-      for (int i = lane; i < cnt * PREP_D2; i += 32) s_prep[wib][i] = src[i];
-      __syncwarp();
-    }
     if (!in) continue;
-    const int idx = s - s0;
-    const int n = deg[s];
-    const int o = coff[s];
-    // end points (the interior control points are re-read pair by pair below,
-    // keeping few values live: occupancy of this latency-bound scatter)
-    const double px0 = TX(ctrl[2 * o]), py0 = TY(ctrl[2 * o + 1]);
-    const double pxn = TX(ctrl[2 * (o + n)]), pyn = TY(ctrl[2 * (o + n) + 1]);
+    const int idx = s - s0_;
+    const double2 e0 = lsta[s], e1 = lend[s];             // lifted end points (K2a)
+    const double px0 = TX(e0.x), py0 = TY(e0.y), pxn = TX(e1.x), pyn = TY(e1.y);
     int r;
     if (!tree) {
       r = r_first + idx + nb;
-      if (s == s0) put_rec<R>(hot, r - 1, px0, py0, 0.0, K_MOVE | fa);
+      if (s == s0_) put_rec<R>(hot, r - 1, px0, py0, 0.0, K_MOVE | fa);
       else if (bk) put_rec<R>(hot, r - 1, px0, py0, 0.0, K_MOVEG | fa);
     } else {
       // path hierarchy: each chain of m segments becomes a pre-order
@@ -788,7 +812,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
       const int j = idx - ch.x;
       int a = 0, bnd = ch.y - 1, off = r_first + 2 * ch.x;
       if (j == 0) {
-        if (s == s0) put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVE | fa);
+        if (s == s0_) put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVE | fa);
         else put_rec<R>(hot, off - 1, px0, py0, 0.0, K_MOVEG | fa);
       }
       int depth = 0;
@@ -804,17 +828,17 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
         ++depth;
         if (j == a) {
           // SPAN over chain segments [a, bnd]: foci = run ends, span = sum of S0
-          const int se = s0 + ch.x + bnd;                // last segment of the run
-          const int sa = s0 + ch.x + a;
+          const int se = s0_ + ch.x + bnd;               // last segment of the run
+          const int sa = s0_ + ch.x + a;
           double ex, ey, sum;
           if (staged) {
-            const double2 le = s_end[wib][se - s0];
+            const double2 le = s_end[wib][se - s0_];
             ex = le.x; ey = le.y;
-            sum = s_pre[wib][se - s0] - (sa > s0 ? s_pre[wib][sa - 1 - s0] : 0.0);
+            sum = s_pre[wib][se - s0_] - (sa > s0_ ? s_pre[wib][sa - 1 - s0_] : 0.0);
           } else {
             const double2 le = lend[se];                 // its lifted end point (K2a)
             ex = TX(le.x); ey = TY(le.y);
-            sum = s0pre[se] - (sa > s0 ? s0pre[sa - 1] : 0.0);
+            sum = s0pre[se] - (sa > s0_ ? s0pre[sa - 1] : 0.0);
           }
           const int sub = 2 * (bnd - a + 1) - 2;          // records of the subtree after the SPAN
           put_rec<R>(hot, off, ex, ey, filter_span(sum), K_SPAN | fa | ((uint32_t)sub << 8));
@@ -824,57 +848,25 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
       }
       r = off;
     }
-    const double2 *pr2 = &s_prep[wib][lane * PREP_D2];   // this segment's K1 record (staged)
-    const double2 bs = pr2[0];                            // (B, S0)
-    const double bpB = bs.x, bpS0 = bs.y;
     // Root span (Eq. 1, R9) with the R5 margin.  fp64 records: the span of the
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // and the filter's (1 - 2^-18) error shrink folded in as a further
     // (1 + 2^-17); fp32 records: S0 (1 + 2^-17) + M32.
-    const double S0 = filter_span(bpS0);
-    const double Bm = bpB * (1.0 + rel);
-    const R Br = (sizeof(R) == 4) ? (R)f_up(Bm) : (R)Bm;
-    put_rec<R>(hot, r, pxn, pyn, S0, K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
-    // cold record written field pair by field pair (vector stores, no local copy)
-    Cold<R> *Cp = cold + G.cold_off + idx;
-    st2<R>(&Cp->f0x, (R)px0, (R)py0);
-    st2<R>(&Cp->f1x, (R)pxn, (R)pyn);
-    st2<R>(&Cp->B, Br, (sizeof(R) == 4) ? (R)f_up(G.M) : (R)G.M);
-    *reinterpret_cast<int2 *>(&Cp->n) = make_int2(n, 0);
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const double2 bq = pr2[1 + q / 2];
-      const double b0 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.x)) * (1.0 + rel);
-      const double b1 = (dbg_flags & 1 ? bpB : fmin(bpB, bq.y)) * (1.0 + rel);
-      st2<float>(&Cp->Bq[q], f_up(b0), f_up(b1));   // fp32 rounded up: still upper bounds
-      const double2 lq = pr2[5 + q / 2];
-      const double l0 = lq.x * (1.0 + rel), l1 = lq.y * (1.0 + rel);
-      st2<float>(&Cp->Lq[q], f_up(l0), f_up(l1));
-    }
-    // homogeneous Horner coefficients c_j = C(n,j) w_j (x_j, y_j, 1), zero above n
-#pragma unroll
-    for (int j = 0; j < 6; j += 2) {
-      R cx2[2], cy2[2], cw2[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int jj = j + h;
-        cx2[h] = cy2[h] = cw2[h] = (R)0;
-        if (jj <= n) {
-          const double wj = wts ? wts[o + jj] : 1.0;
-          const double cw = binom5(n, jj) * wj;
-          cx2[h] = (R)(cw * TX(ctrl[2 * (o + jj)]));
-          cy2[h] = (R)(cw * TY(ctrl[2 * (o + jj) + 1]));
-          cw2[h] = (R)cw;
-        }
-      }
-      st2<R>(&Cp->cx[j], cx2[0], cx2[1]);
-      st2<R>(&Cp->cy[j], cy2[0], cy2[1]);
-      st2<R>(&Cp->cw[j], cw2[0], cw2[1]);
-    }
+    put_rec<R>(hot, r, pxn, pyn, filter_span(s0[s]), K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
+    // the copy record: base segment, target face, lift shift, copy translate
+    const int2 k = shift[s];
+    CopyRec cr;
+    cr.s = s;
+    cr.face = G.face;
+    cr.ksu = pu ? k.x : 0;
+    cr.ksv = pv ? k.y : 0;
+    cr.ku = pu ? G.ku : 0;
+    cr.kv = pv ? G.kv : 0;
+    copy[G.cold_off + idx] = cr;
   }
   if (lane == 0) {
-    int r = tree ? G.rec_off + cull + 1 + tree_recs(s1 - s0, omit_root ? OMIT_LEVELS : 0)
-                 : r_first + (s1 - s0) + carry;
+    int r = tree ? G.rec_off + cull + 1 + tree_recs(s1 - s0_, omit_root ? OMIT_LEVELS : 0)
+                 : r_first + (s1 - s0_) + carry;
     if (G.flags & PF_TAIL_CLOSEG) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_CLOSEG | fa);
     if (G.flags & PF_TAIL_XCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_XCH | fa);
     if (G.flags & PF_TAIL_NCH) put_rec<R>(hot, r++, 0.0, 0.0, 0.0, K_NCH | fa);
@@ -1469,7 +1461,8 @@ void free_handle(wn_faces_t F) {
   // stream-ordered frees on the legacy stream, after the handle's last use
   // (its build or its latest query, on whatever stream that ran)
   if (F->last_use) cudaStreamWaitEvent(0, F->last_use, 0);
-  void *ps[] = {F->hot, F->cold, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
+  if (F->owns_cold && F->cold) cache_free(F->cold, 0);
+  void *ps[] = {F->hot, F->copy, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
                 F->face_per, F->face_ok, F->face_M, F->face_box, F->counters};
   for (void *p : ps)
     if (p) cache_free(p, 0);
@@ -1484,15 +1477,16 @@ void free_handle(wn_faces_t F) {
 // buffers are read only by work that completes before wn_build_faces returns.
 struct BuildCtx {
   int32_t n_faces, n_loops, n_segs;
-  const double *ctrl, *w;
   const int32_t *deg, *lso, *flo;
   const uint8_t *per;
   const double *dom;
   int32_t *coff, *loop_face;
-  SegPrep *prep;
+  double *s0;       // per segment: root span S0 (K1, unmargined)
+  int2 *shift;      // per segment: lift shift (K2a)
   uint8_t *brk;
   int2 *chain;      // per segment: (chain start index within its loop, chain length)
   double *s0pre;    // per segment: prefix sum of root spans S0 along its loop
+  double2 *lsta;    // per segment: lifted start point
   double2 *lend;    // per segment: lifted end point
   LoopInfo *info;
   cudaStream_t st;
@@ -1500,9 +1494,10 @@ struct BuildCtx {
 
 // K1 launch, shared by wn_build_faces and wn_segment_prep: segments sorted by
 // degree (3-bit radix sort), then one kernel per degree over its range of the
-// sorted order, each with its own register budget (PREP_SPLIT; 0 = one k_prep).
+// sorted order, each with its own register budget (PREP_SPLIT CTAs per SM).
+template <class Sink>
 cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, const double *ctrl, const double *w,
-                      SegPrep *prep, uint8_t *serr, DevBuf &D, cudaStream_t st) {
+                      const Sink &sink, uint8_t *serr, DevBuf &D, cudaStream_t st) {
   if (n_segs <= 0) return cudaSuccess;
   int32_t *d_iota = nullptr, *d_order = nullptr, *d_degs = nullptr;
   cudaError_t e;
@@ -1516,22 +1511,17 @@ cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, c
   if ((e = D.alloc(&dt, tmp)) != cudaSuccess) return e;
   cub::DeviceRadixSort::SortPairs(dt, tmp, deg, d_degs, d_iota, d_order, n_segs, 0, 3, st);
   g_build_launches += 4;
-#if PREP_SPLIT
   int32_t *d_bnd = nullptr;
   if ((e = D.alloc(&d_bnd, 9)) != cudaSuccess) return e;
   k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
   const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
-  k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
-  k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
-  k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
-  k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
-  k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, prep, serr, d_order);
-  k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, prep, serr, d_order);
+  k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, sink, serr, d_order);
   g_build_launches += 7;
-#else
-  k_prep<<<(n_segs + 127) / 128, 128, 0, st>>>(n_segs, deg, coff, ctrl, w, prep, serr, d_order);
-  ++g_build_launches;
-#endif
   return cudaGetLastError();
 }
 
@@ -1542,9 +1532,8 @@ cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces
   const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
   ++g_build_launches;
   k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, B.st>>>(
-      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.deg, B.coff, B.ctrl, B.w, B.prep, B.brk, B.chain,
-      B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, (Cold<R> *)F->cold,
-      std::getenv("WN_DBG") ? atoi(std::getenv("WN_DBG")) : 0);
+      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.lsta, B.s0, B.shift, B.brk, B.chain,
+      B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, F->copy);
   return cudaGetLastError();
 }
 
@@ -1553,7 +1542,8 @@ cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces
 // the device)
 template <typename R>
 wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<uint8_t> &fper,
-                        const std::vector<double> &fdom, const std::vector<double> &fM, wn_faces_t F) {
+                        const std::vector<double> &fdom, const std::vector<double> &fM, void *base_cold,
+                        wn_faces_t F) {
   cudaStream_t st = B.st;
   const int nf = (int)fper.size();
   F->n_faces = nf;
@@ -1562,7 +1552,9 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   F->n_lines = plan.n_lines;
   F->n_groups = plan.n_cull;
   WN_CUDA(cache_alloc((void **)&F->hot, sizeof(Hot<R>) * (size_t)std::max(plan.recs, 1), st));
-  WN_CUDA(cache_alloc((void **)&F->cold, sizeof(Cold<R>) * (size_t)std::max(plan.colds, 1), st));
+  F->cold = base_cold;      // the main build's per-segment records (borrowed)
+  F->owns_cold = 0;
+  WN_CUDA(cache_alloc((void **)&F->copy, sizeof(CopyRec) * (size_t)std::max(plan.colds, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_rec_off, sizeof(int32_t) * (nf + 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_cold_off, sizeof(int32_t) * (nf + 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_order, sizeof(int32_t) * std::max(nf, 1), st));
@@ -1572,8 +1564,8 @@ wn_status_t materialise(const BuildCtx &B, const Plan &plan, const std::vector<u
   WN_CUDA(cache_alloc((void **)&F->face_M, sizeof(double) * std::max(nf, 1), st));
   WN_CUDA(cache_alloc((void **)&F->face_box, sizeof(float4) * std::max(nf, 1), st));
   WN_CUDA(cudaMemsetAsync(F->face_box, 0, sizeof(float4) * std::max(nf, 1), st));   // probes: no regrouping
-  WN_CUDA(cache_alloc((void **)&F->counters, 12 * sizeof(unsigned long long), st));
-  F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(Cold<R>) * plan.colds + (int64_t)nf * 50;
+  WN_CUDA(cache_alloc((void **)&F->counters, 16 * sizeof(unsigned long long), st));
+  F->bytes = (int64_t)sizeof(Hot<R>) * plan.recs + (int64_t)sizeof(CopyRec) * plan.colds + (int64_t)nf * 50;
   int32_t maxr = 0;
   for (int f = 0; f < nf; ++f) maxr = std::max(maxr, plan.rec_off[f + 1] - plan.rec_off[f]);
   F->max_face_records = maxr;
@@ -1718,17 +1710,14 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   tr.mark("csr copies + degree scan (async)");
   // --- K1 prep, loop->face, K2a lift ---
   uint8_t *d_serr = nullptr;
-  double *d_lctrl = nullptr, *d_lw = nullptr;   // lifted control points / weights (k_lift): <= 6 per segment
-  WN_CUDA(D.alloc(&B.prep, n_segs));
+  WN_CUDA(D.alloc(&B.s0, n_segs));
   WN_CUDA(D.alloc(&d_serr, n_segs));
   WN_CUDA(D.alloc(&B.loop_face, n_loops));
-  WN_CUDA(D.alloc(&d_lctrl, 12 * (size_t)n_segs));
-  if (ctrl_w) WN_CUDA(D.alloc(&d_lw, 6 * (size_t)n_segs));
-  B.ctrl = d_lctrl;
-  B.w = d_lw;
+  WN_CUDA(D.alloc(&B.shift, n_segs));
   WN_CUDA(D.alloc(&B.brk, n_segs));
   WN_CUDA(D.alloc(&B.chain, n_segs));
   WN_CUDA(D.alloc(&B.s0pre, n_segs));
+  WN_CUDA(D.alloc(&B.lsta, n_segs));
   WN_CUDA(D.alloc(&B.lend, n_segs));
   WN_CUDA(D.alloc(&B.info, n_loops));
   // K2a and K2b (lifting, then the device planner) on an auxiliary stream,
@@ -1743,7 +1732,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   if (n_loops)
     k_lift<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st2>>>(n_loops, n_faces, n_segs, B.lso, B.loop_face, face_periodic,
                                                                        face_domain, B.deg, B.coff, ctrl_uv, ctrl_w,
-                                                                       d_lctrl, d_lw, B.brk, B.chain, B.lend, B.info);
+                                                                       B.shift, B.brk, B.chain, B.lsta, B.lend, B.info);
   g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
   WN_CUDA(cudaGetLastError());
   if (tr.on) { cudaStreamSynchronize(st2); tr.mark("(trace) k_loop_face + k_lift"); }
@@ -1817,9 +1806,17 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     if (rc != WN_OK) return rc;
   }
   // K1 (reads the caller's control points: the host waits for g_ev_k1 before returning)
-  WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w, B.prep, d_serr, D, st));
+  // K1 writes the handle's per-segment cold records (BaseCold) and S0
+  WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(BaseCold<float>) : sizeof(BaseCold<double>)) * (size_t)std::max(n_segs, 1),
+                      st));
+  if (fp32)
+    WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
+                      ColdSink<float>{(BaseCold<float> *)F->cold, B.s0, std::ldexp(1.0, -17)}, d_serr, D, st));
+  else
+    WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
+                      ColdSink<double>{(BaseCold<double> *)F->cold, B.s0, std::ldexp(1.0, -40)}, d_serr, D, st));
   if (n_loops) {
-    k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, B.lso, B.prep, B.s0pre);
+    k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, B.lso, B.s0, B.s0pre);
     ++g_build_launches;
   }
   WN_CUDA(cudaGetLastError());
@@ -1980,11 +1977,20 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     std::vector<QueryRec> qs;
     for (const Cand &c : cands) qs.push_back({vface[c.alpha], c.px, c.py});
     // run probes through the query kernel on a temporary handle (fp64, crossing mode)
+    // the probes run fp64 records: an fp32 build gets fp64 base cold records for them
+    void *probe_cold = F->cold;
+    if (fp32) {
+      double *tmp_s0 = nullptr;
+      WN_CUDA(D.alloc((BaseCold<double> **)&probe_cold, std::max(n_segs, 1)));
+      WN_CUDA(D.alloc(&tmp_s0, std::max(n_segs, 1)));
+      WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
+                        ColdSink<double>{(BaseCold<double> *)probe_cold, tmp_s0, std::ldexp(1.0, -40)}, d_serr, D, st));
+    }
     WN_CUDA(cudaStreamSynchronize(st));   // K1 outputs (bounds, span prefixes) are read by the probes' k_emit
     auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
       wn_faces_t T = new wn_faces_s();
       T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0; T->opt.angle_mode = 0;   // the probe records are crossing-mode (C.angle = false)
-      wn_status_t rc = materialise<double>(B, VP, vper, vdom, vM, T);
+      wn_status_t rc = materialise<double>(B, VP, vper, vdom, vM, probe_cold, T);
       if (rc != WN_OK) { free_handle(T); return rc; }
       const int nq = (int)Q.size();
       std::vector<int32_t> hf(nq);
@@ -2094,9 +2100,10 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   F->n_bands = (int64_t)h_sum->bands;
   F->max_face_records = h_sum->maxr;
   WN_CUDA(cache_alloc(&F->hot, (fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * (size_t)std::max(h_sum->tot_r, 1), st));
-  WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * (size_t)std::max(h_sum->tot_c, 1), st));
+  WN_CUDA(cache_alloc((void **)&F->copy, sizeof(CopyRec) * (size_t)std::max(h_sum->tot_c, 1), st));
   F->bytes = (int64_t)(fp32 ? sizeof(Hot<float>) : sizeof(Hot<double>)) * h_sum->tot_r +
-             (int64_t)(fp32 ? sizeof(Cold<float>) : sizeof(Cold<double>)) * h_sum->tot_c + (int64_t)n_faces * 50;
+             (int64_t)(fp32 ? sizeof(BaseCold<float>) : sizeof(BaseCold<double>)) * n_segs +
+             (int64_t)sizeof(CopyRec) * h_sum->tot_c + (int64_t)n_faces * 50;
   const int ng = h_sum->tot_g;
   // the plan groups: written by k_plan_fill on st2, read by k_emit on st --
   // released on st (after k_emit), not with the auxiliary stream's buffers
@@ -2172,7 +2179,7 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
   // through this entry point cover the shipped K1 code.
   SegPrep *dst = (SegPrep *)out;
   if ((uintptr_t)out & 15) WN_CUDA(D.alloc(&dst, n_segs));
-  WN_CUDA(launch_k1(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, dst, serr, D, st));
+  WN_CUDA(launch_k1(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, PrepSink{dst}, serr, D, st));
   if ((void *)dst != (void *)out)
     WN_CUDA(cudaMemcpyAsync(out, dst, sizeof(SegPrep) * (size_t)n_segs, cudaMemcpyDeviceToDevice, st));
   WN_CUDA(cudaGetLastError());

@@ -62,21 +62,47 @@ struct __align__(16) Hot<float> {
   uint32_t meta;
 };
 
-// Cold record: exact chain end points, the derivative bound and Horner-ready
-// homogeneous coefficients c_j = C(n,j) w_j (x_j, y_j, 1) (O(n) evaluation,
-// Table 1).
+// Cold records, read only by the recursion of hard pairs (a6).  Split in two:
+//  * BaseCold: one per INPUT segment, written by K1 -- everything that is
+//    invariant under the lattice translations of lifting and copy emission:
+//    the exact stored end points, the derivative bound (A.1; R29),
+//    the Horner-ready homogeneous coefficients c_j = C(n,j) w_j (x_j, y_j, 1)
+//    of the STORED (unlifted) curve (O(n) evaluation, Table 1), the
+//    8 dyadic piece bounds and piece arc-length bounds.
+//  * CopyRec: one per EMITTED segment (a lifted, lattice-translated copy),
+//    written by k_emit -- its base segment, target face and the two integer
+//    translations (lift shift k_s, copy translate k_g).  The copy's end points
+//    are lat(lat(x, k_s, T), k_g, T): the same operations k_emit uses for the
+//    hot chain points, so they are bit-identical to them (telescoping).
 template <typename R>
-struct __align__(16) Cold {   // 16-B aligned; every field pair below starts on a 16-B (fp64) boundary
-  R f0x, f0y, f1x, f1y;
-  R B;      // derivative bound (A.1; R29) incl. relative margin
-  R M;      // absolute margin (R5)
-  R cx[6], cy[6], cw[6];
-  float Bq[8];  // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin, rounded up
-  float Lq[8];  // arc-length bound (control-polygon length) of each dyadic piece, incl. margin, rounded up
-  int32_t n, pad;
+struct BaseCold;
+template <>
+struct __align__(16) BaseCold<double> {   // 256 B; coefficient pairs on 16-B boundaries
+  double x0, y0, xn, yn;   // exact stored (unlifted) end control points
+  double B;                // derivative bound incl. relative margin
+  int32_t n, pad;          // degree
+  double cx[6], cy[6], cw[6];
+  float Bq[8];   // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin, rounded up
+  float Lq[8];   // arc-length bound (control-polygon length) of each dyadic piece, incl. margin, rounded up
+};
+template <>
+struct __align__(16) BaseCold<float> {    // 192 B
+  double x0, y0, xn, yn;   // exact stored end points (fp64: the hot fp32 points are rounded from the fp64 lift)
+  float B;
+  int32_t n;
+  float cx[6], cy[6], cw[6];
+  float Bq[8];
+  float Lq[8];
+  float pad[2];
+};
+struct __align__(8) CopyRec {
+  int32_t s;          // base (input) segment
+  int32_t face;       // face whose domain holds the periods of the translations
+  int32_t ksu, ksv;   // lift shift of the segment (0 on non-periodic axes)
+  int32_t ku, kv;     // lattice translate of the copy (0 on non-periodic axes)
 };
 
-// K1 output per input segment (translation invariant)
+// K1 output for wn_segment_prep (diagnostics): per input segment, no margins
 struct SegPrep {
   double B, S0;
   double Bq[8];
@@ -101,7 +127,7 @@ struct Tile {
 struct HardEntry {
   double px, py;      // reduced query point
   int32_t q;          // query index (output position)
-  uint32_t c;         // global cold record index | angle-mode bit 31
+  uint32_t c;         // global copy record index (CopyRec) | angle-mode bit 31
 };
 
 // build-plan group (host -> device), 32 B
@@ -177,6 +203,28 @@ __device__ __forceinline__ R canon_cross(R ax, R ay, R bx, R by) {
   return cr == R(0) ? R(0) : cr;   // -0 -> +0 (R11)
 }
 
+// Lattice translate x + k T with explicit roundings (no contraction): the one
+// formula every lifted / translated point of the library goes through, so
+// chain points computed by different kernels are bit-identical.
+__device__ __forceinline__ double lat(double x, int k, double T) { return __dadd_rn(x, __dmul_rn((double)k, T)); }
+
+// The frame of an emitted copy (CopyRec): lat(lat(x, k_s, T), k_g, T) =
+// (x + k_s T) + k_g T per axis, with the products precomputed (same roundings).
+struct CopyFrame {
+  double au, bu, av, bv;   // k_s Tu, k_g Tu, k_s Tv, k_g Tv
+  __device__ __forceinline__ double X(double x) const { return __dadd_rn(__dadd_rn(x, au), bu); }
+  __device__ __forceinline__ double Y(double y) const { return __dadd_rn(__dadd_rn(y, av), bv); }
+};
+__device__ __forceinline__ CopyFrame copy_frame(const CopyRec &c, const double *__restrict__ face_dom) {
+  const double Tu = face_dom[4 * c.face + 1], Tv = face_dom[4 * c.face + 3];
+  CopyFrame F;
+  F.au = __dmul_rn((double)c.ksu, Tu);
+  F.bu = __dmul_rn((double)c.ku, Tu);
+  F.av = __dmul_rn((double)c.ksv, Tv);
+  F.bv = __dmul_rn((double)c.kv, Tv);
+  return F;
+}
+
 // omega(p,a,b) * 2pi = atan2(cross, dot) (R7, R11), coordinates relative to p
 template <typename R>
 __device__ __forceinline__ R chord_angle(R ax, R ay, R bx, R by) {
@@ -197,7 +245,9 @@ struct wn_faces_s {
   int max_depth = 48;
   int device = 0;
   void *hot = nullptr;             // Hot<R>[n_records]
-  void *cold = nullptr;            // Cold<R>[n_seg]
+  void *cold = nullptr;            // BaseCold<R>[n input segments]
+  wn::CopyRec *copy = nullptr;     // [n_seg] emitted segments
+  int owns_cold = 1;               // 0: `cold` borrowed from another handle (pairing probes)
   int32_t *face_rec_off = nullptr; // [n_faces+1]
   int32_t *face_cold_off = nullptr;// [n_faces+1]
   int32_t *face_order = nullptr;   // [n_faces] by cost, descending

@@ -74,7 +74,8 @@ __device__ __forceinline__ double reduce_coord(double x, double x0, double T) {
 template <typename R>
 struct QParams {
   const Hot<R> *hot;
-  const Cold<R> *cold;
+  const BaseCold<R> *cold;   // per input segment
+  const CopyRec *copy;       // per emitted segment
   const int32_t *face_rec_off;
   const int32_t *face_cold_off;
   const double *face_dom;
@@ -127,7 +128,9 @@ __device__ __forceinline__ void grid_point(const QParams<R> &P, int64_t q, doubl
 // Counters (optional, COUNT=true): 0 (query, segment) root tests, 1 hard pairs,
 // 2 nodes, 3 evaluations, 4 leaves, 5 max depth, 6 warp-level skips (culled
 // groups + pruned hierarchy subtrees), 7 on-boundary, 8 (query, SPAN) tests,
-// 9 warp-record iterations of phase 1
+// 9 warp-record iterations of phase 1, 10 (query, SPAN) tests that descend
+// (the rest substitute the run's chord), 11 (query, SEG) tests that substitute
+// the chord (pruned, a5)
 template <bool COUNT>
 __device__ __forceinline__ void cnt_add(unsigned long long *c, int i, unsigned long long v) {
   if (COUNT && v) atomicAdd(c + i, v);
@@ -140,7 +143,7 @@ __device__ __forceinline__ void cnt_add(unsigned long long *c, int i, unsigned l
 // zero coefficients above n, so every lane of a warp runs the same code
 // whatever its segment's degree (the coefficient pairs load as 16-B vectors).
 template <typename R>
-__device__ __forceinline__ void eval_point(const Cold<R> *__restrict__ C, int n, R t, R &x, R &y) {
+__device__ __forceinline__ void eval_point(const BaseCold<R> *__restrict__ C, int n, R t, R &x, R &y) {
   const R u = R(1) - t;
   R cx[6], cy[6], cw[6];
   if constexpr (sizeof(R) == 8) {
@@ -174,20 +177,39 @@ struct HardResult {
   bool ob;
 };
 
-// One hard pair (query point q, segment C) by Alg. 1 with an explicit stack of
-// right end points.  The root is split immediately (phase 1
-// could not certify it as pruned).  All arithmetic in R, exact decisions.
+// Margin M of a face as R (fp32: rounded up, still a valid margin)
+template <typename R>
+__device__ __forceinline__ R margin_r(double M) {
+  if constexpr (sizeof(R) == 8) return M;
+  else return __double2float_ru(M);
+}
+
+// Split point of a copy: the base (stored) curve evaluated by Horner, then
+// moved into the copy's frame (lift shift + copy translate, CopyFrame).
+template <typename R>
+__device__ __forceinline__ void eval_copy(const BaseCold<R> *__restrict__ C, int n, const CopyFrame &Fr, R t, R &x,
+                                          R &y) {
+  R x0, y0;
+  eval_point(C, n, t, x0, y0);
+  x = (R)Fr.X((double)x0);
+  y = (R)Fr.Y((double)y0);
+}
+
+// One hard pair (query point q, emitted segment = copy record cr of base
+// segment C) by Alg. 1 with an explicit stack of right end points (DESIGN.md
+// 6).  The root is split immediately (phase 1 could not certify it as
+// pruned).  All arithmetic in R, exact decisions; the copy's end points are
+// lat(lat(x, k_s), k_g) exactly as the emission computed the hot chain points.
 template <typename R, bool COUNT>
-__device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx, R qy, bool angle, R eps,
-                                             int max_depth, unsigned long long *counters) {
-  const R M = __ldg(&C->M);
+__device__ __noinline__ HardResult hard_pair(const BaseCold<R> *__restrict__ C, const CopyFrame Fr, R M, R qx, R qy,
+                                             bool angle, R eps, int max_depth, unsigned long long *counters) {
   const int n = __ldg(&C->n);
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
-  R Lx = __ldg(&C->f0x) - qx, Ly = __ldg(&C->f0y) - qy;
+  R Lx = (R)Fr.X(__ldg(&C->x0)) - qx, Ly = (R)Fr.Y(__ldg(&C->y0)) - qy;
   R dL = dsqrt(Lx * Lx + Ly * Ly);
-  stx[0] = __ldg(&C->f1x) - qx;
-  sty[0] = __ldg(&C->f1y) - qy;
+  stx[0] = (R)Fr.X(__ldg(&C->xn)) - qx;
+  sty[0] = (R)Fr.Y(__ldg(&C->yn)) - qy;
   std_[0] = 0;
   int sp = 1;
   double ta = 0.0;   // node start: exact dyadic (double also for fp32 records)
@@ -238,7 +260,7 @@ __device__ __noinline__ HardResult hard_pair(const Cold<R> *__restrict__ C, R qx
       if (d >= max_depth) { res.ob = true; break; }         // depth cap (R6)
       const double tm = ta + ldexp(1.0, -(d + 1));         // m = (a+b)/2
       R mx, my;
-      eval_point(C, n, (R)tm, mx, my);
+      eval_copy(C, n, Fr, (R)tm, mx, my);
       ++evals;
       std_[sp - 1] = (int8_t)(d + 1);
       stx[sp] = mx - qx;
@@ -443,7 +465,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   asm volatile("mov.u32 %0, %1;" : "=r"(sbase) : "r"(smem_u32(s_rec)));
   unsigned phase = 0;
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
-  unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0;
+  unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0, c_desc = 0, c_prn = 0;
   __syncthreads();               // barrier initialised
   // pend bits of the lane's current query: 1 hard pairs queued, 2 one of them
   // overflowed the queue, 4 entries still in the warp buffer
@@ -723,6 +745,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             if (COUNT && act) ++c_span;
             // descend unless every active lane prunes the whole run
             const bool descend = act && !pr;
+            if (COUNT && descend) ++c_desc;
             if (!__any_sync(0xffffffffu, descend)) {
               // every active lane substitutes the run's chord (homotopy)
               if (__any_sync(0xffffffffu, act && (u1 != up || ANGLE))) {
@@ -743,8 +766,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             }
           } else {
             const bool need = act && (!pr || u1 != up || ANGLE);
+            bool hard = false;
             if (__any_sync(0xffffffffu, need)) {
-              bool hard = false;
               if (need) {
                 if (!(df > eps_c)) {                             // filter cannot certify d >= eps
                   if constexpr (F64) {
@@ -780,6 +803,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             }
             if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
             if (COUNT && act) ++c_pairs;
+            if (COUNT && act && !hard && !onb) ++c_prn;      // chord substituted (a5)
           }
         } else if (kind == K_MOVE || kind == K_MOVEG) {
           const double nx = h.x - px, ny = h.y - py;
@@ -858,6 +882,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     cnt_add<COUNT>(P.counters, 6, c_cull);
     cnt_add<COUNT>(P.counters, 8, c_span);
     cnt_add<COUNT>(P.counters, 9, c_rec);
+    cnt_add<COUNT>(P.counters, 10, c_desc);
+    cnt_add<COUNT>(P.counters, 11, c_prn);
   }
 }
 
@@ -879,7 +905,8 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
-  const Cold<R> *C = nullptr;
+  const BaseCold<R> *C = nullptr;
+  CopyFrame Fr{0.0, 0.0, 0.0, 0.0};
   R qx = 0, qy = 0, M = 0, Lx = 0, Ly = 0, dL = 0;
   int n = 0, sp = 0, xsum = 0, q = 0;
   double ta = 0.0, fsum = 0.0;
@@ -893,17 +920,19 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       if (i + stride < total)   // this lane's next pair, to L2 while this one recurses
         asm volatile("prefetch.global.L2 [%0];" ::"l"(P.hq + i + stride));
       angle = H.c >> 31;
-      C = P.cold + (H.c & 0x7fffffffu);
+      const CopyRec cr = P.copy[H.c & 0x7fffffffu];
+      C = P.cold + cr.s;
+      Fr = copy_frame(cr, P.face_dom);
       qx = (R)H.px;
       qy = (R)H.py;
       q = H.q;
-      M = __ldg(&C->M);
+      M = margin_r<R>(__ldg(P.face_M + cr.face));
       n = __ldg(&C->n);
-      Lx = __ldg(&C->f0x) - qx;
-      Ly = __ldg(&C->f0y) - qy;
+      Lx = (R)Fr.X(__ldg(&C->x0)) - qx;
+      Ly = (R)Fr.Y(__ldg(&C->y0)) - qy;
       dL = dsqrt(Lx * Lx + Ly * Ly);
-      stx[0] = __ldg(&C->f1x) - qx;
-      sty[0] = __ldg(&C->f1y) - qy;
+      stx[0] = (R)Fr.X(__ldg(&C->xn)) - qx;
+      sty[0] = (R)Fr.Y(__ldg(&C->yn)) - qy;
       std_[0] = 0;
       sp = 1;
       ta = 0.0;
@@ -956,7 +985,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       } else {
         const double tm = ta + ldexp(1.0, -(d + 1));       // m = (a+b)/2
         R mx, my;
-        eval_point(C, n, (R)tm, mx, my);
+        eval_copy(C, n, Fr, (R)tm, mx, my);
         ++evals;
         std_[sp - 1] = (int8_t)(d + 1);
         stx[sp] = mx - qx;
@@ -1004,7 +1033,7 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id, in
     if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
     if (sizeof(R) == 4) { u = (double)(float)u; v = (double)(float)v; }
     const int rec0 = P.face_rec_off[f], rec1 = P.face_rec_off[f + 1];
-    const Cold<R> *cold_face = P.cold + P.face_cold_off[f];
+    const CopyRec *copy_face = P.copy + P.face_cold_off[f];
     double cx = 0, cy = 0, cd = 0, ax = 0, ay = 0, fr = 0;
     int xs = 0, halves = 0;
     bool ob = false;
@@ -1022,8 +1051,10 @@ __global__ void k_overflow(QParams<R> P, const int32_t *__restrict__ face_id, in
             if (meta & F_ANGLE) fr += chord_angle(cx, cy, nx, ny);
             else xs += xcount(cx, cy, nx, ny);
           } else {
-            const HardResult res = hard_pair<R, false>(cold_face + (meta >> 8), (R)u, (R)v, (meta & F_ANGLE) != 0,
-                                                       (R)P.eps, P.max_depth, nullptr);
+            const CopyRec cr = copy_face[meta >> 8];
+            const HardResult res = hard_pair<R, false>(P.cold + cr.s, copy_frame(cr, P.face_dom),
+                                                       margin_r<R>(P.face_M[cr.face]), (R)u, (R)v,
+                                                       (meta & F_ANGLE) != 0, (R)P.eps, P.max_depth, nullptr);
             if (res.ob) { ob = true; break; }
             xs += res.xsum;
             fr += res.fsum;
@@ -1296,7 +1327,7 @@ static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const
     }
   };
   if (F->counters_on) {
-    WN_CUDA(cudaMemsetAsync(F->counters, 0, 12 * sizeof(unsigned long long), st));
+    WN_CUDA(cudaMemsetAsync(F->counters, 0, 16 * sizeof(unsigned long long), st));
     phase1(std::true_type{});
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
@@ -1385,7 +1416,8 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   ++launches;
   QParams<R> P;
   P.hot = (const Hot<R> *)F->hot;
-  P.cold = (const Cold<R> *)F->cold;
+  P.cold = (const BaseCold<R> *)F->cold;
+  P.copy = F->copy;
   P.face_rec_off = F->face_rec_off;
   P.face_cold_off = F->face_cold_off;
   P.face_dom = F->face_dom;
@@ -1472,7 +1504,8 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   ++launches;
   QParams<R> P;
   P.hot = (const Hot<R> *)F->hot;
-  P.cold = (const Cold<R> *)F->cold;
+  P.cold = (const BaseCold<R> *)F->cold;
+  P.copy = F->copy;
   P.face_rec_off = F->face_rec_off;
   P.face_cold_off = F->face_cold_off;
   P.face_dom = F->face_dom;

@@ -236,6 +236,16 @@ wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, const double 
  * Synchronous; uses the current device. */
 wn_status_t wn_measure_fp_peak(int fp32, double seconds, double *lane_fma_per_s, double *sm_mhz);
 
+/* Diagnostics: the recursion bounds the handle's hard-pair recursion uses, per
+ * INPUT segment s (in wn_build_faces order): out[s][23] = {B, Bq[0..7],
+ * Sp[0..13]} -- the derivative bound of Lemma 1 / App. A.1 (P:335-345,
+ * P:1095-1109, R29) with its relative margin, the bounds of the 8 dyadic
+ * pieces [q/8,(q+1)/8] (used for nodes of depth > 3, span = Bq 2^-d, Eq. 2
+ * P:351-356) and the spans of the depth-1..3 nodes (index 2^d - 2 + k: the
+ * minimum of 2^-d max Bq and the pieces' arc-length bounds, R9), as stored
+ * (fp32, rounded up).  `out` is a device pointer; synchronises `stream`. */
+wn_status_t wn_recursion_bounds(wn_faces_t faces, double *out, void *stream);
+
 /* libwn keeps freed device buffers (records, query scratch) in a per-device
  * cache for reuse; wn_trim_memory returns them to the driver. */
 void wn_trim_memory(void);

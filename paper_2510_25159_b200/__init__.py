@@ -30,7 +30,8 @@ FACE_STATUS = {0: "ok", 1: "B1", 2: "unbalanced", 3: "class", 4: "general_pq", 5
 EXPORTS = ["wn_build_faces", "wn_query", "wn_faces_info", "wn_set_counters", "wn_get_counters",
            "wn_set_timing", "wn_get_timing", "wn_free_faces", "wn_last_error", "wn_last_query_launches",
            "wn_last_build_launches", "wn_segment_prep", "wn_trim_memory", "wn_query_host", "wn_query_grid",
-           "wn_nurbs_to_bezier", "wn_build_faces_nurbs", "wn_measure_fp_peak"]
+           "wn_nurbs_to_bezier", "wn_build_faces_nurbs", "wn_measure_fp_peak",
+           "wn_recursion_bounds"]
 COUNTER_NAMES = ["pairs_tested", "hard_pairs", "nodes", "evals", "leaves", "max_depth",
                  "warp_skips", "on_boundary", "span_tests", "warp_records", "span_descended",
                  "seg_pruned"]
@@ -100,6 +101,8 @@ def load():
         L.wn_free_faces.argtypes = [vp]
         L.wn_last_error.restype = C.c_char_p
         L.wn_last_error.argtypes = []
+        L.wn_recursion_bounds.restype = C.c_int
+        L.wn_recursion_bounds.argtypes = [vp, vp, vp]
         L.wn_measure_fp_peak.restype = C.c_int
         L.wn_measure_fp_peak.argtypes = [C.c_int, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.wn_last_query_launches.restype = C.c_int32
@@ -328,6 +331,15 @@ class Faces:
         if rc != WN_OK:
             raise WNError(rc, last_error())
         return {k: getattr(inf, k) for k, _ in FacesInfo._fields_}
+
+    def recursion_bounds(self, n_segs):
+        """[n_segs, 23] = (B, Bq[8], Sp[14]) per input segment (wn_recursion_bounds)."""
+        torch = _torch()
+        out = torch.empty((max(int(n_segs), 1), 23), dtype=torch.float64, device=self.device)
+        rc = load().wn_recursion_bounds(self._h, _ptr(out), _stream(None, self.device))
+        if rc != WN_OK:
+            raise WNError(rc, last_error())
+        return out[:n_segs]
 
     def set_counters(self, enable=True):
         load().wn_set_counters(self._h, int(bool(enable)))

@@ -278,10 +278,36 @@ struct ColdSink {
     for (int k = 0; k < (int)(sizeof(BaseCold<R>) / 16); ++k) o[k] = make_uint4(0, 0, 0, 0);
     s0[s] = 0.0;
   }
+  // piece bounds go to Bq; the piece arc-length bounds are parked in Sp[0..7]
+  // until root() folds them into the per-node spans
   __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) const {
     BaseCold<R> *C = out + s;
     *reinterpret_cast<float2 *>(&C->Bq[q]) = make_float2(f_up(fmin(B, b0) * (1.0 + rel)), f_up(fmin(B, b1) * (1.0 + rel)));
-    *reinterpret_cast<float2 *>(&C->Lq[q]) = make_float2(f_up(l0 * (1.0 + rel)), f_up(l1 * (1.0 + rel)));
+    *reinterpret_cast<float2 *>(&C->Sp[q]) = make_float2(f_up(l0 * (1.0 + rel)), f_up(l1 * (1.0 + rel)));
+  }
+  // spans of the depth-1..3 nodes from the rounded-up piece values (sums and
+  // maxima of a few floats are exact in double; the result rounded up)
+  __device__ void spans(BaseCold<R> *C) const {
+    float bq[8], lq[8];
+#pragma unroll
+    for (int q = 0; q < 8; q += 2) {
+      const float2 b = *reinterpret_cast<const float2 *>(&C->Bq[q]);
+      const float2 l = *reinterpret_cast<const float2 *>(&C->Sp[q]);
+      bq[q] = b.x; bq[q + 1] = b.y; lq[q] = l.x; lq[q + 1] = l.y;
+    }
+    float sp[14];
+#pragma unroll
+    for (int d = 1; d <= 3; ++d)
+#pragma unroll
+      for (int k = 0; k < (1 << d); ++k) {
+        const int nq = 8 >> d;
+        double bm = 0.0, ls = 0.0;
+#pragma unroll
+        for (int q = k * nq; q < (k + 1) * nq; ++q) { bm = fmax(bm, (double)bq[q]); ls += (double)lq[q]; }
+        sp[(1 << d) - 2 + k] = f_up(fmin(ldexp(bm, -d), ls));
+      }
+#pragma unroll
+    for (int i = 0; i < 14; i += 2) *reinterpret_cast<float2 *>(&C->Sp[i]) = make_float2(sp[i], sp[i + 1]);
   }
   // end points (exact, stored coordinates), bound, degree, homogeneous Horner
   // coefficients c_j = (C(n,j) w_j) (x_j, y_j, 1), zero above the degree
@@ -289,6 +315,7 @@ struct ColdSink {
   __device__ void root(int s, double B, double S0, const double *px, const double *py, const double *W, int) const {
     BaseCold<R> *C = out + s;
     s0[s] = S0;
+    spans(C);
     *reinterpret_cast<double2 *>(&C->x0) = make_double2(px[0], py[0]);
     *reinterpret_cast<double2 *>(&C->xn) = make_double2(px[N], py[N]);
     const double Bm = B * (1.0 + rel);
@@ -1807,6 +1834,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   }
   // K1 (reads the caller's control points: the host waits for g_ev_k1 before returning)
   // K1 writes the handle's per-segment cold records (BaseCold) and S0
+  F->n_base = n_segs;
   WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(BaseCold<float>) : sizeof(BaseCold<double>)) * (size_t)std::max(n_segs, 1),
                       st));
   if (fp32)
@@ -2182,6 +2210,34 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
   WN_CUDA(launch_k1(n_segs, seg_degree, coff, ctrl_uv, ctrl_w, PrepSink{dst}, serr, D, st));
   if ((void *)dst != (void *)out)
     WN_CUDA(cudaMemcpyAsync(out, dst, sizeof(SegPrep) * (size_t)n_segs, cudaMemcpyDeviceToDevice, st));
+  WN_CUDA(cudaGetLastError());
+  WN_CUDA(cudaStreamSynchronize(st));
+  return WN_OK;
+}
+
+namespace wn {
+namespace {
+template <typename R>
+__global__ void k_rec_bounds(int32_t n, const BaseCold<R> *__restrict__ C, double *__restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  double *o = out + 23 * (size_t)s;
+  o[0] = (double)C[s].B;
+  for (int q = 0; q < 8; ++q) o[1 + q] = (double)C[s].Bq[q];
+  for (int i = 0; i < 14; ++i) o[9 + i] = (double)C[s].Sp[i];
+}
+}  // namespace
+}  // namespace wn
+
+extern "C" wn_status_t wn_recursion_bounds(wn_faces_t F, double *out, void *stream) {
+  if (!F || (!out && F->n_base > 0)) { set_error("wn_recursion_bounds: NULL"); return WN_ERR_ARG; }
+  if (F->n_base == 0) return WN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  WN_CUDA(cudaSetDevice(F->device));
+  if (F->ready) WN_CUDA(cudaStreamWaitEvent(st, F->ready, 0));
+  const int n = F->n_base;
+  if (F->precision == 1) k_rec_bounds<float><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<float> *)F->cold, out);
+  else k_rec_bounds<double><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<double> *)F->cold, out);
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaStreamSynchronize(st));
   return WN_OK;

@@ -76,14 +76,22 @@ struct __align__(16) Hot<float> {
 //    hot chain points, so they are bit-identical to them (telescoping).
 template <typename R>
 struct BaseCold;
+// Recursion spans (Eq. 2 with the tightest stored bound covering the node):
+//   Bq[q]  bound on the dyadic piece [q/8, (q+1)/8] (t-units): nodes of depth
+//          d > 3 lie inside one piece, span = Bq[q] 2^-d;
+//   Sp[i]  nodes of depth d = 1..3 are unions of whole pieces: span =
+//          min(2^-d max Bq, sum of the pieces' arc-length bounds Lq) (R9),
+//          tabulated per node, i = 2^d - 2 + k (no per-node loop in k_hard).
+// All incl. the relative margin, fp32 rounded up (still upper bounds).
 template <>
-struct __align__(16) BaseCold<double> {   // 256 B; coefficient pairs on 16-B boundaries
+struct __align__(16) BaseCold<double> {   // 288 B; coefficient pairs on 16-B boundaries
   double x0, y0, xn, yn;   // exact stored (unlifted) end control points
   double B;                // derivative bound incl. relative margin
   int32_t n, pad;          // degree
   double cx[6], cy[6], cw[6];
-  float Bq[8];   // bound on the dyadic pieces [q/8, (q+1)/8] (t-units), incl. margin, rounded up
-  float Lq[8];   // arc-length bound (control-polygon length) of each dyadic piece, incl. margin, rounded up
+  float Bq[8];
+  float Sp[14];
+  float pad2[2];
 };
 template <>
 struct __align__(16) BaseCold<float> {    // 192 B
@@ -92,7 +100,7 @@ struct __align__(16) BaseCold<float> {    // 192 B
   int32_t n;
   float cx[6], cy[6], cw[6];
   float Bq[8];
-  float Lq[8];
+  float Sp[14];
   float pad[2];
 };
 struct __align__(8) CopyRec {
@@ -248,6 +256,7 @@ struct wn_faces_s {
   void *cold = nullptr;            // BaseCold<R>[n input segments]
   wn::CopyRec *copy = nullptr;     // [n_seg] emitted segments
   int owns_cold = 1;               // 0: `cold` borrowed from another handle (pairing probes)
+  int32_t n_base = 0;              // input segments (BaseCold records)
   int32_t *face_rec_off = nullptr; // [n_faces+1]
   int32_t *face_cold_off = nullptr;// [n_faces+1]
   int32_t *face_order = nullptr;   // [n_faces] by cost, descending

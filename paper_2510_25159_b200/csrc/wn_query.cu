@@ -90,6 +90,7 @@ struct QParams {
   const int32_t *unsorted;
   HardEntry *hq;          // global hard-pair queue
   int32_t *hq_count;
+  int32_t *hq_next;       // k_hard's dynamic fetch cursor (zeroed with the flags)
   int32_t hq_cap;
   double eps;
   int max_depth;
@@ -177,6 +178,19 @@ struct HardResult {
   bool ob;
 };
 
+// Span of the recursion node [ta, ta + 2^-d], d >= 1 (Eq. 2, with the
+// tightest stored bound covering the node, R29): depth 1..3 nodes are unions
+// of whole dyadic pieces -- tabulated min(2^-d max Bq, sum Lq) (R9); deeper
+// nodes lie inside piece q: Bq[q] 2^-d.  One load, no per-node loop.
+template <typename R>
+__device__ __forceinline__ R node_span(const BaseCold<R> *__restrict__ C, int d, double ta) {
+  if (d <= 3) {
+    const int k = (int)(ta * (double)(1 << d));
+    return (R)__ldg(&C->Sp[(1 << d) - 2 + k]);
+  }
+  return ldexp((R)__ldg(&C->Bq[(int)(ta * 8.0)]), -d);
+}
+
 // Margin M of a face as R (fp32: rounded up, still a valid margin)
 template <typename R>
 __device__ __forceinline__ R margin_r(double M) {
@@ -229,24 +243,7 @@ __device__ __noinline__ HardResult hard_pair(const BaseCold<R> *__restrict__ C, 
       if (dL < eps || dR < eps) { res.ob = true; break; }   // Alg. 1 line 1 on the root
     } else {
       if (dR < eps) { res.ob = true; break; }               // Alg. 1 line 1
-      // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
-      // (piece bounds for d >= 3, their max above), + margin (R5)
-      R Bn, span;
-      if (d > 3) {
-        Bn = (R)__ldg(&C->Bq[(int)(ta * 8.0)]);
-        span = ldexp(Bn, -d) + M;
-      } else {
-        // nodes made of whole dyadic pieces: also the sum of their polygon
-        // lengths (arc-length bounds, R9)
-        const int q0 = (int)(ta * 8.0), nq = 8 >> d;
-        Bn = (R)__ldg(&C->Bq[q0]);
-        R Ls = (R)__ldg(&C->Lq[q0]);
-        for (int k = 1; k < nq; ++k) {
-          Bn = max(Bn, (R)__ldg(&C->Bq[q0 + k]));
-          Ls += (R)__ldg(&C->Lq[q0 + k]);
-        }
-        span = min(ldexp(Bn, -d), Ls) + M;
-      }
+      const R span = node_span(C, d, ta) + M;                // Eq. 2 + margin (R5)
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     if (!split) {                                           // chord substitution
@@ -893,16 +890,18 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
 // ---------------------------------------------------------------------------
 template <typename R, bool COUNT>
 __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
-  // Each lane runs Alg. 1 on its pairs i, i + stride, ... as a state machine
-  // that advances ONE recursion node per loop iteration and starts its next
-  // pair as soon as the current one ends, so a warp waits for its slowest lane
-  // once (at the end) instead of once per pair (the recursion depth is data
-  // dependent).  Same decisions and arithmetic as hard_pair().
+  // Each lane runs Alg. 1 on one pair at a time as a state machine that
+  // advances ONE recursion node per loop iteration; as soon as its pair ends it
+  // takes the next one from the queue (dynamic fetching: one atomic per warp
+  // for all its free lanes), so lanes stay busy until the queue is drained and
+  // a warp waits for its slowest lane only at the very end (the recursion
+  // depth is data dependent).  Same decisions and arithmetic as hard_pair().
   const int total = min(*P.hq_count, P.hq_cap);
-  const int stride = gridDim.x * blockDim.x;
   const R eps = (R)P.eps;
   const int max_depth = P.max_depth;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool drained = false;          // warp-uniform: the queue returned no more pairs
+  int i = 0;
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
   const BaseCold<R> *C = nullptr;
@@ -914,11 +913,21 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   unsigned long long nodes = 0, evals = 0, leaves = 0;
   int dmax = 0;
   while (true) {
+    if (!drained) {
+      const unsigned freem = __ballot_sync(0xffffffffu, !live);
+      if (freem) {
+        int base = 0;
+        const int leader = __ffs(freem) - 1;
+        if (lane == leader) base = atomicAdd(P.hq_next, __popc(freem));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (!live) i = base + __popc(freem & ((1u << lane) - 1u));
+        drained = base + __popc(freem) >= total;
+      }
+    }
+    if (!__any_sync(0xffffffffu, live || i < total)) break;
     if (!live) {
-      if (i >= total) break;
+      if (i >= total) continue;
       const HardEntry H = P.hq[i];
-      if (i + stride < total)   // this lane's next pair, to L2 while this one recurses
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.hq + i + stride));
       angle = H.c >> 31;
       const CopyRec cr = P.copy[H.c & 0x7fffffffu];
       C = P.cold + cr.s;
@@ -953,23 +962,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       split = true;
     } else {
       ob = dR < eps;                                        // Alg. 1 line 1
-      // Eq. 2: B(b-a) with the tightest stored bound covering [a,b]
-      const int q0 = (int)(ta * 8.0);
-      R Bn = (R)__ldg(&C->Bq[q0]);
-      R span;
-      if (d <= 3) {
-        // nodes made of whole dyadic pieces: also the sum of their polygon
-        // lengths (arc-length bounds, R9)
-        const int nq = 8 >> d;
-        R Ls = (R)__ldg(&C->Lq[q0]);
-        for (int k = 1; k < nq; ++k) {
-          Bn = max(Bn, (R)__ldg(&C->Bq[q0 + k]));
-          Ls += (R)__ldg(&C->Lq[q0 + k]);
-        }
-        span = min(ldexp(Bn, -d), Ls) + M;
-      } else {
-        span = ldexp(Bn, -d) + M;
-      }
+      const R span = node_span(C, d, ta) + M;                // Eq. 2 + margin (R5)
       split = !(dL + dR > span);                            // Alg. 1 line 3
     }
     bool done = ob;
@@ -1004,7 +997,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
         if (add != 0.0) atomicAdd(w, add);
       }
       live = false;
-      i += stride;
+      i = total;                 // fetch again
     }
   }
   if (COUNT) {
@@ -1432,6 +1425,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.unsorted = flags;
   P.hq = hq;
   P.hq_count = flags + 2;
+  P.hq_next = flags + 3;
   P.hq_cap = hq_cap;
   P.eps = F->eps;
   P.max_depth = F->max_depth;
@@ -1520,6 +1514,7 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   P.unsorted = flags;            // 0: the query index is the position
   P.hq = (HardEntry *)(base + o_hq);
   P.hq_count = flags + 2;
+  P.hq_next = flags + 3;
   P.hq_cap = hq_cap;
   P.eps = F->eps;
   P.max_depth = F->max_depth;

@@ -271,3 +271,38 @@ def test_nurbs_overclamped_end_knot_rejected():
     assert e.value.status == 2
     with pytest.raises(ValueError):
         oracle.nurbs_decompose(1, P, None, np.array([0.0, 0.0, 0.3, 0.6, 1.0, 1.0, 1.0]))
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_recursion_bounds_sound(precision):
+    """The bounds the shipped recursion uses (BaseCold written by K1 in the
+    build, read back with wn_recursion_bounds) are sound: B >= max |gamma'|,
+    every piece bound Bq[q] >= max |gamma'| on [q/8, (q+1)/8] and every
+    tabulated depth-1..3 node span >= the node's arc length (Lemma 1 P:335-345,
+    Eq. 2, R9, R29), by dense sampling with the oracle's evaluation
+    and derivative (2048 intervals)."""
+    rng = np.random.default_rng(17 + precision)
+    segs = []
+    for _ in range(200):
+        n = int(rng.integers(1, 6))
+        P = rng.uniform(-1, 1, size=(n + 1, 2))
+        w = rng.uniform(0.5, 2.0, size=n + 1) if rng.random() < 0.8 else np.exp(rng.uniform(-3, 3, n + 1))
+        segs.append((P, w))
+    # one open loop of unrelated segments (a valid, if odd, face: gaps are chain breaks)
+    wl = H.make_wl([([segs], 0, (0, 1, 0, 1))])
+    faces = wn.Faces.from_workload(wl, precision=precision)
+    rb = faces.recursion_bounds(len(segs)).cpu().numpy()
+    faces.close()
+    ts = np.linspace(0, 1, 2049)
+    for (P, w), row in zip(segs, rb):
+        sp = np.array([np.hypot(*oracle.derivative(P, w, t)) for t in ts])
+        pts = np.array([oracle.evaluate(P, w, t) for t in ts])
+        arc = np.hypot(*np.diff(pts, axis=0).T)
+        assert row[0] >= sp.max() * (1 - 1e-12)
+        for q in range(8):
+            m = (ts >= q / 8) & (ts <= (q + 1) / 8)
+            assert row[1 + q] >= sp[m].max() * (1 - 1e-12), (q, row[1 + q], sp[m].max())
+        for d in (1, 2, 3):
+            L = 2048 >> d
+            for k in range(1 << d):
+                assert row[9 + (1 << d) - 2 + k] >= arc[k * L:(k + 1) * L].sum() * (1 - 1e-9), (d, k)

@@ -139,21 +139,39 @@ def _perp(v):
 def _star_segments(rng, V, degs, jit_frac, rational):
     """Segments V_k -> V_{k+1} (cyclic) with degree degs[k]; interior control points
     on the edge plus a perpendicular jitter U(-jit_frac, jit_frac) * perp(edge).
-    Junctions reuse the same V entries, so shared endpoints are bit-identical."""
+    Junctions reuse the same V entries, so shared endpoints are bit-identical.
+    Vectorised per degree; the random stream is consumed exactly as the
+    per-segment form (jitter of segment k, then its weights, k = 0, 1, ...):
+    uniform(low, high) = low + (high - low) * next_double."""
     n = V.shape[0]
-    out = []
-    for k in range(n):
-        A = V[k]
-        B = V[(k + 1) % n]
-        d = int(degs[k])
-        j = np.arange(d + 1)[:, None] / d
-        P = A + j * (B - A)
+    degs = np.asarray(degs, dtype=np.int64)
+    cj = np.where(degs >= 2, degs - 1, 0)
+    cw = degs + 1 if rational else np.zeros_like(degs)
+    off = np.concatenate([[0], np.cumsum(cj + cw)])
+    U = rng.random(int(off[-1]))
+    A = V
+    B = V[(np.arange(n) + 1) % n]
+    E = B - A
+    prp = _perp(E)
+    out = [None] * n
+    jlo, jsc = -jit_frac, jit_frac - (-jit_frac)
+    wlo, wsc = 0.5, 2.0 - 0.5
+    for d in np.unique(degs):
+        d = int(d)
+        ks = np.nonzero(degs == d)[0]
+        jj = (np.arange(d + 1) / d)[None, :, None]
+        P = A[ks, None, :] + jj * E[ks, None, :]
         if d >= 2:
-            P[1:d] += rng.uniform(-jit_frac, jit_frac, size=(d - 1, 1)) * _perp(B - A)
-        P[0] = A
-        P[d] = B
-        w = rng.uniform(0.5, 2.0, size=d + 1) if rational else np.ones(d + 1)
-        out.append((P, w))
+            u = U[off[ks][:, None] + np.arange(d - 1)[None, :]]              # [m, d-1]
+            P[:, 1:d] += (jlo + jsc * u)[:, :, None] * prp[ks, None, :]
+        P[:, 0] = A[ks]
+        P[:, d] = B[ks]
+        if rational:
+            W = wlo + wsc * U[off[ks][:, None] + cj[ks][:, None] + np.arange(d + 1)[None, :]]
+        else:
+            W = np.ones((len(ks), d + 1))
+        for i, k in enumerate(ks):
+            out[k] = (P[i], W[i])
     return out
 
 

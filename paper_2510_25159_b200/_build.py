@@ -22,20 +22,24 @@ def _stale():
     return False
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile libwn.so (or, for A/B experiments, a variant `out` with extra
+    -D `defines`)."""
+    target = out or LIB
+    if not force and not out and not _stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + FLAGS + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    tmp = target + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
     if verbose:
         print(r.stderr)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if not out:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(r.stderr)
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

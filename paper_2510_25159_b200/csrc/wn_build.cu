@@ -241,9 +241,8 @@ struct PrepSink {
     o2[5 + q / 2] = make_double2(l0, l1);
   }
   template <int N>
-  __device__ void root(int s, double B, double S0, const double *, const double *, const double *, int) const {
-    reinterpret_cast<double2 *>(out + s)[0] = make_double2(B, S0);
-  }
+  __device__ void head(int, double, const double *, const double *, const double *) const {}
+  __device__ void tail(int s, double B, double S0) const { reinterpret_cast<double2 *>(out + s)[0] = make_double2(B, S0); }
 };
 
 __device__ __forceinline__ float f_dn(double x) { return __double2float_rd(x); }
@@ -278,44 +277,34 @@ struct ColdSink {
     for (int k = 0; k < (int)(sizeof(BaseCold<R>) / 16); ++k) o[k] = make_uint4(0, 0, 0, 0);
     s0[s] = 0.0;
   }
-  // piece bounds go to Bq; the piece arc-length bounds are parked in Sp[0..7]
-  // until root() folds them into the per-node spans
-  __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) const {
+  // Piece bounds go to Bq.  The spans of the depth-1..3 nodes are built as the
+  // pieces arrive (q = 0, 2, 4, 6 with their right neighbours): depth 3 = the
+  // piece itself, depth 2 = the pair, depth 1 = two pairs (running max / sum in
+  // scalars); min(2^-d max Bq, sum Lq) from the margined doubles, rounded up.
+  double acc_b = 0.0, acc_l = 0.0;
+  __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) {
     BaseCold<R> *C = out + s;
-    *reinterpret_cast<float2 *>(&C->Bq[q]) = make_float2(f_up(fmin(B, b0) * (1.0 + rel)), f_up(fmin(B, b1) * (1.0 + rel)));
-    *reinterpret_cast<float2 *>(&C->Sp[q]) = make_float2(f_up(l0 * (1.0 + rel)), f_up(l1 * (1.0 + rel)));
-  }
-  // spans of the depth-1..3 nodes from the rounded-up piece values (sums and
-  // maxima of a few floats are exact in double; the result rounded up)
-  __device__ void spans(BaseCold<R> *C) const {
-    float bq[8], lq[8];
-#pragma unroll
-    for (int q = 0; q < 8; q += 2) {
-      const float2 b = *reinterpret_cast<const float2 *>(&C->Bq[q]);
-      const float2 l = *reinterpret_cast<const float2 *>(&C->Sp[q]);
-      bq[q] = b.x; bq[q + 1] = b.y; lq[q] = l.x; lq[q + 1] = l.y;
+    const double m0 = fmin(B, b0) * (1.0 + rel), m1 = fmin(B, b1) * (1.0 + rel);
+    const double L0 = l0 * (1.0 + rel), L1 = l1 * (1.0 + rel);
+    *reinterpret_cast<float2 *>(&C->Bq[q]) = make_float2(f_up(m0), f_up(m1));
+    // depth 3 (index 6 + q), depth 2 (index 2 + q/2)
+    *reinterpret_cast<float2 *>(&C->Sp[6 + q]) = make_float2(f_up(fmin(ldexp(m0, -3), L0)), f_up(fmin(ldexp(m1, -3), L1)));
+    const double pb = fmax(m0, m1), pl = L0 + L1;
+    C->Sp[2 + q / 2] = f_up(fmin(ldexp(pb, -2), pl));
+    if ((q & 2) == 0) {
+      acc_b = pb;
+      acc_l = pl;
+    } else {                                               // depth 1 (index q / 4)
+      C->Sp[q / 4] = f_up(fmin(ldexp(fmax(acc_b, pb), -1), acc_l + pl));
     }
-    float sp[14];
-#pragma unroll
-    for (int d = 1; d <= 3; ++d)
-#pragma unroll
-      for (int k = 0; k < (1 << d); ++k) {
-        const int nq = 8 >> d;
-        double bm = 0.0, ls = 0.0;
-#pragma unroll
-        for (int q = k * nq; q < (k + 1) * nq; ++q) { bm = fmax(bm, (double)bq[q]); ls += (double)lq[q]; }
-        sp[(1 << d) - 2 + k] = f_up(fmin(ldexp(bm, -d), ls));
-      }
-#pragma unroll
-    for (int i = 0; i < 14; i += 2) *reinterpret_cast<float2 *>(&C->Sp[i]) = make_float2(sp[i], sp[i + 1]);
   }
   // end points (exact, stored coordinates), bound, degree, homogeneous Horner
   // coefficients c_j = (C(n,j) w_j) (x_j, y_j, 1), zero above the degree
+  __device__ void tail(int s, double, double S0) const { s0[s] = S0; }
+  // written before the piece loop so that the control points die early
   template <int N>
-  __device__ void root(int s, double B, double S0, const double *px, const double *py, const double *W, int) const {
+  __device__ void head(int s, double B, const double *px, const double *py, const double *W) const {
     BaseCold<R> *C = out + s;
-    s0[s] = S0;
-    spans(C);
     *reinterpret_cast<double2 *>(&C->x0) = make_double2(px[0], py[0]);
     *reinterpret_cast<double2 *>(&C->xn) = make_double2(px[N], py[N]);
     const double Bm = B * (1.0 + rel);
@@ -364,7 +353,7 @@ struct ColdSink {
 // piece bounds and piece polygon lengths, written through the sink.
 template <int N, class Sink>
 __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const double *__restrict__ w, int o, int s,
-                                       const Sink &sink, uint8_t *__restrict__ err_out) {
+                                       Sink &sink, uint8_t *__restrict__ err_out) {
   double X[N + 1], Y[N + 1], W[N + 1], px[N + 1], py[N + 1];
   bool err = false;
   double lpoly = 0.0;
@@ -382,6 +371,7 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     return;
   }
   const double B = fmin(floater_bound<N>(px, py, W), hodo_bound<N>(X, Y, W));
+  sink.template head<N>(s, B, px, py, W);
   double l8 = 0.0;   // sum of the 8 dyadic pieces' polygon lengths >= arc length (R9, tighter)
 #pragma unroll 1
   for (int q = 0; q < 8; q += 2) {
@@ -395,7 +385,7 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
     l8 += l0 + l1;
     sink.pieces(s, q, B, b0, b1, l0, l1);
   }
-  sink.template root<N>(s, B, fmin(B, fmin(lpoly, l8)), px, py, W, 0);
+  sink.tail(s, B, fmin(B, fmin(lpoly, l8)));
 }
 
 #ifndef PREP_SPLIT

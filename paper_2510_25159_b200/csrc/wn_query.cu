@@ -383,12 +383,23 @@ constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classif
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
+constexpr int HCHUNK = 64;   // hard pairs a k_hard warp reserves per atomic
+#ifndef WN_P1_NOVOTE
+#define WN_P1_NOVOTE 1          // no warp vote in front of per-lane slow paths (plain branches)
+#endif
+#ifndef WN_P1_PINF
+#define WN_P1_PINF 1            // the query's fp32 coordinates pinned in registers
+#endif
+#ifndef WN_HARD_DYN
+#define WN_HARD_DYN 1           // 1: dynamic fetching of hard pairs per warp; 0: static grid stride
+#endif
 constexpr int SP_BINS = 1024;   // Morton cells of the spatial regrouping (32 x 32)
 constexpr int SP_COHERENT = 24; // mean warp-footprint perimeter (cells) above which a unit is regrouped
 
 #ifndef WN_P1_MINB
 #define WN_P1_MINB 4
 #endif
+
 // ANGLE: the build's angle_mode (every record of a handle carries the same F_ANGLE);
 // GRID: implicit-grid batch (wn_query_grid) instead of explicit uv
 template <typename R, bool COUNT, bool ANGLE, bool GRID>
@@ -678,7 +689,12 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         py = v;
       }
     }
-    const float pxf = (float)px, pyf = (float)py;
+    float pxf = (float)px, pyf = (float)py;
+#if WN_P1_PINF
+    // opaque: kept in registers instead of re-derived from (px, py) with an
+    // F2F.F32.F64 conversion in every record iteration
+    asm volatile("" : "+f"(pxf), "+f"(pyf));
+#endif
 
     double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
     // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
@@ -745,12 +761,19 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             if (COUNT && descend) ++c_desc;
             if (!__any_sync(0xffffffffu, descend)) {
               // every active lane substitutes the run's chord (homotopy)
+#if WN_P1_NOVOTE
+              if (act && (u1 != up || ANGLE)) {       // (a plain branch: uniform when no lane crosses)
+                if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
+                else xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+              }
+#else
               if (__any_sync(0xffffffffu, act && (u1 != up || ANGLE))) {
                 if (act) {
                   if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
                   else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
                 }
               }
+#endif
               if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
               sp += (int)(meta >> 8) * RB;
               if (COUNT && lane == 0) ++c_cull;
@@ -764,8 +787,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           } else {
             const bool need = act && (!pr || u1 != up || ANGLE);
             bool hard = false;
+#if WN_P1_NOVOTE
+            {
+              if (need) {            // (a plain branch; the ballot below is the one vote)
+#else
             if (__any_sync(0xffffffffu, need)) {
               if (need) {
+#endif
                 if (!(df > eps_c)) {                             // filter cannot certify d >= eps
                   if constexpr (F64) {
                     const double dx = h.x - px, dy = h.y - py;
@@ -901,7 +929,8 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   const int max_depth = P.max_depth;
   const int lane = threadIdx.x & 31;
   bool drained = false;          // warp-uniform: the queue returned no more pairs
-  int i = 0;
+  int wb = 0, we = 0;            // warp-uniform: pairs [wb, we) reserved by this warp, not yet handed out
+  int i = WN_HARD_DYN ? total : (int)(blockIdx.x * blockDim.x + threadIdx.x);   // this lane's next pair (total: none)
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
   const BaseCold<R> *C = nullptr;
@@ -913,15 +942,24 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   unsigned long long nodes = 0, evals = 0, leaves = 0;
   int dmax = 0;
   while (true) {
-    if (!drained) {
-      const unsigned freem = __ballot_sync(0xffffffffu, !live);
-      if (freem) {
-        int base = 0;
-        const int leader = __ffs(freem) - 1;
-        if (lane == leader) base = atomicAdd(P.hq_next, __popc(freem));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (!live) i = base + __popc(freem & ((1u << lane) - 1u));
-        drained = base + __popc(freem) >= total;
+    if (WN_HARD_DYN && !drained) {
+      // hand the warp's reserved pairs to its free lanes; reserve HCHUNK more
+      // (one atomic per warp per HCHUNK pairs) when they run out
+      unsigned freem = __ballot_sync(0xffffffffu, !live && i >= total);
+      while (freem) {
+        if (wb >= we) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(P.hq_next, HCHUNK);
+          base = __shfl_sync(0xffffffffu, base, 0);
+          wb = base;
+          we = min(base + HCHUNK, total);
+          if (wb >= we) { drained = true; break; }
+        }
+        const int avail = we - wb;
+        const int rank = __popc(freem & ((1u << lane) - 1u));
+        if (((freem >> lane) & 1u) && rank < avail) i = wb + rank;
+        wb += min(__popc(freem), avail);
+        freem = __ballot_sync(0xffffffffu, !live && i >= total);
       }
     }
     if (!__any_sync(0xffffffffu, live || i < total)) break;
@@ -997,7 +1035,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
         if (add != 0.0) atomicAdd(w, add);
       }
       live = false;
-      i = total;                 // fetch again
+      i = WN_HARD_DYN ? total : i + (int)(gridDim.x * blockDim.x);   // fetch again / static grid stride
     }
   }
   if (COUNT) {

@@ -391,6 +391,9 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
 #ifndef PREP_SPLIT
 #define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels
 #endif
+#ifndef PREP_ONE
+#define PREP_ONE 1     // 1: one K1 kernel over all degrees (k_prep_all); 0: one kernel per degree
+#endif
 // Per-degree K1: the degree-sorted segments split into the ranges of the sort
 // key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with
 // its own register budget (degree 1-3 need far fewer than degree 5).  bnd[k] =
@@ -404,7 +407,7 @@ __global__ void k_deg_bounds(int32_t n, const int32_t *__restrict__ sdeg, int32_
 }
 
 #ifndef PREP_DEG_MINB
-#define PREP_DEG_MINB 1
+#define PREP_DEG_MINB 4   // 128 registers: degree 5 spills 72 B but runs at 4 CTAs / SM (measured faster than 1-3)
 #endif
 template <int N, class Sink>
 __global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *__restrict__ bnd, const int32_t *__restrict__ deg,
@@ -419,6 +422,29 @@ __global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *
     } else {   // a degree outside 1..5 with these low bits (rejected on the host)
       serr[s] = 1;
       sink.zero(s);
+    }
+  }
+}
+
+// One K1 kernel for all degrees: a grid-stride loop over the degree-sorted
+// order from the top (degree 5 first, the longest), one degree per warp except
+// at the range boundaries; no per-degree launches and no tail between them.
+template <class Sink>
+__global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_all(int32_t n, const int32_t *__restrict__ deg,
+                                                  const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
+                                                  const double *__restrict__ w, Sink sink,
+                                                  uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int s = order[n - 1 - i];
+    switch (deg[s]) {
+      case 5: prep_n<5>(ctrl, w, coff[s], s, sink, serr); break;
+      case 4: prep_n<4>(ctrl, w, coff[s], s, sink, serr); break;
+      case 3: prep_n<3>(ctrl, w, coff[s], s, sink, serr); break;
+      case 2: prep_n<2>(ctrl, w, coff[s], s, sink, serr); break;
+      case 1: prep_n<1>(ctrl, w, coff[s], s, sink, serr); break;
+      default:   // rejected on the host (k_deg flag)
+        serr[s] = 1;
+        sink.zero(s);
     }
   }
 }
@@ -1528,6 +1554,12 @@ cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, c
   if ((e = D.alloc(&dt, tmp)) != cudaSuccess) return e;
   cub::DeviceRadixSort::SortPairs(dt, tmp, deg, d_degs, d_iota, d_order, n_segs, 0, 3, st);
   g_build_launches += 4;
+#if PREP_ONE
+  k_prep_all<<<std::min((n_segs + 127) / 128, 148 * PREP_DEG_MINB), 128, 0, st>>>(n_segs, deg, coff, ctrl, w, sink, serr,
+                                                                                   d_order);
+  ++g_build_launches;
+  return cudaGetLastError();
+#endif
   int32_t *d_bnd = nullptr;
   if ((e = D.alloc(&d_bnd, 9)) != cudaSuccess) return e;
   k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);

@@ -191,6 +191,22 @@ __device__ __forceinline__ R node_span(const BaseCold<R> *__restrict__ C, int d,
   return ldexp((R)__ldg(&C->Bq[(int)(ta * 8.0)]), -d);
 }
 
+// Alg. 1 line 3 without square roots: with r0 = d0^2, r1 = d1^2 and
+// k = S^2 - r0 - r1,  d0 + d1 > S  <=>  k < 0 or 4 r0 r1 > k^2  (S > 0).  The
+// rounding of either form is far inside the R5 margin folded into S.
+#ifndef WN_HARD_SQRTFREE
+#define WN_HARD_SQRTFREE 1
+#endif
+template <typename R>
+__device__ __forceinline__ bool outside_ellipse(R r0, R r1, R S) {
+#if WN_HARD_SQRTFREE
+  const R k = S * S - r0 - r1;
+  return k < R(0) || R(4) * r0 * r1 > k * k;
+#else
+  return dsqrt(r0) + dsqrt(r1) > S;
+#endif
+}
+
 // Margin M of a face as R (fp32: rounded up, still a valid margin)
 template <typename R>
 __device__ __forceinline__ R margin_r(double M) {
@@ -221,7 +237,8 @@ __device__ __noinline__ HardResult hard_pair(const BaseCold<R> *__restrict__ C, 
   R stx[MAXD + 1], sty[MAXD + 1];
   int8_t std_[MAXD + 1];
   R Lx = (R)Fr.X(__ldg(&C->x0)) - qx, Ly = (R)Fr.Y(__ldg(&C->y0)) - qy;
-  R dL = dsqrt(Lx * Lx + Ly * Ly);
+  R rL = Lx * Lx + Ly * Ly;          // squared distances (no square roots, outside_ellipse)
+  const R eps2 = eps * eps;
   stx[0] = (R)Fr.X(__ldg(&C->xn)) - qx;
   sty[0] = (R)Fr.Y(__ldg(&C->yn)) - qy;
   std_[0] = 0;
@@ -234,23 +251,23 @@ __device__ __noinline__ HardResult hard_pair(const BaseCold<R> *__restrict__ C, 
   while (sp > 0) {
     const R rx = stx[sp - 1], ry = sty[sp - 1];
     const int d = std_[sp - 1];
-    const R dR = dsqrt(rx * rx + ry * ry);
+    const R rR = rx * rx + ry * ry;
     bool split;
     ++nodes;
     if (root) {
       split = true;
       root = false;
-      if (dL < eps || dR < eps) { res.ob = true; break; }   // Alg. 1 line 1 on the root
+      if (rL < eps2 || rR < eps2) { res.ob = true; break; } // Alg. 1 line 1 on the root
     } else {
-      if (dR < eps) { res.ob = true; break; }               // Alg. 1 line 1
+      if (rR < eps2) { res.ob = true; break; }              // Alg. 1 line 1
       const R span = node_span(C, d, ta) + M;                // Eq. 2 + margin (R5)
-      split = !(dL + dR > span);                            // Alg. 1 line 3
+      split = !outside_ellipse(rL, rR, span);               // Alg. 1 line 3
     }
     if (!split) {                                           // chord substitution
       if (angle) res.fsum += (double)chord_angle(Lx, Ly, rx, ry);
       else res.xsum += xcount(Lx, Ly, rx, ry);
       ++leaves;
-      Lx = rx; Ly = ry; dL = dR;
+      Lx = rx; Ly = ry; rL = rR;
       ta += ldexp(1.0, -d);
       --sp;
     } else {
@@ -383,7 +400,7 @@ constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classif
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
-constexpr int HCHUNK = 64;   // hard pairs a k_hard warp reserves per atomic
+constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (one per lane: small queues stay spread)
 #ifndef WN_P1_NOVOTE
 #define WN_P1_NOVOTE 1          // no warp vote in front of per-lane slow paths (plain branches)
 #endif
@@ -935,7 +952,8 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   int8_t std_[MAXD + 1];
   const BaseCold<R> *C = nullptr;
   CopyFrame Fr{0.0, 0.0, 0.0, 0.0};
-  R qx = 0, qy = 0, M = 0, Lx = 0, Ly = 0, dL = 0;
+  R qx = 0, qy = 0, M = 0, Lx = 0, Ly = 0, rL = 0;     // rL: squared distance to the left end
+  const R eps2 = eps * eps;
   int n = 0, sp = 0, xsum = 0, q = 0;
   double ta = 0.0, fsum = 0.0;
   bool live = false, root = false, angle = false;
@@ -977,7 +995,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       n = __ldg(&C->n);
       Lx = (R)Fr.X(__ldg(&C->x0)) - qx;
       Ly = (R)Fr.Y(__ldg(&C->y0)) - qy;
-      dL = dsqrt(Lx * Lx + Ly * Ly);
+      rL = Lx * Lx + Ly * Ly;
       stx[0] = (R)Fr.X(__ldg(&C->xn)) - qx;
       sty[0] = (R)Fr.Y(__ldg(&C->yn)) - qy;
       std_[0] = 0;
@@ -991,17 +1009,17 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
     // one node [ta, ta + 2^-d] with right end point (rx, ry), top of the stack
     const R rx = stx[sp - 1], ry = sty[sp - 1];
     const int d = std_[sp - 1];
-    const R dR = dsqrt(rx * rx + ry * ry);
+    const R rR = rx * rx + ry * ry;
     bool split, ob;
     ++nodes;
     if (root) {
       root = false;
-      ob = dL < eps || dR < eps;                            // Alg. 1 line 1 on the root
+      ob = rL < eps2 || rR < eps2;                          // Alg. 1 line 1 on the root
       split = true;
     } else {
-      ob = dR < eps;                                        // Alg. 1 line 1
+      ob = rR < eps2;                                       // Alg. 1 line 1
       const R span = node_span(C, d, ta) + M;                // Eq. 2 + margin (R5)
-      split = !(dL + dR > span);                            // Alg. 1 line 3
+      split = !outside_ellipse(rL, rR, span);               // Alg. 1 line 3
     }
     bool done = ob;
     if (!ob && split && d >= max_depth) { ob = true; done = true; }   // depth cap (R6)
@@ -1010,7 +1028,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
         if (angle) fsum += (double)chord_angle(Lx, Ly, rx, ry);
         else xsum += xcount(Lx, Ly, rx, ry);
         ++leaves;
-        Lx = rx; Ly = ry; dL = dR;
+        Lx = rx; Ly = ry; rL = rR;
         ta += ldexp(1.0, -d);
         done = --sp == 0;
       } else {

@@ -392,7 +392,7 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
 #define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels
 #endif
 #ifndef PREP_ONE
-#define PREP_ONE 1     // 1: one K1 kernel over all degrees (k_prep_all); 0: one kernel per degree
+#define PREP_ONE 0     // 1: one K1 kernel over all degrees (k_prep_all, measured slower); 0: one kernel per degree
 #endif
 // Per-degree K1: the degree-sorted segments split into the ranges of the sort
 // key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with

@@ -23,9 +23,12 @@ namespace wn {
 
 static thread_local char g_err[512] = "";
 
-// WN_TRACE=1: host-side phase timings of wn_build_faces on stderr
+// WN_TRACE=1: host-side phase timings of wn_build_faces on stderr, with stream
+// synchronisations after the kernel groups (device phase times); WN_TRACE=2:
+// host timestamps only (no added synchronisation)
 struct Trace {
   bool on = std::getenv("WN_TRACE") != nullptr;
+  bool sync = on && std::atoi(std::getenv("WN_TRACE")) == 1;
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
   void mark(const char *what) {
     if (!on) return;
@@ -1275,7 +1278,38 @@ struct BuildSummary {
   int tot_g, tot_r, tot_c, pad;
   unsigned long long lines, cull;
   unsigned long long copies, bands;   // extended-copy groups; Eq. 8 bands (line pairs of bi-periodic faces)
+  int csr_bad;                        // loop / face CSR offsets not a valid CSR (k_csr_check)
+  unsigned dom_bad;                   // min over faces of (face << 1 | axis) with a bad period, else ~0
 };
+
+// Input validation on the device (the host reads only the summary): CSR
+// offsets start at 0, end at the element count and never decrease; periodic
+// axes have a finite start and a finite period > 0.
+__global__ void k_csr_check(int32_t n_loops, int32_t n_faces, int32_t n_segs, const int32_t *__restrict__ lso,
+                            const int32_t *__restrict__ flo, const uint8_t *__restrict__ per,
+                            const double *__restrict__ dom, BuildSummary *__restrict__ sum) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i <= n_loops) {
+    const int a = lso[i];
+    if (i == 0 && a != 0) bad = true;
+    if (i == n_loops && a != n_segs) bad = true;
+    if (i < n_loops && a > lso[i + 1]) bad = true;
+  }
+  if (i <= n_faces) {
+    const int a = flo[i];
+    if (i == 0 && a != 0) bad = true;
+    if (i == n_faces && a != n_loops) bad = true;
+    if (i < n_faces && a > flo[i + 1]) bad = true;
+  }
+  if (bad) atomicOr(&sum->csr_bad, 1);
+  if (i < n_faces) {
+    const uint8_t pf = per[i];
+    const double *d = dom + 4 * i;
+    if ((pf & 1) && !(isfinite(d[0]) && isfinite(d[1]) && d[1] > 0)) atomicMin(&sum->dom_bad, ((unsigned)i << 1) | 0u);
+    if ((pf & 2) && !(isfinite(d[2]) && isfinite(d[3]) && d[3] > 0)) atomicMin(&sum->dom_bad, ((unsigned)i << 1) | 1u);
+  }
+}
 
 struct CountSink {
   int ng = 0, recs = 0, colds = 0, lines = 0, cull = 0, copies = 0;
@@ -1714,18 +1748,12 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
 
   // --- host copies of the small CSR / face arrays ---
   // (pinned staging: the copies stay asynchronous; read after the plan summary event)
-  int32_t *h_lso = (int32_t *)g_pin.get(sizeof(int32_t) * (n_loops + 1));
+  // (validated on the device, k_csr_check; the pairing path copies what it needs)
   int32_t *h_flo = (int32_t *)g_pin.get(sizeof(int32_t) * (n_faces + 1));
   uint8_t *h_per = (uint8_t *)g_pin.get(std::max(n_faces, 1));
   double *h_dom = (double *)g_pin.get(sizeof(double) * 4 * std::max(n_faces, 1));
   int32_t *h_bad = (int32_t *)g_pin.get(sizeof(int32_t));
-  if (!h_lso || !h_flo || !h_per || !h_dom || !h_bad) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
-  WN_CUDA(cudaMemcpyAsync(h_lso, loop_seg_off, sizeof(int32_t) * (n_loops + 1), cudaMemcpyDeviceToHost, st));
-  WN_CUDA(cudaMemcpyAsync(h_flo, face_loop_off, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st));
-  if (n_faces) {
-    WN_CUDA(cudaMemcpyAsync(h_per, face_periodic, n_faces, cudaMemcpyDeviceToHost, st));
-    WN_CUDA(cudaMemcpyAsync(h_dom, face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st));
-  }
+  if (!h_flo || !h_per || !h_dom || !h_bad) { set_error("pinned host allocation failed"); return WN_ERR_NOMEM; }
   // --- library copies of the caller's CSR / degree arrays (the caller may free
   // or overwrite every input as soon as this call returns, include/wn.h) ---
   BuildCtx B{};
@@ -1784,7 +1812,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
                                                                        B.shift, B.brk, B.chain, B.lsta, B.lend, B.info);
   g_build_launches += (n_faces ? 1 : 0) + (n_loops ? 1 : 0);
   WN_CUDA(cudaGetLastError());
-  if (tr.on) { cudaStreamSynchronize(st2); tr.mark("(trace) k_loop_face + k_lift"); }
+  if (tr.sync) { cudaStreamSynchronize(st2); tr.mark("(trace) k_loop_face + k_lift"); }
   DevBuf D2;
   D2.st = st2;
   wn_faces_t F = new wn_faces_s();
@@ -1832,6 +1860,12 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   auto plan_pass = [&](const int *pair_beta, const int *pair_s) -> wn_status_t {
     WN_CUDA(cudaMemsetAsync(d_sum, 0, sizeof(BuildSummary), st2));
     WN_CUDA(cudaMemsetAsync(&d_sum->first_bad, 0xFF, sizeof(unsigned long long), st2));
+    WN_CUDA(cudaMemsetAsync(&d_sum->dom_bad, 0xFF, sizeof(unsigned), st2));
+    if (!pair_beta) {
+      k_csr_check<<<(std::max(n_loops, n_faces) + 1 + 255) / 256, 256, 0, st2>>>(n_loops, n_faces, n_segs, B.lso, B.flo,
+                                                                                face_periodic, face_domain, d_sum);
+      ++g_build_launches;
+    }
     if (n_faces) {
       k_plan_count<<<(n_faces + 127) / 128, 128, 0, st2>>>(
           n_faces, n_loops, B.flo, face_periodic, face_domain, B.info, angle ? 1 : 0, O.strict ? 1 : 0,
@@ -1871,7 +1905,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   }
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaEventRecord(g_ev_k1[dev], st));
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep + k_s0pre"); }
+  if (tr.sync) { cudaStreamSynchronize(st); tr.mark("(trace) k_prep + k_s0pre"); }
   WN_CUDA(cudaEventSynchronize(g_ev_plan[dev]));
   tr.mark("device plan summary");
   // CSR / domain checks on the host (the kernels above clamp every CSR index,
@@ -1882,21 +1916,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     cudaEventSynchronize(g_ev_k1[dev]);
     return rc;
   };
-  bool csr_ok = h_lso[0] == 0 && h_lso[n_loops] == n_segs && h_flo[0] == 0 && h_flo[n_faces] == n_loops;
-  for (int l = 0; csr_ok && l < n_loops; ++l) csr_ok = h_lso[l] <= h_lso[l + 1];
-  for (int f = 0; csr_ok && f < n_faces; ++f) csr_ok = h_flo[f] <= h_flo[f + 1];
-  if (!csr_ok) { set_error("wn_build_faces: bad loop/face CSR offsets"); return fail(WN_ERR_ARG); }
+  if (h_sum->csr_bad) { set_error("wn_build_faces: bad loop/face CSR offsets"); return fail(WN_ERR_ARG); }
   if (*h_bad) { set_error("wn_build_faces: segment degree outside 1..5"); return fail(WN_ERR_ARG); }
-  for (int f = 0; f < n_faces; ++f) {
-    const double *d = &h_dom[4 * f];
-    if ((h_per[f] & 1) && !(std::isfinite(d[0]) && std::isfinite(d[1]) && d[1] > 0)) {
-      set_error("face %d: bad u period", f);
-      return fail(WN_ERR_GEOM);
-    }
-    if ((h_per[f] & 2) && !(std::isfinite(d[2]) && std::isfinite(d[3]) && d[3] > 0)) {
-      set_error("face %d: bad v period", f);
-      return fail(WN_ERR_GEOM);
-    }
+  if (h_sum->dom_bad != 0xFFFFFFFFu) {
+    set_error("face %u: bad %s period", h_sum->dom_bad >> 1, (h_sum->dom_bad & 1) ? "v" : "u");
+    return fail(WN_ERR_GEOM);
   }
   auto report_bad = [&]() {
     const int first = (int)(h_sum->first_bad >> 32), code = (int)(h_sum->first_bad & 0xffffffffu);
@@ -1909,6 +1933,11 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   const int *d_pair_beta = nullptr, *d_pair_s = nullptr;
   if (h_sum->needp) {
     // --- pairing (Algs. 7-9) for bi-periodic faces via probe queries (host) ---
+    WN_CUDA(cudaMemcpyAsync(h_flo, B.flo, sizeof(int32_t) * (n_faces + 1), cudaMemcpyDeviceToHost, st2));
+    if (n_faces) {
+      WN_CUDA(cudaMemcpyAsync(h_per, face_periodic, n_faces, cudaMemcpyDeviceToHost, st2));
+      WN_CUDA(cudaMemcpyAsync(h_dom, face_domain, sizeof(double) * 4 * n_faces, cudaMemcpyDeviceToHost, st2));
+    }
     LoopInfo *L = (LoopInfo *)g_pin.get(sizeof(LoopInfo) * std::max(n_loops, 1));
     if (!L) { set_error("pinned host allocation failed"); return fail(WN_ERR_NOMEM); }
     if (n_loops) WN_CUDA(cudaMemcpyAsync(L, B.info, sizeof(LoopInfo) * n_loops, cudaMemcpyDeviceToHost, st2));
@@ -2179,6 +2208,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   // lifted copies): once it is done the inputs may be freed (include/wn.h).
   // The emission is already queued behind it, so this wait leaves no gap.
   WN_CUDA(cudaEventSynchronize(g_ev_k1[dev]));
+  tr.mark("K1 done (inputs released)");
   // no final synchronisation: the handle's records are complete in stream
   // order, so queries enqueued on `stream` after this call see them
   {
@@ -2188,7 +2218,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
     if (e == cudaSuccess) e = cudaEventRecord(F->ready, st);
     if (e != cudaSuccess) return cuda_fail(e, "build event");
   }
-  if (tr.on) { cudaStreamSynchronize(st); tr.mark("(trace) k_plan_fill + k_emit"); }
+  if (tr.sync) { cudaStreamSynchronize(st); tr.mark("(trace) k_plan_fill + k_emit"); }
   *out = F_guard.release();
   return WN_OK;
 }

@@ -90,9 +90,6 @@ struct QParams {
   const int32_t *unsorted;
   HardEntry *hq;          // global hard-pair queue
   int32_t *hq_count;
-  int32_t counted;        // 1: flag array 4-B aligned -> counted pending flags (k_hard classifies)
-  int32_t maxcnt;         // largest counted n (FLAG_MAXCNT; lowered by WN_MAXCNT in tests)
-  int32_t *uncounted;     // set when a query had to use FLAG_PENDING (k_finish then scans)
   int32_t *hq_next;       // k_hard's dynamic fetch cursor (zeroed with the flags)
   int32_t hq_cap;
   double eps;
@@ -399,14 +396,8 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
 }
 
 // intermediate flag values between phase 1 and k_finish / k_overflow
-constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued, not counted: k_finish classifies
+constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classifies
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
-// counted pending: 0x80 | n, n = 1..FLAG_MAXCNT hard pairs still to add; the
-// k_hard lane that completes the query's last pair classifies it (no k_finish scan)
-constexpr int FLAG_MAXCNT = 0x7C;
-#ifndef WN_COUNTED
-#define WN_COUNTED 1
-#endif
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (one per lane: small queues stay spread)
@@ -731,7 +722,6 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
     int xs = 0, halves = 0;
     pend = 0;
-    int nh = 0;                    // hard pairs queued for this lane's query
     double fr = 0.0;
     int gr = 0;                    // warp-uniform record cursor
 
@@ -848,7 +838,6 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                   H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | (ANGLE ? 0x80000000u : 0u);
                   s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
                   pend |= 1 | 4;
-                  ++nh;
                   if (COUNT) ++c_hard;
                 }
                 hn_ += cnt;
@@ -924,12 +913,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       } else {
         const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
         P.winding[qi] = w;
-        uint8_t fl;
-        if (pend & 2) fl = FLAG_OVERFLOW;
-        else if (!(pend & 1)) fl = classify(w, P.rule);
-        else if (P.counted && nh <= P.maxcnt) fl = (uint8_t)(0x80 | nh);
-        else { fl = FLAG_PENDING; *P.uncounted = 1; }
-        P.flag[qi] = fl;
+        P.flag[qi] = (pend & 2) ? FLAG_OVERFLOW : (pend & 1) ? FLAG_PENDING : classify(w, P.rule);
       }
     }
   }
@@ -1068,26 +1052,6 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
         const double add = (double)xsum + fsum * (1.0 / TWO_PI);
         if (add != 0.0) atomicAdd(w, add);
       }
-      if (P.counted) {
-        // counted pending flag 0x80 | n of this query (4-B aligned word, byte q & 3):
-        // decrement n; the lane that takes it to 0 reads the final winding and
-        // writes the class (a8).  Bytes outside 0x81..0xFC (overflow, uncounted,
-        // on-boundary in phase 1) are not counted and never touched here.
-        uint32_t *word = reinterpret_cast<uint32_t *>(P.flag + (q & ~3));
-        const int sh = 8 * (q & 3);
-        const uint32_t b0 = (*reinterpret_cast<volatile uint32_t *>(word) >> sh) & 0xFFu;
-        if (b0 >= 0x81u && b0 <= 0x80u + FLAG_MAXCNT) {
-          __threadfence();                                   // the winding update before the count
-          const uint32_t old = atomicSub(word, 1u << sh);
-          if (((old >> sh) & 0xFFu) == 0x81u) {             // this was the query's last pair
-            __threadfence();
-            const double wv = *reinterpret_cast<volatile double *>(w);
-            const uint32_t cls = isnan(wv) ? 2u : (uint32_t)classify(wv, P.rule);
-            atomicSub(word, (0x80u - cls) << sh);             // 0x80 -> cls, no borrow
-            if (COUNT && cls == 2u) atomicAdd(P.counters + 7, 1ull);
-          }
-        }
-      }
       live = false;
       i = WN_HARD_DYN ? total : i + (int)(gridDim.x * blockDim.x);   // fetch again / static grid stride
     }
@@ -1193,8 +1157,7 @@ __device__ __forceinline__ uint8_t finish_one(uint8_t fl, const double *__restri
 }
 
 __global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule,
-                         unsigned long long *counters, const int32_t *__restrict__ uncounted, int counted) {
-  if (counted && !*uncounted) return;   // every pending query was classified by k_hard (uniform)
+                         unsigned long long *counters) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   if (((uintptr_t)flag & 15) == 0) {
     const int64_t nv = n >> 4;
@@ -1418,13 +1381,13 @@ static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters, P.uncounted, P.counted);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters);
   } else {
     phase1(std::false_type{});
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr, P.uncounted, P.counted);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr);
   }
   launches += 4;
   if (F->timing_on) {
@@ -1519,9 +1482,6 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.hq = hq;
   P.hq_count = flags + 2;
   P.hq_next = flags + 3;
-  P.uncounted = flags + 4;
-  P.counted = (WN_COUNTED && ((uintptr_t)flag & 3) == 0 && !(std::getenv("WN_NO_COUNTED") && *std::getenv("WN_NO_COUNTED"))) ? 1 : 0;
-  P.maxcnt = std::getenv("WN_MAXCNT") ? std::max(1, std::min(FLAG_MAXCNT, atoi(std::getenv("WN_MAXCNT")))) : FLAG_MAXCNT;
   P.hq_cap = hq_cap;
   P.eps = F->eps;
   P.max_depth = F->max_depth;
@@ -1611,9 +1571,6 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   P.hq = (HardEntry *)(base + o_hq);
   P.hq_count = flags + 2;
   P.hq_next = flags + 3;
-  P.uncounted = flags + 4;
-  P.counted = (WN_COUNTED && ((uintptr_t)flag & 3) == 0 && !(std::getenv("WN_NO_COUNTED") && *std::getenv("WN_NO_COUNTED"))) ? 1 : 0;
-  P.maxcnt = std::getenv("WN_MAXCNT") ? std::max(1, std::min(FLAG_MAXCNT, atoi(std::getenv("WN_MAXCNT")))) : FLAG_MAXCNT;
   P.hq_cap = hq_cap;
   P.eps = F->eps;
   P.max_depth = F->max_depth;

@@ -13,7 +13,8 @@ for l in open("gpurun_out/bench_dev.log"):
             d["ms_per_step"], d["query_only"]["ms"], r["kernel_ms"], r["k3"]["ms"], r["frac"], d["grid"]["ms_per_step"], d["grid"]["query_ms"]))
         print(d["counters"])
 PY
-timeout 300 python scripts/trace_build.py 2>&1 | tail -25
+timeout 300 python scripts/trace_build.py 2>&1 | tail -12
+TRACE_MODE=2 timeout 300 python scripts/trace_build.py 2>&1 | tail -12
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-configs"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncuL.log 2>&1; echo "ncu launches rc=$?"
 python scripts/launch_summary.py gpurun_out/launches.csv | cut -c1-100 | head -24

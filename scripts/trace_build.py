@@ -10,6 +10,6 @@ geo = [T(wl["ctrl_uv"], torch.float64), T(wl["ctrl_w"], torch.float64), T(wl["se
        T(wl["loop_seg_off"], torch.int32), T(wl["face_loop_off"], torch.int32), T(wl["face_periodic"], torch.uint8),
        T(wl["face_domain"], torch.float64)]
 for i in range(6):
-    if i == 5: os.environ["WN_TRACE"] = "1"
+    if i == 5: os.environ["WN_TRACE"] = os.environ.get("TRACE_MODE", "1")
     wn.Faces.build(*geo).close()
     torch.cuda.synchronize()

@@ -308,28 +308,31 @@ def test_recursion_bounds_sound(precision):
                 assert row[9 + (1 << d) - 2 + k] >= arc[k * L:(k + 1) * L].sum() * (1 - 1e-9), (d, k)
 
 
-@pytest.mark.parametrize("mode", ["counted", "maxcnt1", "uncounted", "unaligned"])
-def test_pending_classification_paths(mode, monkeypatch):
-    """Queries with hard pairs are classified either by the k_hard lane that
-    completes their last pair (counted pending flags, 4-B aligned flag array)
-    or by the k_finish scan (more pairs than the count field holds, forced
-    here with WN_MAXCNT=1; counting disabled; an unaligned flag array): every
-    path gives the same flags and windings, and parity with the oracle."""
+def test_unaligned_flag_output():
+    """An output flag array at an odd address (k_finish's scalar path) gives
+    the same results as an aligned one, with parity against the oracle."""
     wl = G.gen_c2(n_queries=30_000)
-    if mode == "maxcnt1":
-        monkeypatch.setenv("WN_MAXCNT", "1")
-    if mode == "uncounted":
-        monkeypatch.setenv("WN_NO_COUNTED", "1")
     faces = wn.Faces.from_workload(wl)
     n = len(wl["face_id"])
-    if mode == "unaligned":
-        wbuf = torch.empty(n, dtype=torch.float64, device="cuda")
-        fbuf = torch.empty(n + 1, dtype=torch.uint8, device="cuda")[1:]     # odd address
-        r = faces.query(wl["face_id"], wl["uv"], out=(wbuf, fbuf))
-    else:
-        r = faces.query(wl["face_id"], wl["uv"])
+    wbuf = torch.empty(n, dtype=torch.float64, device="cuda")
+    fbuf = torch.empty(n + 1, dtype=torch.uint8, device="cuda")[1:]     # odd address
+    r = faces.query(wl["face_id"], wl["uv"], out=(wbuf, fbuf))
+    r2 = faces.query(wl["face_id"], wl["uv"])
     torch.cuda.synchronize()
     w, fl = r.winding.cpu().numpy(), r.flag.cpu().numpy()
+    assert np.array_equal(fl, r2.flag.cpu().numpy())
     faces.close()
-    assert fl.max() <= 3
     _check(wl, w, fl, min_cmp=0.85)
+
+
+def test_bad_period_rejected():
+    """A periodic axis needs a finite start and a finite period > 0 (device-side
+    input validation, WN_ERR_GEOM naming the first bad face and axis)."""
+    wl = G.gen_c3(n_queries=10)
+    for bad in ((0.0, 0.0, 0.0, wl["meta"]["T"]), (0.0, wl["meta"]["T"], np.nan, wl["meta"]["T"]),
+                (0.0, -1.0, 0.0, 1.0)):
+        w2 = dict(wl)
+        w2["face_domain"] = np.array([bad], dtype=np.float64)
+        with pytest.raises(wn.WNError) as e:
+            wn.Faces.from_workload(w2)
+        assert e.value.status == 2 and "period" in str(e.value)

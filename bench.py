@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 extra keys")
+    ap.add_argument("--shard", default="none", choices=["none", "faces"],
+                    help="N > 1: 'none' = weak scaling (a batch per GPU), 'faces' = strong scaling (one batch, face shards)")
     ap.add_argument("--cpu-1t-frac", type=float, default=0.01, help="fixed subsample of the 1-thread oracle rate")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
@@ -306,9 +308,24 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    wl = G.gen_c5(seed=rank_seed(rank))
+    if args.shard == "faces" and world > 1:
+        # strong scaling (SURVEY 8(e) face shards): ONE C5 batch split into
+        # contiguous face ranges balanced by (segments + 1) x queries
+        from paper_2510_25159_b200 import shard
+        full = G.gen_c5(seed=5)
+        bounds = shard.partition(shard.face_costs(full["loop_seg_off"], full["face_loop_off"], full["face_id"]), world)
+        f0, f1 = int(bounds[rank]), int(bounds[rank + 1])
+        wl, _ = shard.sub_batch(full, f0, f1, take_invalid=(rank == 0))
+        wl["meta"] = dict(grid=full["meta"]["grid"], grid_box=np.ascontiguousarray(full["meta"]["grid_box"][f0:f1]))
+        job_nq, job_pairs, scaling = len(full["face_id"]), G.n_input_pairs(full), "strong"
+        del full
+    else:
+        wl = G.gen_c5(seed=rank_seed(rank))
+        job_nq, job_pairs, scaling = None, None, "weak"
     nq = len(wl["face_id"])
     pairs = G.n_input_pairs(wl)
+    if job_nq is None:
+        job_nq, job_pairs = nq * world, pairs * world
     st = torch.cuda.current_stream(dev)
     T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
     geo_np = [wl["ctrl_uv"], wl["ctrl_w"], wl["seg_degree"], wl["loop_seg_off"], wl["face_loop_off"],
@@ -366,8 +383,8 @@ def main():
     clocks = _clock_summary(clk, tw0, tw1) if rank == 0 else None
     t_max = max_over_ranks(elapsed, dist, dev)
     ms_step = t_max / args.steps
-    value = nq * world / (ms_step / 1e3)
-    pairs_s = pairs * world / (ms_step / 1e3)
+    value = job_nq / (ms_step / 1e3)
+    pairs_s = job_pairs / (ms_step / 1e3)
     gpu_launches = (launches["build"] + launches["query"]) * args.steps
 
     # ---- query-only breakdown (untimed for the contract) ----
@@ -426,7 +443,7 @@ def main():
         b.record(st)
         torch.cuda.synchronize()
         et = max_over_ranks(a.elapsed_time(b), dist, dev)
-        e2e = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+        e2e = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
     # ---- implicit-grid path (wn_query_grid, Sec. 5.4.3 tessellation): the same
@@ -462,7 +479,7 @@ def main():
     torch.cuda.synchronize()
     gq_ms = g0.elapsed_time(g1) / nrep
     fc.close()
-    grid = {"api": "wn_query_grid", "ms_per_step": g_ms, "value": nq * world / (g_ms / 1e3), "unit": UNIT,
+    grid = {"api": "wn_query_grid", "ms_per_step": g_ms, "value": job_nq / (g_ms / 1e3), "unit": UNIT,
             "query_ms": gq_ms, "query_queries_per_s": nq / (gq_ms / 1e3), "steps": args.steps,
             "input_bytes_per_query": 0, "e2e": None}
     if not args.no_e2e:
@@ -501,7 +518,7 @@ def main():
         b.record(st)
         torch.cuda.synchronize()
         et = max_over_ranks(a.elapsed_time(b), dist, dev)
-        grid["e2e"] = {"value": nq * world / (et / ksteps / 1e3), "unit": UNIT,
+        grid["e2e"] = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in h_geo) + h_gb.numel() * 8),
                        "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
@@ -549,10 +566,11 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, no datasets)",
                 "config": {"workload": WORKLOAD, "queries": nq, "input_segment_pairs": pairs,
-                           "parallelism": "independent batch per GPU" if world > 1 else "single GPU",
+                           "parallelism": ("single GPU" if world == 1 else "independent batch per GPU" if scaling == "weak"
+                                           else "face shards of one batch (no exchange)"),
                            "l2": "inputs larger than L2 (1.64 GB queries per step), no flush",
                            "step": "wn_build_faces + wn_query + wn_free_faces",
                            "angle_mode": args.angle_mode},

@@ -233,7 +233,10 @@ __device__ __forceinline__ double poly_len(const double (&a)[N + 1], const doubl
 // bounds) plus its root span S0 (unmargined) for the hierarchy prefix sums and
 // the hot SEG record.  Both are fed by the same bound code (prep_n).
 struct PrepSink {
+  static constexpr bool kStaged = false;
+  using Rec = SegPrep;
   SegPrep *out;
+  __device__ void at(int, int, SegPrep *) {}
   __device__ void zero(int s) const {
     double2 *o2 = reinterpret_cast<double2 *>(out + s);
     for (int k = 0; k < 9; ++k) o2[k] = make_double2(0.0, 0.0);
@@ -272,11 +275,22 @@ __device__ __forceinline__ double binom5(int n, int j) {
 
 template <typename R>
 struct ColdSink {
-  BaseCold<R> *out;
-  double *s0;
-  double rel;   // relative margin (R5): 2^-40 fp64, 2^-17 fp32
+  // The records are indexed by the segment's position p in the degree-sorted
+  // order (inv[s] = p): a K1 CTA's records are then contiguous, assembled in
+  // shared memory (slot) and written with one bulk copy (coalesced).
+  static constexpr bool kStaged = true;
+  using Rec = BaseCold<R>;
+  BaseCold<R> *out;    // [p]
+  double *s0;          // [s] root span S0
+  int32_t *inv;        // [s] -> p
+  double rel;          // relative margin (R5): 2^-40 fp64, 2^-17 fp32
+  BaseCold<R> *slot;   // record under assembly (shared memory; global for k_prep_bad)
+  __device__ void at(int p, int s, BaseCold<R> *where) {
+    slot = where;
+    inv[s] = p;
+  }
   __device__ void zero(int s) const {
-    uint4 *o = reinterpret_cast<uint4 *>(out + s);
+    uint4 *o = reinterpret_cast<uint4 *>(slot);
     for (int k = 0; k < (int)(sizeof(BaseCold<R>) / 16); ++k) o[k] = make_uint4(0, 0, 0, 0);
     s0[s] = 0.0;
   }
@@ -285,8 +299,8 @@ struct ColdSink {
   // piece itself, depth 2 = the pair, depth 1 = two pairs (running max / sum in
   // scalars); min(2^-d max Bq, sum Lq) from the margined doubles, rounded up.
   double acc_b = 0.0, acc_l = 0.0;
-  __device__ void pieces(int s, int q, double B, double b0, double b1, double l0, double l1) {
-    BaseCold<R> *C = out + s;
+  __device__ void pieces(int, int q, double B, double b0, double b1, double l0, double l1) {
+    BaseCold<R> *C = slot;
     const double m0 = fmin(B, b0) * (1.0 + rel), m1 = fmin(B, b1) * (1.0 + rel);
     const double L0 = l0 * (1.0 + rel), L1 = l1 * (1.0 + rel);
     *reinterpret_cast<float2 *>(&C->Bq[q]) = make_float2(f_up(m0), f_up(m1));
@@ -306,8 +320,8 @@ struct ColdSink {
   __device__ void tail(int s, double, double S0) const { s0[s] = S0; }
   // written before the piece loop so that the control points die early
   template <int N>
-  __device__ void head(int s, double B, const double *px, const double *py, const double *W) const {
-    BaseCold<R> *C = out + s;
+  __device__ void head(int, double B, const double *px, const double *py, const double *W) const {
+    BaseCold<R> *C = slot;
     *reinterpret_cast<double2 *>(&C->x0) = make_double2(px[0], py[0]);
     *reinterpret_cast<double2 *>(&C->xn) = make_double2(px[N], py[N]);
     const double Bm = B * (1.0 + rel);
@@ -394,9 +408,6 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
 #ifndef PREP_SPLIT
 #define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels
 #endif
-#ifndef PREP_ONE
-#define PREP_ONE 0     // 1: one K1 kernel over all degrees (k_prep_all, measured slower); 0: one kernel per degree
-#endif
 // Per-degree K1: the degree-sorted segments split into the ranges of the sort
 // key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with
 // its own register budget (degree 1-3 need far fewer than degree 5).  bnd[k] =
@@ -418,36 +429,45 @@ __global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *
                                                   const double *__restrict__ w, Sink sink,
                                                   uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
   const int lo = bnd[N], hi = bnd[N + 1];
-  for (int p = lo + blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += gridDim.x * blockDim.x) {
-    const int s = order[p];
-    if (deg[s] == N) {
-      prep_n<N>(ctrl, w, coff[s], s, sink, serr);
-    } else {   // a degree outside 1..5 with these low bits (rejected on the host)
-      serr[s] = 1;
-      sink.zero(s);
+  if constexpr (Sink::kStaged) {
+    // records of this CTA's 128 consecutive sorted positions assembled in
+    // shared memory, then written out with one 1-D bulk copy (TMA store)
+    extern __shared__ __align__(128) unsigned char k1_stage[];
+    using Rec = typename Sink::Rec;
+    Rec *stage = reinterpret_cast<Rec *>(k1_stage);
+    for (int base = lo + blockIdx.x * blockDim.x; base < hi; base += gridDim.x * blockDim.x) {
+      const int p = base + threadIdx.x;
+      if (p < hi) {
+        const int s = order[p];
+        sink.at(p, s, stage + threadIdx.x);
+        if (deg[s] == N) {
+          prep_n<N>(ctrl, w, coff[s], s, sink, serr);
+        } else {   // a degree outside 1..5 with these low bits (rejected on the host)
+          serr[s] = 1;
+          sink.zero(s);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> async proxy
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned bytes = (unsigned)(min((int)blockDim.x, hi - base) * sizeof(Rec));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(sink.out + base),
+                     "r"((unsigned)__cvta_generic_to_shared(stage)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // stage reusable
+      }
+      __syncthreads();
     }
-  }
-}
-
-// One K1 kernel for all degrees: a grid-stride loop over the degree-sorted
-// order from the top (degree 5 first, the longest), one degree per warp except
-// at the range boundaries; no per-degree launches and no tail between them.
-template <class Sink>
-__global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_all(int32_t n, const int32_t *__restrict__ deg,
-                                                  const int32_t *__restrict__ coff, const double *__restrict__ ctrl,
-                                                  const double *__restrict__ w, Sink sink,
-                                                  uint8_t *__restrict__ serr, const int32_t *__restrict__ order) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int s = order[n - 1 - i];
-    switch (deg[s]) {
-      case 5: prep_n<5>(ctrl, w, coff[s], s, sink, serr); break;
-      case 4: prep_n<4>(ctrl, w, coff[s], s, sink, serr); break;
-      case 3: prep_n<3>(ctrl, w, coff[s], s, sink, serr); break;
-      case 2: prep_n<2>(ctrl, w, coff[s], s, sink, serr); break;
-      case 1: prep_n<1>(ctrl, w, coff[s], s, sink, serr); break;
-      default:   // rejected on the host (k_deg flag)
+  } else {
+    for (int p = lo + blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += gridDim.x * blockDim.x) {
+      const int s = order[p];
+      if (deg[s] == N) {
+        prep_n<N>(ctrl, w, coff[s], s, sink, serr);
+      } else {   // a degree outside 1..5 with these low bits (rejected on the host)
         serr[s] = 1;
         sink.zero(s);
+      }
     }
   }
 }
@@ -458,8 +478,10 @@ __global__ void k_prep_bad(const int32_t *__restrict__ bnd, Sink sink, uint8_t *
                            const int32_t *__restrict__ order) {
   const int n0 = bnd[1] - bnd[0], n1 = bnd[8] - bnd[6];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n0 + n1; i += gridDim.x * blockDim.x) {
-    const int s = order[i < n0 ? bnd[0] + i : bnd[6] + (i - n0)];
+    const int p = i < n0 ? bnd[0] + i : bnd[6] + (i - n0);
+    const int s = order[p];
     serr[s] = 1;
+    if constexpr (Sink::kStaged) sink.at(p, s, sink.out + p);
     sink.zero(s);
   }
 }
@@ -771,7 +793,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
                        const int32_t *__restrict__ loop_off,
                        const int32_t *__restrict__ loop_face, const uint8_t *__restrict__ face_per,
                        const double *__restrict__ face_dom, const double2 *__restrict__ lsta,
-                       const double *__restrict__ s0, const int2 *__restrict__ shift,
+                       const double *__restrict__ s0, const int32_t *__restrict__ inv, const int2 *__restrict__ shift,
                        const uint8_t *__restrict__ brk,
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const double2 *__restrict__ lend,
@@ -902,7 +924,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     // the copy record: base segment, target face, lift shift, copy translate
     const int2 k = shift[s];
     CopyRec cr;
-    cr.s = s;
+    cr.s = inv[s];
     cr.face = G.face;
     cr.ksu = pu ? k.x : 0;
     cr.ksv = pv ? k.y : 0;
@@ -1539,7 +1561,7 @@ void free_handle(wn_faces_t F) {
   // (its build or its latest query, on whatever stream that ran)
   if (F->last_use) cudaStreamWaitEvent(0, F->last_use, 0);
   if (F->owns_cold && F->cold) cache_free(F->cold, 0);
-  void *ps[] = {F->hot, F->copy, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
+  void *ps[] = {F->hot, F->copy, F->owns_cold ? (void *)F->inv : nullptr, F->face_rec_off, F->face_cold_off, F->face_order, F->face_dom,
                 F->face_per, F->face_ok, F->face_M, F->face_box, F->counters};
   for (void *p : ps)
     if (p) cache_free(p, 0);
@@ -1559,6 +1581,7 @@ struct BuildCtx {
   const double *dom;
   int32_t *coff, *loop_face;
   double *s0;       // per segment: root span S0 (K1, unmargined)
+  int32_t *inv;     // per segment: its BaseCold record (position in K1's degree-sorted order)
   int2 *shift;      // per segment: lift shift (K2a)
   uint8_t *brk;
   int2 *chain;      // per segment: (chain start index within its loop, chain length)
@@ -1588,21 +1611,16 @@ cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, c
   if ((e = D.alloc(&dt, tmp)) != cudaSuccess) return e;
   cub::DeviceRadixSort::SortPairs(dt, tmp, deg, d_degs, d_iota, d_order, n_segs, 0, 3, st);
   g_build_launches += 4;
-#if PREP_ONE
-  k_prep_all<<<std::min((n_segs + 127) / 128, 148 * PREP_DEG_MINB), 128, 0, st>>>(n_segs, deg, coff, ctrl, w, sink, serr,
-                                                                                   d_order);
-  ++g_build_launches;
-  return cudaGetLastError();
-#endif
   int32_t *d_bnd = nullptr;
   if ((e = D.alloc(&d_bnd, 9)) != cudaSuccess) return e;
   k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
   const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
-  k_prep_deg<5><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
-  k_prep_deg<4><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
-  k_prep_deg<3><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
-  k_prep_deg<2><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
-  k_prep_deg<1><<<pg, 128, 0, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  const size_t sm = Sink::kStaged ? 128 * sizeof(typename Sink::Rec) : 0;
+  k_prep_deg<5><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<4><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<3><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<2><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<1><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, sink, serr, d_order);
   g_build_launches += 7;
   return cudaGetLastError();
@@ -1615,7 +1633,7 @@ cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces
   const double rel = (sizeof(R) == 4) ? std::ldexp(1.0, -17) : std::ldexp(1.0, -40);
   ++g_build_launches;
   k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, B.st>>>(
-      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.lsta, B.s0, B.shift, B.brk, B.chain,
+      ng, dg, B.lso, B.loop_face, B.per, B.dom, B.lsta, B.s0, B.inv, B.shift, B.brk, B.chain,
       B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, F->copy);
   return cudaGetLastError();
 }
@@ -1891,14 +1909,16 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
   // K1 (reads the caller's control points: the host waits for g_ev_k1 before returning)
   // K1 writes the handle's per-segment cold records (BaseCold) and S0
   F->n_base = n_segs;
+  WN_CUDA(cache_alloc((void **)&F->inv, sizeof(int32_t) * (size_t)std::max(n_segs, 1), st));
+  B.inv = F->inv;
   WN_CUDA(cache_alloc(&F->cold, (fp32 ? sizeof(BaseCold<float>) : sizeof(BaseCold<double>)) * (size_t)std::max(n_segs, 1),
                       st));
   if (fp32)
     WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
-                      ColdSink<float>{(BaseCold<float> *)F->cold, B.s0, std::ldexp(1.0, -17)}, d_serr, D, st));
+                      ColdSink<float>{(BaseCold<float> *)F->cold, B.s0, F->inv, std::ldexp(1.0, -17)}, d_serr, D, st));
   else
     WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
-                      ColdSink<double>{(BaseCold<double> *)F->cold, B.s0, std::ldexp(1.0, -40)}, d_serr, D, st));
+                      ColdSink<double>{(BaseCold<double> *)F->cold, B.s0, F->inv, std::ldexp(1.0, -40)}, d_serr, D, st));
   if (n_loops) {
     k_s0pre<<<(int)((32 * (int64_t)n_loops + 255) / 256), 256, 0, st>>>(n_loops, n_segs, B.lso, B.s0, B.s0pre);
     ++g_build_launches;
@@ -2063,7 +2083,8 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       WN_CUDA(D.alloc((BaseCold<double> **)&probe_cold, std::max(n_segs, 1)));
       WN_CUDA(D.alloc(&tmp_s0, std::max(n_segs, 1)));
       WN_CUDA(launch_k1(n_segs, B.deg, B.coff, ctrl_uv, ctrl_w,
-                        ColdSink<double>{(BaseCold<double> *)probe_cold, tmp_s0, std::ldexp(1.0, -40)}, d_serr, D, st));
+                        ColdSink<double>{(BaseCold<double> *)probe_cold, tmp_s0, F->inv, std::ldexp(1.0, -40)}, d_serr, D,
+                        st));
     }
     WN_CUDA(cudaStreamSynchronize(st));   // K1 outputs (bounds, span prefixes) are read by the probes' k_emit
     auto run_probes = [&](const std::vector<QueryRec> &Q, std::vector<double> &res) -> wn_status_t {
@@ -2270,13 +2291,15 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
 namespace wn {
 namespace {
 template <typename R>
-__global__ void k_rec_bounds(int32_t n, const BaseCold<R> *__restrict__ C, double *__restrict__ out) {
+__global__ void k_rec_bounds(int32_t n, const BaseCold<R> *__restrict__ C, const int32_t *__restrict__ inv,
+                             double *__restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
+  const BaseCold<R> &c = C[inv[s]];
   double *o = out + 23 * (size_t)s;
-  o[0] = (double)C[s].B;
-  for (int q = 0; q < 8; ++q) o[1 + q] = (double)C[s].Bq[q];
-  for (int i = 0; i < 14; ++i) o[9 + i] = (double)C[s].Sp[i];
+  o[0] = (double)c.B;
+  for (int q = 0; q < 8; ++q) o[1 + q] = (double)c.Bq[q];
+  for (int i = 0; i < 14; ++i) o[9 + i] = (double)c.Sp[i];
 }
 }  // namespace
 }  // namespace wn
@@ -2288,8 +2311,10 @@ extern "C" wn_status_t wn_recursion_bounds(wn_faces_t F, double *out, void *stre
   WN_CUDA(cudaSetDevice(F->device));
   if (F->ready) WN_CUDA(cudaStreamWaitEvent(st, F->ready, 0));
   const int n = F->n_base;
-  if (F->precision == 1) k_rec_bounds<float><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<float> *)F->cold, out);
-  else k_rec_bounds<double><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<double> *)F->cold, out);
+  if (F->precision == 1)
+    k_rec_bounds<float><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<float> *)F->cold, F->inv, out);
+  else
+    k_rec_bounds<double><<<(n + 255) / 256, 256, 0, st>>>(n, (const BaseCold<double> *)F->cold, F->inv, out);
   WN_CUDA(cudaGetLastError());
   WN_CUDA(cudaStreamSynchronize(st));
   return WN_OK;

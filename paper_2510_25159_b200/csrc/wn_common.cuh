@@ -104,7 +104,7 @@ struct __align__(16) BaseCold<float> {    // 192 B
   float pad[2];
 };
 struct __align__(8) CopyRec {
-  int32_t s;          // base (input) segment
+  int32_t s;          // base record (BaseCold index of the input segment)
   int32_t face;       // face whose domain holds the periods of the translations
   int32_t ksu, ksv;   // lift shift of the segment (0 on non-periodic axes)
   int32_t ku, kv;     // lattice translate of the copy (0 on non-periodic axes)
@@ -257,6 +257,7 @@ struct wn_faces_s {
   wn::CopyRec *copy = nullptr;     // [n_seg] emitted segments
   int owns_cold = 1;               // 0: `cold` borrowed from another handle (pairing probes)
   int32_t n_base = 0;              // input segments (BaseCold records)
+  int32_t *inv = nullptr;          // [n_base] input segment -> its BaseCold record
   int32_t *face_rec_off = nullptr; // [n_faces+1]
   int32_t *face_cold_off = nullptr;// [n_faces+1]
   int32_t *face_order = nullptr;   // [n_faces] by cost, descending

@@ -48,7 +48,23 @@ static bool alloc_exact() {
   return v != 0;
 }
 
+// WN_ALLOC_POISON=1 (checked runs): every block handed out is first filled
+// with 0xA5 bytes (NaN-like doubles, huge ints), so a kernel that reads memory
+// nobody wrote changes its results -- the determinism / parity comparisons of
+// scripts/checked_run.sh then catch it (an initcheck substitute).
+static bool alloc_poison() {
+  static const int v = [] { const char *s = std::getenv("WN_ALLOC_POISON"); return (s && *s && *s != '0') ? 1 : 0; }();
+  return v != 0;
+}
+static cudaError_t cache_alloc_raw(void **out, size_t bytes, cudaStream_t st);
+
 cudaError_t cache_alloc(void **out, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cache_alloc_raw(out, bytes, st);
+  if (e == cudaSuccess && alloc_poison() && bytes) e = cudaMemsetAsync(*out, 0xA5, bytes, st);
+  return e;
+}
+
+static cudaError_t cache_alloc_raw(void **out, size_t bytes, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;

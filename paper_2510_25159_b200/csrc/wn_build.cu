@@ -437,6 +437,7 @@ __global__ void __launch_bounds__(128, PREP_DEG_MINB) k_prep_deg(const int32_t *
     Rec *stage = reinterpret_cast<Rec *>(k1_stage);
     for (int base = lo + blockIdx.x * blockDim.x; base < hi; base += gridDim.x * blockDim.x) {
       const int p = base + threadIdx.x;
+      WN_DCHECK(blockDim.x <= 128);
       if (p < hi) {
         const int s = order[p];
         sink.at(p, s, stage + threadIdx.x);
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
                        const int2 *__restrict__ chain, const double *__restrict__ s0pre,
                        const double2 *__restrict__ lend,
                        const LoopInfo *__restrict__ info, double rel, Hot<R> *__restrict__ hot,
-                       CopyRec *__restrict__ copy) {
+                       CopyRec *__restrict__ copy, int32_t n_rec_total, int32_t n_copy_total) {
   const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (g >= n_groups) return;
@@ -909,6 +910,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
             sum = s0pre[se] - (sa > s0_ ? s0pre[sa - 1] : 0.0);
           }
           const int sub = 2 * (bnd - a + 1) - 2;          // records of the subtree after the SPAN
+          WN_DCHECK(off >= G.rec_off && off + sub < G.rec_off + G.nrec);
           put_rec<R>(hot, off, ex, ey, filter_span(sum), K_SPAN | fa | ((uint32_t)sub << 8));
         }
         if (j <= mid) { bnd = mid; off += 1; }
@@ -920,6 +922,7 @@ __global__ void __launch_bounds__(32 * EMIT_WARPS, EMIT_MINB) k_emit(int32_t n_g
     // conservative fp32 filter, S0 (1 + 2^-17) + 2^-16 scale (scale = M 2^40),
     // and the filter's (1 - 2^-18) error shrink folded in as a further
     // (1 + 2^-17); fp32 records: S0 (1 + 2^-17) + M32.
+    WN_DCHECK(r >= G.rec_off && r < G.rec_off + G.nrec && r < n_rec_total && G.cold_off + idx < n_copy_total);
     put_rec<R>(hot, r, pxn, pyn, filter_span(s0[s]), K_SEG | fa | ((uint32_t)(G.cold_local + idx) << 8));
     // the copy record: base segment, target face, lift shift, copy translate
     const int2 k = shift[s];
@@ -1477,6 +1480,7 @@ __global__ void k_plan_fill(int32_t n_faces, int32_t n_loops, const int32_t *__r
   FillSink S{groups + o.x, f, o.y, o.z, o.z};
   const int l0 = min(max(flo[f], 0), n_loops), l1 = min(max(flo[f + 1], l0), n_loops);
   plan_face(S, L, l0, l1, C, pair_beta, pair_s, tree != 0);
+  WN_DCHECK(f + 1 >= n_faces || S.out == groups + off[f + 1].x);   // the fill pass wrote exactly the counted groups
 }
 
 }  // namespace wn
@@ -1634,7 +1638,7 @@ cudaError_t launch_emit(const BuildCtx &B, int ng, const PlanGroup *dg, wn_faces
   ++g_build_launches;
   k_emit<R><<<(int)((32 * (int64_t)ng + 32 * EMIT_WARPS - 1) / (32 * EMIT_WARPS)), 32 * EMIT_WARPS, 0, B.st>>>(
       ng, dg, B.lso, B.loop_face, B.per, B.dom, B.lsta, B.s0, B.inv, B.shift, B.brk, B.chain,
-      B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, F->copy);
+      B.s0pre, B.lend, B.info, (double)rel, (Hot<R> *)F->hot, F->copy, (int32_t)F->n_records, (int32_t)F->n_seg);
   return cudaGetLastError();
 }
 
@@ -2091,6 +2095,7 @@ extern "C" wn_status_t wn_build_faces(int32_t n_faces, int32_t n_loops, int32_t 
       wn_faces_t T = new wn_faces_s();
       T->precision = 0; T->eps = 1e-12; T->max_depth = 60; T->device = dev; T->opt = O; T->opt.rule = 0; T->opt.angle_mode = 0;   // the probe records are crossing-mode (C.angle = false)
       wn_status_t rc = materialise<double>(B, VP, vper, vdom, vM, probe_cold, T);
+      T->n_base = n_segs;
       if (rc != WN_OK) { free_handle(T); return rc; }
       const int nq = (int)Q.size();
       std::vector<int32_t> hf(nq);

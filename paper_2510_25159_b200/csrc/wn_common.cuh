@@ -16,6 +16,26 @@
 
 #include "../../include/wn.h"
 
+// Device-side invariant checks of the CHECKED build (-DWN_CHECKED, see
+// scripts/checked_run.sh): bounds of every shared / global index the kernels
+// derive.  A failure prints the condition and traps (the launch fails, the
+// caller sees WN_ERR_CUDA).  Compiled out otherwise.
+#ifdef WN_CHECKED
+#include <cstdio>
+#define WN_DCHECK(c)                                                                                   \
+  do {                                                                                                 \
+    if (!(c)) {                                                                                        \
+      printf("WN_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x,   \
+             (int)threadIdx.x, #c);                                                                    \
+      __trap();                                                                                        \
+    }                                                                                                  \
+  } while (0)
+#else
+#define WN_DCHECK(c) \
+  do {               \
+  } while (0)
+#endif
+
 namespace wn {
 
 // ---------------------------------------------------------------------------

@@ -76,6 +76,8 @@ struct QParams {
   const Hot<R> *hot;
   const BaseCold<R> *cold;   // per input segment
   const CopyRec *copy;       // per emitted segment
+  int64_t nq;                // queries of the batch (checked build: index bounds)
+  int32_t n_copy, n_base, n_rec;
   const int32_t *face_rec_off;
   const int32_t *face_cold_off;
   const double *face_dom;
@@ -446,6 +448,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   if (t == 0) {
     mbar_init(&s_bar, 1);
     fence_mbar_init();
+    WN_DCHECK(nrec >= 0 && rec0 >= 0 && rec0 + nrec <= P.n_rec);
     if (single && nrec > 0) {
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&s_bar, (unsigned)(nrec * sizeof(Hot<R>)));
@@ -517,6 +520,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     b = __shfl_sync(0xffffffffu, b, 0);
     bool ovf = false;
     for (int i = lane; i < hn_; i += 32) {
+      WN_DCHECK(i < HWB && s_hb[warp][i].q >= 0 && s_hb[warp][i].q < P.nq);
       if (b + i < P.hq_cap) {
         P.hq[b + i] = s_hb[warp][i];
       } else {
@@ -656,6 +660,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         const int kr = P.skey[pos];
         const int k = kr >> 12;
         const uint32_t off = (s_hist[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+        WN_DCHECK((int)off + (kr & 0xFFF) < T.qcnt);
         P.sorder[T.qbeg + (int)off + (kr & 0xFFF)] = unsorted ? P.perm[pos] : pos;
       }
       __syncthreads();   // the order (global, this CTA's range) is visible to the block
@@ -678,6 +683,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     bool valid = sub + lt < T.qcnt;
     const int32_t pos = (int32_t)(T.qbeg + sub) + lt;
     int32_t qi = valid ? (spatial ? P.sorder[pos] : unsorted ? P.perm[pos] : pos) : 0;
+    WN_DCHECK(!valid || (qi >= 0 && qi < P.nq));
     double px = 0.0, py = 0.0;
     if (valid) {
       double u, v;
@@ -749,9 +755,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       const int spe = (int)sbase + cn * RB;
       while (sp < spe) {
         HotView<R> h;
+        WN_DCHECK(sp >= (int)sbase && ((sp - (int)sbase) % RB) == 0);
         h.load((unsigned)sp);
         const uint32_t meta = h.meta;
         const uint32_t kind = meta & 0xFu;
+        WN_DCHECK(kind <= K_SLINE && kind != 2u);
         const bool act = valid && sp >= sse;
         if (COUNT && lane == 0) ++c_rec;
         if (__builtin_expect((meta & 0xEu) == 0u, 1)) {   // SEG (0) or SPAN (1)
@@ -836,6 +844,8 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                   H.py = py;
                   H.q = qi;
                   H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | (ANGLE ? 0x80000000u : 0u);
+                  WN_DCHECK(hn_ + cnt <= HWB && (int)(meta >> 8) >= 0 &&
+                            cold0 + (int)(meta >> 8) < P.n_copy);
                   s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
                   pend |= 1 | 4;
                   if (COUNT) ++c_hard;
@@ -985,7 +995,9 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
       if (i >= total) continue;
       const HardEntry H = P.hq[i];
       angle = H.c >> 31;
+      WN_DCHECK((int)(H.c & 0x7fffffffu) < P.n_copy && H.q >= 0 && H.q < P.nq);
       const CopyRec cr = P.copy[H.c & 0x7fffffffu];
+      WN_DCHECK(cr.s >= 0 && cr.s < P.n_base);
       C = P.cold + cr.s;
       Fr = copy_frame(cr, P.face_dom);
       qx = (R)H.px;
@@ -1036,6 +1048,7 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
         R mx, my;
         eval_copy(C, n, Fr, (R)tm, mx, my);
         ++evals;
+        WN_DCHECK(sp <= MAXD);
         std_[sp - 1] = (int8_t)(d + 1);
         stx[sp] = mx - qx;
         sty[sp] = my - qy;
@@ -1467,6 +1480,10 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   P.hot = (const Hot<R> *)F->hot;
   P.cold = (const BaseCold<R> *)F->cold;
   P.copy = F->copy;
+  P.nq = n;
+  P.n_copy = (int32_t)F->n_seg;
+  P.n_base = F->n_base;
+  P.n_rec = (int32_t)F->n_records;
   P.face_rec_off = F->face_rec_off;
   P.face_cold_off = F->face_cold_off;
   P.face_dom = F->face_dom;
@@ -1556,6 +1573,10 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   P.hot = (const Hot<R> *)F->hot;
   P.cold = (const BaseCold<R> *)F->cold;
   P.copy = F->copy;
+  P.nq = n;
+  P.n_copy = (int32_t)F->n_seg;
+  P.n_base = F->n_base;
+  P.n_rec = (int32_t)F->n_records;
   P.face_rec_off = F->face_rec_off;
   P.face_cold_off = F->face_cold_off;
   P.face_dom = F->face_dom;

@@ -403,9 +403,6 @@ constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: 
 
 constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (one per lane: small queues stay spread)
-#ifndef WN_P1_NOVOTE
-#define WN_P1_NOVOTE 1          // no warp vote in front of per-lane slow paths (plain branches)
-#endif
 #ifndef WN_P1_PINF
 #define WN_P1_PINF 1            // the query's fp32 coordinates pinned in registers
 #endif
@@ -415,12 +412,19 @@ constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (on
 constexpr int SP_BINS = 1024;   // Morton cells of the spatial regrouping (32 x 32)
 constexpr int SP_COHERENT = 24; // mean warp-footprint perimeter (cells) above which a unit is regrouped
 
-#ifndef WN_P1_MINB
-#define WN_P1_MINB 4
+#ifndef WN_QPL
+#define WN_QPL 1                // queries per thread in k_phase1 (1 or 2)
 #endif
+#ifndef WN_P1_MINB
+#define WN_P1_MINB (WN_QPL == 1 ? 4 : 3)
+#endif
+constexpr int QPL = WN_QPL;
+constexpr int QTK = QT * QPL;   // queries per sub-tile of k_phase1
 
 // ANGLE: the build's angle_mode (every record of a handle carries the same F_ANGLE);
-// GRID: implicit-grid batch (wn_query_grid) instead of explicit uv
+// GRID: implicit-grid batch (wn_query_grid) instead of explicit uv.
+// Each thread evaluates QPL queries (QPL = 2: two independent query chains per
+// record, the record load / decode / warp decisions shared by 64 queries).
 template <typename R, bool COUNT, bool ANGLE, bool GRID>
 __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
@@ -459,8 +463,6 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   const double *dom = P.face_dom + 4 * f;
   const int unsorted = *P.unsorted;
   const int cold0 = P.face_cold_off[f];
-  // implicit grid: a unit lies inside one grid (units are cut per grid), so the
-  // grid index, its box and the cell steps are per-CTA values
   // spatial regrouping of explicit units (see below)
   __shared__ uint32_t s_hist[SP_BINS / 2];   // 16-bit counters, two per word
   __shared__ int s_wsum[NWARP];
@@ -468,8 +470,10 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   __shared__ double s_v0;                    // row probe: v of the unit's first query
   __shared__ int s_nu;                       // row probe: first index with another v
   if (t < 2) s_coh[t] = 0;
-  if (t == 0) s_nu = QT;
-  // (kept in shared memory, not in registers across the record loop)
+  if (t == 0) s_nu = QTK;
+  // implicit grid: a unit lies inside one grid (units are cut per grid), so the
+  // grid index, its box and the cell steps are per-CTA values (kept in shared
+  // memory, not in registers across the record loop)
   __shared__ double s_grid[4];   // u_lo, v_lo, (u_hi - u_lo) / nu, (v_hi - v_lo) / nv
   __shared__ int s_gloc0;
   if constexpr (GRID) {
@@ -495,14 +499,16 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   int hn_ = 0;                   // entries in this warp's hard-pair buffer (warp-uniform)
   unsigned long long c_pairs = 0, c_hard = 0, c_cull = 0, c_span = 0, c_rec = 0, c_desc = 0, c_prn = 0;
   __syncthreads();               // barrier initialised
-  // pend bits of the lane's current query: 1 hard pairs queued, 2 one of them
+  // pend bits of the lane's current queries: 1 hard pairs queued, 2 one of them
   // overflowed the queue, 4 entries still in the warp buffer
-  int pend = 0;
+  int pend[QPL];
+#pragma unroll
+  for (int k = 0; k < QPL; ++k) pend[k] = 0;
 
   // flush the warp's buffer to the global queue with one exact reservation.
   // Entries past the capacity mark their query FLAG_OVERFLOW (recomputed
-  // exactly by k_overflow); the lane's own current query also keeps bit 2
-  // because its final flag is written after this.
+  // exactly by k_overflow); the lane's own current queries also keep bit 2
+  // because their final flags are written after this.
   auto flush = [&]() {
     __syncwarp();
     int b = 0;
@@ -528,20 +534,29 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         ovf = true;
       }
     }
-    if (__any_sync(0xffffffffu, ovf) && (pend & 4)) pend |= 2;
+    const bool any_ovf = __any_sync(0xffffffffu, ovf);
+#pragma unroll
+    for (int k = 0; k < QPL; ++k) {
+      if (any_ovf && (pend[k] & 4)) pend[k] |= 2;
+      pend[k] &= ~4;
+    }
     __syncwarp();
     hn_ = 0;
-    pend &= ~4;
   };
 
   // Spatial regrouping (explicit batches): the unit's queries are put in
   // Morton order of a 32 x 32 cell grid over the face's box (a counting sort
-  // in shared memory, once per unit), so that each warp takes 32 queries
+  // in shared memory, once per unit), so that each warp takes 32 QPL queries
   // that lie close together and agrees more often on pruning a span or
   // culling a group.  A permutation of whole queries: no value changes.  The
   // order goes to a per-unit scratch range (L2-resident), read per sub-tile.
   bool spatial = false;
-  int lt = t;                    // query of this thread within a sub-tile (see below)
+  // queries of this thread within a sub-tile: query k of lane l of warp w is
+  // at sub-tile position w 32 QPL + 32 k + l (given order, Morton order), or
+  // (2-D tiles) in a bw x (32 QPL / bw) block of cells of the warp
+  int lt[QPL];
+#pragma unroll
+  for (int k = 0; k < QPL; ++k) lt[k] = warp * 32 * QPL + 32 * k + lane;
   if constexpr (!GRID) {
     spatial = P.spatial && T.qcnt > 32;
     const float4 fb = spatial ? P.face_box[f] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -593,7 +608,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           }
         }
         // Row probe: a unit that starts with whole rows of length nu (v constant
-        // along a row; nu dividing QT) -- a row-major tessellation grid -- is
+        // along a row; nu dividing QTK) -- a row-major tessellation grid -- is
         // mapped to 2-D warp tiles like wn_query_grid, without sorting
         double vt = 0.0;
         if (t < T.qcnt) {
@@ -606,9 +621,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         if (t > 0 && t < T.qcnt && !(vt == s_v0)) atomicMin(&s_nu, t);
         __syncthreads();
         const int nu = s_nu;
-        if (T.qcnt >= QT && nu >= 8 && nu < QT && QT % nu == 0 && QT / nu <= 32) {
-          const int bw = 32 / (QT / nu);   // row-major unit: the same 2-D tiles as a grid
-          lt = (lane / bw) * nu + warp * bw + lane % bw;
+        if (T.qcnt >= QTK && nu >= 8 && nu < QTK && QTK % nu == 0 && QTK / nu <= 32 * QPL) {
+          const int bw = 32 * QPL / (QTK / nu);   // row-major unit: the same 2-D tiles as a grid
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            const int i = lane + 32 * k;
+            lt[k] = (i / bw) * nu + warp * bw + i % bw;
+          }
           spatial = false;
         } else {
           spatial = s_coh[0] > SP_COHERENT * s_coh[1];
@@ -668,67 +687,91 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     }
   }
 
-  // query of this thread within a sub-tile.  Implicit grids whose rows tile a
-  // sub-tile (grid_blk = 32 / rows-per-sub-tile > 0) give each warp a compact
-  // grid_blk x (32 / grid_blk) block of cells instead of a run of one row: the
+  // Implicit grids whose rows tile a sub-tile (grid_blk > 0) give each warp a
+  // compact bw x (32 QPL / bw) block of cells instead of a run of one row: the
   // warp's queries then lie close together, so they agree more often on
   // pruning a hierarchy span or culling a group (fewer warp-level descents).
   if constexpr (GRID) {
     const int bw = P.grid_blk;
-    if (bw > 0) lt = (lane / bw) * P.grid_nu + warp * bw + lane % bw;
-  }
-
-  // one unit = up to QU queries of face f, processed QT at a time
-  for (int sub = 0; sub < T.qcnt; sub += QT) {
-    bool valid = sub + lt < T.qcnt;
-    const int32_t pos = (int32_t)(T.qbeg + sub) + lt;
-    int32_t qi = valid ? (spatial ? P.sorder[pos] : unsorted ? P.perm[pos] : pos) : 0;
-    WN_DCHECK(!valid || (qi >= 0 && qi < P.nq));
-    double px = 0.0, py = 0.0;
-    if (valid) {
-      double u, v;
-      if constexpr (GRID) {
-        const int loc = s_gloc0 + sub + lt;
-        const int iv = loc / P.grid_nu, iu = loc - iv * P.grid_nu;
-        u = __dadd_rn(s_grid[0], __dmul_rn((double)iu + 0.5, s_grid[2]));   // = grid_coord(), bit for bit
-        v = __dadd_rn(s_grid[1], __dmul_rn((double)iv + 0.5, s_grid[3]));
-      } else {
-        u = P.uv[2 * (int64_t)qi];
-        v = P.uv[2 * (int64_t)qi + 1];
-        // the next sub-tile's point to L2 while this one is swept (given order
-        // or row tiles: the position is the query index)
-        if (!spatial && !unsorted && sub + QT + lt < T.qcnt)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.uv + 2 * (int64_t)(pos + QT)));
-      }
-      if (!isfinite(u) || !isfinite(v)) {
-        P.winding[qi] = nan_d();
-        P.flag[qi] = 3;
-        valid = false;
-      } else {
-        if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
-        if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
-        if (!F64) { u = (double)(float)u; v = (double)(float)v; }
-        px = u;
-        py = v;
+    if (bw > 0) {
+#pragma unroll
+      for (int k = 0; k < QPL; ++k) {
+        const int i = lane + 32 * k;
+        lt[k] = (i / bw) * P.grid_nu + warp * bw + i % bw;
       }
     }
-    float pxf = (float)px, pyf = (float)py;
+  }
+
+  // one unit = up to QU queries of face f, processed QTK at a time
+  for (int sub = 0; sub < T.qcnt; sub += QTK) {
+    bool valid[QPL];
+    int32_t qi[QPL];
+    double px[QPL], py[QPL];
+    float pxf[QPL], pyf[QPL];
+#pragma unroll
+    for (int k = 0; k < QPL; ++k) {
+      valid[k] = sub + lt[k] < T.qcnt;
+      const int32_t pos = (int32_t)(T.qbeg + sub) + lt[k];
+      qi[k] = valid[k] ? (spatial ? P.sorder[pos] : unsorted ? P.perm[pos] : pos) : 0;
+      WN_DCHECK(!valid[k] || (qi[k] >= 0 && qi[k] < P.nq));
+      px[k] = 0.0;
+      py[k] = 0.0;
+      if (valid[k]) {
+        double u, v;
+        if constexpr (GRID) {
+          const int loc = s_gloc0 + sub + lt[k];
+          const int iv = loc / P.grid_nu, iu = loc - iv * P.grid_nu;
+          u = __dadd_rn(s_grid[0], __dmul_rn((double)iu + 0.5, s_grid[2]));   // = grid_coord(), bit for bit
+          v = __dadd_rn(s_grid[1], __dmul_rn((double)iv + 0.5, s_grid[3]));
+        } else {
+          u = P.uv[2 * (int64_t)qi[k]];
+          v = P.uv[2 * (int64_t)qi[k] + 1];
+          // the next sub-tile's point to L2 while this one is swept (given order
+          // or row tiles: the position is the query index)
+          if (!spatial && !unsorted && sub + QTK + lt[k] < T.qcnt)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.uv + 2 * (int64_t)(pos + QTK)));
+        }
+        if (!isfinite(u) || !isfinite(v)) {
+          P.winding[qi[k]] = nan_d();
+          P.flag[qi[k]] = 3;
+          valid[k] = false;
+        } else {
+          if (per & 1) u = reduce_coord(u, dom[0], dom[1]);
+          if (per & 2) v = reduce_coord(v, dom[2], dom[3]);
+          if (!F64) { u = (double)(float)u; v = (double)(float)v; }
+          px[k] = u;
+          py[k] = v;
+        }
+      }
+      pxf[k] = (float)px[k];
+      pyf[k] = (float)py[k];
 #if WN_P1_PINF
-    // opaque: kept in registers instead of re-derived from (px, py) with an
-    // F2F.F32.F64 conversion in every record iteration
-    asm volatile("" : "+f"(pxf), "+f"(pyf));
+      // opaque: kept in registers instead of re-derived from (px, py) with an
+      // F2F.F32.F64 conversion in every record iteration
+      asm volatile("" : "+f"(pxf[k]), "+f"(pyf[k]));
 #endif
+    }
 
     double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
-    // per-lane chain state: previous chain point (exact), its fp32 distance, its side of the cut
-    double zx = 0.0, zy = 0.0;
-    float cdf = 0.f;
-    int up = 0;                    // side of the branch cut of the previous chain point (0/1)
-    bool onb = false;
-    int skip_end = 0;              // lane inactive (culled / pruned subtree) while gr < skip_end
-    int xs = 0, halves = 0;
-    pend = 0;
-    double fr = 0.0;
+    // per-query chain state: previous chain point (exact), its fp32 distance, its side of the cut
+    double zx[QPL], zy[QPL];
+    float cdf[QPL];
+    int up[QPL];                   // side of the branch cut of the previous chain point (0/1)
+    bool onb[QPL];
+    int skip_end[QPL];             // query inactive (culled / pruned subtree) while gr < skip_end
+    int xs[QPL], halves[QPL];
+    double fr[QPL];
+#pragma unroll
+    for (int k = 0; k < QPL; ++k) {
+      zx[k] = zy[k] = 0.0;
+      cdf[k] = 0.f;
+      up[k] = 0;
+      onb[k] = false;
+      skip_end[k] = 0;
+      xs[k] = halves[k] = 0;
+      fr[k] = 0.0;
+      pend[k] = 0;
+    }
     int gr = 0;                    // warp-uniform record cursor
 
     for (int cb = 0; cb < nrec; cb += RCH) {
@@ -747,11 +790,13 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         }
       }
       const int ce = cb + cn;
-      // the record cursor and the lanes' subtree ends as shared addresses
+      // the record cursor and the queries' subtree ends as shared addresses
       // within this chunk (converted back to record indices at its end)
       constexpr int RB = (int)sizeof(Hot<R>);
       int sp = (int)sbase + (gr - cb) * RB;                    // shared address of record gr
-      int sse = (int)sbase + (skip_end - cb) * RB;             // lane inactive while sp < sse
+      int sse[QPL];                                            // query inactive while sp < sse
+#pragma unroll
+      for (int k = 0; k < QPL; ++k) sse[k] = (int)sbase + (skip_end[k] - cb) * RB;
       const int spe = (int)sbase + cn * RB;
       while (sp < spe) {
         HotView<R> h;
@@ -760,170 +805,209 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
         const uint32_t meta = h.meta;
         const uint32_t kind = meta & 0xFu;
         WN_DCHECK(kind <= K_SLINE && kind != 2u);
-        const bool act = valid && sp >= sse;
+        bool act[QPL];
+#pragma unroll
+        for (int k = 0; k < QPL; ++k) act[k] = valid[k] && sp >= sse[k];
         if (COUNT && lane == 0) ++c_rec;
         if (__builtin_expect((meta & 0xEu) == 0u, 1)) {   // SEG (0) or SPAN (1)
           // a4: root eps-test and ellipse test (Alg. 1 lines 1-3, Eq. 1, R9,
           // R5) for SEG; the path-hierarchy bound Omega_{j,k} (span =
           // sum of root spans) for SPAN.  The fp32 filter certifies "outside the
-          // ellipse, d >= eps"; a crossing / hard / uncertain lane takes the exact
-          // slow path.
-          int u1;
-          float df;
-          if constexpr (F64) {
-            u1 = h.y >= py ? 1 : 0;                              // exact side of the branch cut
-            df = fdist_ftz(h.fx - pxf, h.fy - pyf);
-          } else {
-            u1 = h.fy >= pyf ? 1 : 0;
-            const float dx = h.fx - pxf, dy = h.fy - pyf;
-            df = sqrtf(dx * dx + dy * dy);
+          // ellipse, d >= eps"; a crossing / hard / uncertain query takes the
+          // exact slow path.
+          int u1[QPL];
+          float df[QPL];
+          bool pr[QPL];
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            if constexpr (F64) {
+              u1[k] = h.y >= py[k] ? 1 : 0;                        // exact side of the branch cut
+              df[k] = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+            } else {
+              u1[k] = h.fy >= pyf[k] ? 1 : 0;
+              const float dx = h.fx - pxf[k], dy = h.fy - pyf[k];
+              df[k] = sqrtf(dx * dx + dy * dy);
+            }
+            pr[k] = cdf[k] + df[k] > h.fs && df[k] > eps_c;        // certified outside, end point >= eps
           }
-          const bool pr = cdf + df > h.fs && df > eps_c;          // certified outside, end point >= eps
           if (meta & 1u) {                                       // K_SPAN
-            if (COUNT && act) ++c_span;
-            // descend unless every active lane prunes the whole run
-            const bool descend = act && !pr;
-            if (COUNT && descend) ++c_desc;
+            // descend unless every active query prunes the whole run
+            bool descend = false;
+#pragma unroll
+            for (int k = 0; k < QPL; ++k) {
+              if (COUNT && act[k]) ++c_span;
+              if (COUNT && act[k] && !pr[k]) ++c_desc;
+              descend |= act[k] && !pr[k];
+            }
             if (!__any_sync(0xffffffffu, descend)) {
-              // every active lane substitutes the run's chord (homotopy)
-#if WN_P1_NOVOTE
-              if (act && (u1 != up || ANGLE)) {       // (a plain branch: uniform when no lane crosses)
-                if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-                else xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
-              }
-#else
-              if (__any_sync(0xffffffffu, act && (u1 != up || ANGLE))) {
-                if (act) {
-                  if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-                  else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+              // every active query substitutes the run's chord (homotopy)
+#pragma unroll
+              for (int k = 0; k < QPL; ++k) {
+                if (act[k] && (u1[k] != up[k] || ANGLE)) {     // (a plain branch: uniform when no query crosses)
+                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  else xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
                 }
+                if (act[k]) { zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k]; }
               }
-#endif
-              if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
               sp += (int)(meta >> 8) * RB;
               if (COUNT && lane == 0) ++c_cull;
-            } else if (act && pr) {
-              // this lane prunes the run: chord now, inactive for the subtree
-              if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-              else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
-              zx = h.x; zy = h.y; cdf = df; up = u1;
-              sse = sp + RB + (int)(meta >> 8) * RB;
+            } else {
+#pragma unroll
+              for (int k = 0; k < QPL; ++k) {
+                if (act[k] && pr[k]) {
+                  // this query prunes the run: chord now, inactive for the subtree
+                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  else if (u1[k] != up[k]) xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k];
+                  sse[k] = sp + RB + (int)(meta >> 8) * RB;
+                }
+              }
             }
           } else {
-            const bool need = act && (!pr || u1 != up || ANGLE);
-            bool hard = false;
-#if WN_P1_NOVOTE
-            {
-              if (need) {            // (a plain branch; the ballot below is the one vote)
-#else
-            if (__any_sync(0xffffffffu, need)) {
-              if (need) {
-#endif
-                if (!(df > eps_c)) {                             // filter cannot certify d >= eps
+            bool hard[QPL];
+#pragma unroll
+            for (int k = 0; k < QPL; ++k) {
+              hard[k] = false;
+              if (act[k] && (!pr[k] || u1[k] != up[k] || ANGLE)) {   // (a plain branch; the ballot below is the one vote)
+                if (!(df[k] > eps_c)) {                              // filter cannot certify d >= eps
                   if constexpr (F64) {
-                    const double dx = h.x - px, dy = h.y - py;
-                    onb |= sqrt(dx * dx + dy * dy) < eps;
+                    const double dx = h.x - px[k], dy = h.y - py[k];
+                    onb[k] |= sqrt(dx * dx + dy * dy) < eps;
                   } else {
-                    onb |= df < (float)eps;
+                    onb[k] |= df[k] < (float)eps;
                   }
                 }
-                if (cdf + df > h.fs && !onb) {                   // pruned: chord (a5)
-                  if (ANGLE) fr += (double)chord_angle(zx - px, zy - py, h.x - px, h.y - py);
-                  else if (u1 != up) xs += xcount(zx - px, zy - py, h.x - px, h.y - py);
+                if (cdf[k] + df[k] > h.fs && !onb[k]) {              // pruned: chord (a5)
+                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  else if (u1[k] != up[k]) xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
                 } else {
-                  hard = !onb;                                   // exact recursion in phase 2
+                  hard[k] = !onb[k];                                 // exact recursion in phase 2
                 }
               }
-              const unsigned m = __ballot_sync(0xffffffffu, hard);
-              if (m) {
-                const int cnt = __popc(m);
-                if (hn_ + cnt > HWB) flush();
-                if (hard) {
+            }
+            unsigned m[QPL];
+            int cnt = 0;
+#pragma unroll
+            for (int k = 0; k < QPL; ++k) {
+              m[k] = __ballot_sync(0xffffffffu, hard[k]);
+              cnt += __popc(m[k]);
+            }
+            if (cnt) {
+              if (hn_ + cnt > HWB) flush();
+              int basek = hn_;
+#pragma unroll
+              for (int k = 0; k < QPL; ++k) {
+                if (hard[k]) {
                   HardEntry H;
-                  H.px = px;
-                  H.py = py;
-                  H.q = qi;
+                  H.px = px[k];
+                  H.py = py[k];
+                  H.q = qi[k];
                   H.c = (uint32_t)(cold0 + (int)(meta >> 8)) | (ANGLE ? 0x80000000u : 0u);
-                  WN_DCHECK(hn_ + cnt <= HWB && (int)(meta >> 8) >= 0 &&
-                            cold0 + (int)(meta >> 8) < P.n_copy);
-                  s_hb[warp][hn_ + __popc(m & ((1u << lane) - 1u))] = H;
-                  pend |= 1 | 4;
+                  WN_DCHECK(hn_ + cnt <= HWB && (int)(meta >> 8) >= 0 && cold0 + (int)(meta >> 8) < P.n_copy);
+                  s_hb[warp][basek + __popc(m[k] & ((1u << lane) - 1u))] = H;
+                  pend[k] |= 1 | 4;
                   if (COUNT) ++c_hard;
                 }
-                hn_ += cnt;
+                basek += __popc(m[k]);
               }
+              hn_ += cnt;
             }
-            if (act) { zx = h.x; zy = h.y; cdf = df; up = u1; }
-            if (COUNT && act) ++c_pairs;
-            if (COUNT && act && !hard && !onb) ++c_prn;      // chord substituted (a5)
+#pragma unroll
+            for (int k = 0; k < QPL; ++k) {
+              if (act[k]) { zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k]; }
+              if (COUNT && act[k]) ++c_pairs;
+              if (COUNT && act[k] && !hard[k] && !onb[k]) ++c_prn;     // chord substituted (a5)
+            }
           }
         } else if (kind == K_MOVE || kind == K_MOVEG) {
-          const double nx = h.x - px, ny = h.y - py;
-          float nd;
-          if constexpr (F64) nd = fdist_ftz(h.fx - pxf, h.fy - pyf);
-          else nd = sqrtf((float)(nx * nx + ny * ny));
-          if (act) {
-            if (!(nd > eps_c)) onb |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
-            if (kind == K_MOVEG && !ANGLE) {
-              // gap chord Z -> A': -omega(p,Z,A') + its crossing
-              const double ax = zx - px, ay = zy - py;
-              const double cr = canon_cross(ax, ay, nx, ny);
-              fr -= atan2(cr, ax * nx + ay * ny);
-              xs += xcount_exact(ax, ay, nx, ny, cr);
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            const double nx = h.x - px[k], ny = h.y - py[k];
+            float nd;
+            if constexpr (F64) nd = fdist_ftz(h.fx - pxf[k], h.fy - pyf[k]);
+            else nd = sqrtf((float)(nx * nx + ny * ny));
+            if (act[k]) {
+              if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
+              if (kind == K_MOVEG && !ANGLE) {
+                // gap chord Z -> A': -omega(p,Z,A') + its crossing
+                const double ax = zx[k] - px[k], ay = zy[k] - py[k];
+                const double cr = canon_cross(ax, ay, nx, ny);
+                fr[k] -= atan2(cr, ax * nx + ay * ny);
+                xs[k] += xcount_exact(ax, ay, nx, ny, cr);
+              }
             }
+            zx[k] = h.x; zy[k] = h.y; cdf[k] = nd;
+            up[k] = (F64 ? (h.y >= py[k]) : (h.fy >= pyf[k])) ? 1 : 0;
           }
           if (kind == K_MOVE) { gax = h.x; gay = h.y; }
-          zx = h.x; zy = h.y; cdf = nd;
-          up = (F64 ? (h.y >= py) : (h.fy >= pyf)) ? 1 : 0;
         } else if (kind == K_GROUP) {
           // copy-group / closed-loop cull: p outside the group's box => exactly 0
-          const bool out = !act || group_out_v(h, pxf, pyf);
+          bool out[QPL], all_out = true;
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            out[k] = !act[k] || group_out_v(h, pxf[k], pyf[k]);
+            all_out &= out[k];
+          }
           const int skip = (int)(meta >> 8);
-          if (__all_sync(0xffffffffu, out)) {
+          if (__all_sync(0xffffffffu, all_out)) {
             sp += skip * RB;
             if (COUNT && lane == 0) ++c_cull;
-          } else if (out && act) {
-            sse = sp + RB + skip * RB;
+          } else {
+#pragma unroll
+            for (int k = 0; k < QPL; ++k)
+              if (out[k] && act[k]) sse[k] = sp + RB + skip * RB;
           }
         } else if (kind == K_LINE) {
           // omega(p,L) = +-1/2, p on L counts as left (R11)
-          const double q = (meta & F_AXISV) ? px : py;
-          const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
-          if (act) halves += left ? 1 : -1;
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            const double q = (meta & F_AXISV) ? px[k] : py[k];
+            const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
+            if (act[k]) halves[k] += left ? 1 : -1;
+          }
         } else if (kind == K_SLINE) {
-          if (act) halves += sline_left(meta, h.x, h.y, px, py, dom) ? 1 : -1;
+#pragma unroll
+          for (int k = 0; k < QPL; ++k)
+            if (act[k]) halves[k] += sline_left(meta, h.x, h.y, px[k], py[k], dom) ? 1 : -1;
         } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
-          if (act) {
-            const double cx = zx - px, cy = zy - py, ax = gax - px, ay = gay - py;
-            if (kind == K_XCH) {
-              xs -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
-            } else if (kind == K_NCH) {
-              fr -= chord_angle(ax, ay, cx, cy);
-            } else {
-              const double cr = canon_cross(cx, cy, ax, ay);
-              fr -= atan2(cr, cx * ax + cy * ay);
-              xs += xcount_exact(cx, cy, ax, ay, cr);
+#pragma unroll
+          for (int k = 0; k < QPL; ++k) {
+            if (act[k]) {
+              const double cx = zx[k] - px[k], cy = zy[k] - py[k], ax = gax - px[k], ay = gay - py[k];
+              if (kind == K_XCH) {
+                xs[k] -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
+              } else if (kind == K_NCH) {
+                fr[k] -= chord_angle(ax, ay, cx, cy);
+              } else {
+                const double cr = canon_cross(cx, cy, ax, ay);
+                fr[k] -= atan2(cr, cx * ax + cy * ay);
+                xs[k] += xcount_exact(cx, cy, ax, ay, cr);
+              }
             }
           }
         }
         sp += RB;
       }
       gr = cb + (sp - (int)sbase) / RB;
-      skip_end = cb + (sse - (int)sbase) / RB;
+#pragma unroll
+      for (int k = 0; k < QPL; ++k) skip_end[k] = cb + (sse[k] - (int)sbase) / RB;
       // all warps done with this chunk before it is overwritten (multi-chunk faces)
-      if (!single && (ce < nrec || sub + QT < T.qcnt)) __syncthreads();
+      if (!single && (ce < nrec || sub + QTK < T.qcnt)) __syncthreads();
     }
 
     // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
-    if (valid) {
-      if (onb) {
-        P.winding[qi] = nan_d();
-        P.flag[qi] = 2;
-        if (COUNT) atomicAdd(P.counters + 7, 1ull);
-      } else {
-        const double w = (double)xs + 0.5 * (double)halves + fr * (1.0 / TWO_PI);
-        P.winding[qi] = w;
-        P.flag[qi] = (pend & 2) ? FLAG_OVERFLOW : (pend & 1) ? FLAG_PENDING : classify(w, P.rule);
+#pragma unroll
+    for (int k = 0; k < QPL; ++k) {
+      if (valid[k]) {
+        if (onb[k]) {
+          P.winding[qi[k]] = nan_d();
+          P.flag[qi[k]] = 2;
+          if (COUNT) atomicAdd(P.counters + 7, 1ull);
+        } else {
+          const double w = (double)xs[k] + 0.5 * (double)halves[k] + fr[k] * (1.0 / TWO_PI);
+          P.winding[qi[k]] = w;
+          P.flag[qi[k]] = (pend[k] & 2) ? FLAG_OVERFLOW : (pend[k] & 1) ? FLAG_PENDING : classify(w, P.rule);
+        }
       }
     }
   }
@@ -1421,7 +1505,7 @@ static wn_status_t launch_query(wn_faces_t F, int64_t n, const int32_t *face_id,
   // small ones keep >= ~4 waves of CTAs
   int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
   if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(16, atoi(s)));   // <= 16: a unit <= 4096 queries (12-bit rank in the regrouping key)
-  const int qu = QT * sub;
+  const int qu = (QT * sub + QTK - 1) / QTK * QTK;   // whole k_phase1 sub-tiles, <= 4096
   const int64_t max_tiles64 = (n + qu - 1) / qu + nf;
   if (n > INT32_MAX - 1 || max_tiles64 > INT32_MAX) {
     set_error("wn_query: batch too large (n=%lld); split it", (long long)n);
@@ -1536,7 +1620,7 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   }
   int sub = (int)std::min<int64_t>(16, std::max<int64_t>(1, n / ((int64_t)QT * 148 * 16)));
   if (const char *s = std::getenv("WN_SUBTILES")) sub = std::max(1, std::min(16, atoi(s)));   // <= 16: a unit <= 4096 queries (12-bit rank in the regrouping key)
-  const int qu = QT * sub;
+  const int qu = (QT * sub + QTK - 1) / QTK * QTK;   // whole k_phase1 sub-tiles, <= 4096
   const int tpg = (int)((G + qu - 1) / qu);
   const int64_t max_tiles64 = (int64_t)n_grid * tpg;
   if (max_tiles64 > INT32_MAX) { set_error("wn_query_grid: too many tiles"); return WN_ERR_ARG; }
@@ -1609,8 +1693,9 @@ static wn_status_t launch_query_grid(wn_faces_t F, int32_t n_grid, const int32_t
   // 2-D warp blocks when a sub-tile is R whole rows (R = QT / nu) and a block
   // of R rows x (32 / R) columns fits: units start at multiples of QT
   P.grid_blk = 0;
-  if (nu > 0 && nu <= QT && QT % nu == 0 && QT / nu <= 32 && !(std::getenv("WN_GRID_LINEAR") && *std::getenv("WN_GRID_LINEAR")))
-    P.grid_blk = 32 / (QT / nu);
+  if (nu > 0 && nu <= QTK && QTK % nu == 0 && QTK / nu <= 32 * QPL &&
+      !(std::getenv("WN_GRID_LINEAR") && *std::getenv("WN_GRID_LINEAR")))
+    P.grid_blk = 32 * QPL / (QTK / nu);
   {
     const wn_status_t rc = launch_k3<R>(F, P, n, nullptr, max_tiles, st, launches);
     if (rc != WN_OK) return rc;

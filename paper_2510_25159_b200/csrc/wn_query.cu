@@ -406,8 +406,8 @@ constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (on
 #ifndef WN_P1_PINF
 #define WN_P1_PINF 1            // the query's fp32 coordinates pinned in registers
 #endif
-#ifndef WN_HARD_V2
-#define WN_HARD_V2 1            // 1: k_hard2 (evaluation-converged iterations); 0: k_hard (one node per iteration)
+#ifndef WN_HARD_BPS
+#define WN_HARD_BPS 4           // k_hard CTAs per SM
 #endif
 #ifndef WN_HARD_DYN
 #define WN_HARD_DYN 0           // 1: dynamic fetching of hard pairs per warp (measured slower on C5); 0: static grid stride
@@ -1164,125 +1164,6 @@ __global__ void __launch_bounds__(256) k_hard(QParams<R> P) {
   }
 }
 
-// K3b, evaluation-converged form: each outer iteration every lane first
-// advances its own recursion to the next node that must be SPLIT -- testing
-// nodes, substituting the chords of leaves (cheap), finishing pairs and
-// starting new ones (grid-strided) in a per-lane inner loop -- and then all
-// lanes that found one evaluate their split point together, so the O(n)
-// Horner evaluation (the expensive step) runs converged.  Same decisions and
-// arithmetic as hard_pair() / k_hard.
-template <typename R, bool COUNT>
-__global__ void __launch_bounds__(256) k_hard2(QParams<R> P) {
-  const int total = min(*P.hq_count, P.hq_cap);
-  const R eps = (R)P.eps;
-  const R eps2 = eps * eps;
-  const int max_depth = P.max_depth;
-  int i = (int)(blockIdx.x * blockDim.x + threadIdx.x);   // this lane's next pair
-  const int stride = (int)(gridDim.x * blockDim.x);
-  R stx[MAXD + 1], sty[MAXD + 1];
-  int8_t std_[MAXD + 1];
-  const BaseCold<R> *C = nullptr;
-  CopyFrame Fr{0.0, 0.0, 0.0, 0.0};
-  R qx = 0, qy = 0, M = 0, Lx = 0, Ly = 0, rL = 0;     // rL: squared distance to the left end
-  int n = 0, sp = 0, xsum = 0, q = 0;
-  double ta = 0.0, fsum = 0.0;
-  bool live = false, root = false, angle = false;
-  unsigned long long nodes = 0, evals = 0, leaves = 0;
-  int dmax = 0;
-  while (true) {
-    bool need_eval = false;
-    // A: advance to the next split (per lane, divergent, cheap steps)
-    while (true) {
-      if (!live) {
-        if (i >= total) break;                              // nothing left for this lane
-        const HardEntry H = P.hq[i];
-        i += stride;
-        angle = H.c >> 31;
-        WN_DCHECK((int)(H.c & 0x7fffffffu) < P.n_copy && H.q >= 0 && H.q < P.nq);
-        const CopyRec cr = P.copy[H.c & 0x7fffffffu];
-        WN_DCHECK(cr.s >= 0 && cr.s < P.n_base);
-        C = P.cold + cr.s;
-        Fr = copy_frame(cr, P.face_dom);
-        qx = (R)H.px;
-        qy = (R)H.py;
-        q = H.q;
-        M = margin_r<R>(__ldg(P.face_M + cr.face));
-        n = __ldg(&C->n);
-        Lx = (R)Fr.X(__ldg(&C->x0)) - qx;
-        Ly = (R)Fr.Y(__ldg(&C->y0)) - qy;
-        rL = Lx * Lx + Ly * Ly;
-        stx[0] = (R)Fr.X(__ldg(&C->xn)) - qx;
-        sty[0] = (R)Fr.Y(__ldg(&C->yn)) - qy;
-        std_[0] = 0;
-        sp = 1;
-        ta = 0.0;
-        xsum = 0;
-        fsum = 0.0;
-        root = true;
-        live = true;
-      }
-      // node [ta, ta + 2^-d] with right end point (rx, ry), top of the stack
-      const R rx = stx[sp - 1], ry = sty[sp - 1];
-      const int d = std_[sp - 1];
-      const R rR = rx * rx + ry * ry;
-      bool split, ob;
-      ++nodes;
-      if (root) {
-        root = false;
-        ob = rL < eps2 || rR < eps2;                        // Alg. 1 line 1 on the root
-        split = true;
-      } else {
-        ob = rR < eps2;                                     // Alg. 1 line 1
-        const R span = node_span(C, d, ta) + M;              // Eq. 2 + margin (R5)
-        split = !outside_ellipse(rL, rR, span);             // Alg. 1 line 3
-      }
-      if (!ob && split && d >= max_depth) ob = true;        // depth cap (R6)
-      bool done = ob;
-      if (!ob) {
-        if (split) { need_eval = true; break; }             // B evaluates its split point
-        if (angle) fsum += (double)chord_angle(Lx, Ly, rx, ry);   // chord substitution
-        else xsum += xcount(Lx, Ly, rx, ry);
-        ++leaves;
-        Lx = rx; Ly = ry; rL = rR;
-        ta += ldexp(1.0, -d);
-        done = --sp == 0;
-      }
-      if (done) {
-        double *w = P.winding + q;
-        if (ob) {
-          atomicExch(reinterpret_cast<unsigned long long *>(w), 0x7ff8000000000000ULL);
-        } else {
-          const double add = (double)xsum + fsum * (1.0 / TWO_PI);
-          if (add != 0.0) atomicAdd(w, add);
-        }
-        live = false;
-      }
-    }
-    if (!__any_sync(0xffffffffu, need_eval)) break;
-    // B: the split point m = (a+b)/2 of every lane that needs one
-    if (need_eval) {
-      const int d = std_[sp - 1];
-      const double tm = ta + ldexp(1.0, -(d + 1));
-      R mx, my;
-      eval_copy(C, n, Fr, (R)tm, mx, my);
-      ++evals;
-      WN_DCHECK(sp <= MAXD);
-      std_[sp - 1] = (int8_t)(d + 1);
-      stx[sp] = mx - qx;
-      sty[sp] = my - qy;
-      std_[sp] = (int8_t)(d + 1);
-      ++sp;
-      dmax = max(dmax, d + 1);
-    }
-  }
-  if (COUNT) {
-    cnt_add<COUNT>(P.counters, 2, nodes);
-    cnt_add<COUNT>(P.counters, 3, evals);
-    cnt_add<COUNT>(P.counters, 4, leaves);
-    atomicMax(P.counters + 5, (unsigned long long)dmax);
-  }
-}
-
 // K3d: queries whose hard pairs overflowed the global queue: the whole record
 // program again for that query, exact root tests against the (valid, inflated)
 // stored span and the recursion inline.  Normally never has work.
@@ -1581,7 +1462,7 @@ static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const
     WN_CUDA(cudaEventCreate(&e1));
     WN_CUDA(cudaEventRecord(e0, st));
   }
-  const int hb = 148 * 8;
+  const int hb = 148 * WN_HARD_BPS;   // k_hard CTAs (one wave at 4 resident CTAs / SM)
   const bool ang = F->opt.angle_mode == 1;
   const bool grid = P.grid_box != nullptr;
   auto phase1 = [&](auto cnt_tag) {
@@ -1598,15 +1479,13 @@ static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const
     WN_CUDA(cudaMemsetAsync(F->counters, 0, 16 * sizeof(unsigned long long), st));
     phase1(std::true_type{});
     if (em) WN_CUDA(cudaEventRecord(em, st));
-    if (WN_HARD_V2) k_hard2<R, true><<<hb, 256, 0, st>>>(P);
-    else k_hard<R, true><<<hb, 256, 0, st>>>(P);
+    k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
     k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters);
   } else {
     phase1(std::false_type{});
     if (em) WN_CUDA(cudaEventRecord(em, st));
-    if (WN_HARD_V2) k_hard2<R, false><<<hb, 256, 0, st>>>(P);
-    else k_hard<R, false><<<hb, 256, 0, st>>>(P);
+    k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
     k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr);
   }

@@ -407,7 +407,7 @@ constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (on
 #define WN_P1_PINF 1            // the query's fp32 coordinates pinned in registers
 #endif
 #ifndef WN_HARD_BPS
-#define WN_HARD_BPS 4           // k_hard CTAs per SM
+#define WN_HARD_BPS 8           // k_hard CTAs per SM (2 waves; 2 or 4 measured no better)
 #endif
 #ifndef WN_HARD_DYN
 #define WN_HARD_DYN 0           // 1: dynamic fetching of hard pairs per warp (measured slower on C5); 0: static grid stride
@@ -418,6 +418,40 @@ constexpr int SP_COHERENT = 24; // mean warp-footprint perimeter (cells) above w
 #ifndef WN_QPL
 #define WN_QPL 1                // queries per thread in k_phase1 (1 or 2)
 #endif
+#ifndef WN_P1_ZIDX
+#define WN_P1_ZIDX 1            // chain points as shared addresses of their records (not 2 doubles)
+#endif
+
+// exact point of the record at shared address a (fp64 records: (x, y) at +16;
+// fp32 records: (fx, fy) at +0, promoted)
+template <typename R>
+__device__ __forceinline__ void zget(unsigned a, double &x, double &y) {
+  if constexpr (sizeof(R) == 8) {
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + 16) : "memory");
+  } else {
+    float fx, fy;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(fx), "=f"(fy) : "r"(a) : "memory");
+    x = fx;
+    y = fy;
+  }
+}
+// the address zget reads for a 16-B parking slot
+template <typename R>
+__device__ __forceinline__ unsigned zslot(unsigned slot) { return sizeof(R) == 8 ? slot - 16 : slot; }
+// copy the point of record a into the parking slot; returns its zget address
+template <typename R>
+__device__ __forceinline__ unsigned zpark(unsigned a, unsigned slot) {
+  if constexpr (sizeof(R) == 8) {
+    double x, y;
+    zget<R>(a, x, y);
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(slot), "d"(x), "d"(y) : "memory");
+  } else {
+    float fx, fy;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(fx), "=f"(fy) : "r"(a) : "memory");
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(slot), "f"(fx), "f"(fy) : "memory");
+  }
+  return zslot<R>(slot);
+}
 #ifndef WN_P1_MINB
 #define WN_P1_MINB (WN_QPL == 1 ? 4 : 3)
 #endif
@@ -431,10 +465,15 @@ constexpr int QTK = QT * QPL;   // queries per sub-tile of k_phase1
 template <typename R, bool COUNT, bool ANGLE, bool GRID>
 __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
-  constexpr int RCH = F64 ? 1024 : 2048;                 // records per staged chunk (32 KB)
+  // records per staged chunk: 32 KB, or 28 KB when the chain-point parking
+  // slots (4.2 KB) must fit the 48-KB static shared memory too
+  constexpr int RCH = (F64 ? 1024 : 2048) * (WN_P1_ZIDX ? 7 : 8) / 8;
   __shared__ __align__(128) Hot<R> s_rec[RCH];
   __shared__ HardEntry s_hb[NWARP][HWB];
   __shared__ __align__(8) uint64_t s_bar;
+#if WN_P1_ZIDX
+  __shared__ __align__(16) double2 s_park[NTH * QPL + NWARP];   // chain points parked across chunks
+#endif
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
   const Tile T = P.tiles[blockIdx.x];
@@ -755,9 +794,24 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
 #endif
     }
 
-    double gax = 0.0, gay = 0.0;   // group start A (warp-uniform, set by MOVE)
-    // per-query chain state: previous chain point (exact), its fp32 distance, its side of the cut
+    // per-query chain state: previous chain point (exact), its fp32 distance,
+    // its side of the cut; and the group start A (warp-uniform, set by MOVE).
+    // WN_P1_ZIDX: the points are kept as the shared address of the record
+    // that holds them (read back only when a crossing is computed)
+#if WN_P1_ZIDX
+    unsigned zs[QPL], gs = sbase;
+#define ZSET(k) (zs[k] = (unsigned)sp)
+#define ZGET(k, X, Y) double X, Y; zget<R>(zs[k], X, Y)
+#define GSET() (gs = (unsigned)sp)
+#define GGET(X, Y) double X, Y; zget<R>(gs, X, Y)
+#else
     double zx[QPL], zy[QPL];
+    double gax = 0.0, gay = 0.0;
+#define ZSET(k) (zx[k] = h.x, zy[k] = h.y)
+#define ZGET(k, X, Y) const double X = zx[k], Y = zy[k]
+#define GSET() (gax = h.x, gay = h.y)
+#define GGET(X, Y) const double X = gax, Y = gay
+#endif
     float cdf[QPL];
     int up[QPL];                   // side of the branch cut of the previous chain point (0/1)
     bool onb[QPL];
@@ -766,7 +820,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     double fr[QPL];
 #pragma unroll
     for (int k = 0; k < QPL; ++k) {
+#if WN_P1_ZIDX
+      zs[k] = sbase;
+#else
       zx[k] = zy[k] = 0.0;
+#endif
       cdf[k] = 0.f;
       up[k] = 0;
       onb[k] = false;
@@ -847,10 +905,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
 #pragma unroll
               for (int k = 0; k < QPL; ++k) {
                 if (act[k] && (u1[k] != up[k] || ANGLE)) {     // (a plain branch: uniform when no query crosses)
-                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
-                  else xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  ZGET(k, zxk, zyk);
+                  if (ANGLE) fr[k] += (double)chord_angle(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
+                  else xs[k] += xcount(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
                 }
-                if (act[k]) { zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k]; }
+                if (act[k]) { ZSET(k); cdf[k] = df[k]; up[k] = u1[k]; }
               }
               sp += (int)(meta >> 8) * RB;
               if (COUNT && lane == 0) ++c_cull;
@@ -859,9 +918,12 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
               for (int k = 0; k < QPL; ++k) {
                 if (act[k] && pr[k]) {
                   // this query prunes the run: chord now, inactive for the subtree
-                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
-                  else if (u1[k] != up[k]) xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
-                  zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k];
+                  if (ANGLE || u1[k] != up[k]) {
+                    ZGET(k, zxk, zyk);
+                    if (ANGLE) fr[k] += (double)chord_angle(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
+                    else xs[k] += xcount(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
+                  }
+                  ZSET(k); cdf[k] = df[k]; up[k] = u1[k];
                   sse[k] = sp + RB + (int)(meta >> 8) * RB;
                 }
               }
@@ -881,8 +943,11 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
                   }
                 }
                 if (cdf[k] + df[k] > h.fs && !onb[k]) {              // pruned: chord (a5)
-                  if (ANGLE) fr[k] += (double)chord_angle(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
-                  else if (u1[k] != up[k]) xs[k] += xcount(zx[k] - px[k], zy[k] - py[k], h.x - px[k], h.y - py[k]);
+                  if (ANGLE || u1[k] != up[k]) {
+                    ZGET(k, zxk, zyk);
+                    if (ANGLE) fr[k] += (double)chord_angle(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
+                    else xs[k] += xcount(zxk - px[k], zyk - py[k], h.x - px[k], h.y - py[k]);
+                  }
                 } else {
                   hard[k] = !onb[k];                                 // exact recursion in phase 2
                 }
@@ -917,7 +982,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
             }
 #pragma unroll
             for (int k = 0; k < QPL; ++k) {
-              if (act[k]) { zx[k] = h.x; zy[k] = h.y; cdf[k] = df[k]; up[k] = u1[k]; }
+              if (act[k]) { ZSET(k); cdf[k] = df[k]; up[k] = u1[k]; }
               if (COUNT && act[k]) ++c_pairs;
               if (COUNT && act[k] && !hard[k] && !onb[k]) ++c_prn;     // chord substituted (a5)
             }
@@ -933,16 +998,17 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
               if (!(nd > eps_c)) onb[k] |= F64 ? (sqrt(nx * nx + ny * ny) < eps) : (nd < (float)eps);
               if (kind == K_MOVEG && !ANGLE) {
                 // gap chord Z -> A': -omega(p,Z,A') + its crossing
-                const double ax = zx[k] - px[k], ay = zy[k] - py[k];
+                ZGET(k, zxk, zyk);
+                const double ax = zxk - px[k], ay = zyk - py[k];
                 const double cr = canon_cross(ax, ay, nx, ny);
                 fr[k] -= atan2(cr, ax * nx + ay * ny);
                 xs[k] += xcount_exact(ax, ay, nx, ny, cr);
               }
             }
-            zx[k] = h.x; zy[k] = h.y; cdf[k] = nd;
+            ZSET(k); cdf[k] = nd;
             up[k] = (F64 ? (h.y >= py[k]) : (h.fy >= pyf[k])) ? 1 : 0;
           }
-          if (kind == K_MOVE) { gax = h.x; gay = h.y; }
+          if (kind == K_MOVE) GSET();
         } else if (kind == K_GROUP) {
           // copy-group / closed-loop cull: p outside the group's box => exactly 0
           bool out[QPL], all_out = true;
@@ -976,7 +1042,9 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
 #pragma unroll
           for (int k = 0; k < QPL; ++k) {
             if (act[k]) {
-              const double cx = zx[k] - px[k], cy = zy[k] - py[k], ax = gax - px[k], ay = gay - py[k];
+              ZGET(k, zxk, zyk);
+              GGET(gxk, gyk);
+              const double cx = zxk - px[k], cy = zyk - py[k], ax = gxk - px[k], ay = gyk - py[k];
               if (kind == K_XCH) {
                 xs[k] -= xcount_exact(ax, ay, cx, cy, canon_cross(ax, ay, cx, cy));
               } else if (kind == K_NCH) {
@@ -994,10 +1062,31 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       gr = cb + (sp - (int)sbase) / RB;
 #pragma unroll
       for (int k = 0; k < QPL; ++k) skip_end[k] = cb + (sse[k] - (int)sbase) / RB;
+#if WN_P1_ZIDX
+      if (!single) {
+        // the chunk is about to be overwritten: chain points that still live in
+        // it move to this thread's (warp's) parking slot
+        const unsigned lo = sbase, hi = sbase + (unsigned)(RCH * RB);
+#pragma unroll
+        for (int k = 0; k < QPL; ++k)
+          if (zs[k] >= lo && zs[k] < hi) zs[k] = zpark<R>(zs[k], smem_u32(&s_park[t * QPL + k]));
+        if (gs >= lo && gs < hi) {
+          const unsigned slot = smem_u32(&s_park[NTH * QPL + warp]);
+          __syncwarp();
+          if (lane == 0) zpark<R>(gs, slot);
+          __syncwarp();
+          gs = zslot<R>(slot);
+        }
+      }
+#endif
       // all warps done with this chunk before it is overwritten (multi-chunk faces)
       if (!single && (ce < nrec || sub + QTK < T.qcnt)) __syncthreads();
     }
 
+#undef ZSET
+#undef ZGET
+#undef GSET
+#undef GGET
     // ---- a8 (phase-1 part): reduce, classify or hand over to phase 2 ----
 #pragma unroll
     for (int k = 0; k < QPL; ++k) {

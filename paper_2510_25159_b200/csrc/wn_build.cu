@@ -408,6 +408,9 @@ __device__ __forceinline__ void prep_n(const double *__restrict__ ctrl, const do
 #ifndef PREP_SPLIT
 #define PREP_SPLIT 8   // CTAs per SM of the per-degree K1 kernels
 #endif
+#ifndef K1_STREAMS
+#define K1_STREAMS 1   // 1: the per-degree K1 kernels run concurrently on side streams
+#endif
 // Per-degree K1: the degree-sorted segments split into the ranges of the sort
 // key (deg & 7, the radix sort's 3 bits) so that each degree variant runs with
 // its own register budget (degree 1-3 need far fewer than degree 5).  bnd[k] =
@@ -1521,6 +1524,9 @@ cudaEvent_t g_pin_ev[64] = {};
 bool g_pin_pending[64] = {};
 // per device: the auxiliary stream of the device planner and its fork/join events
 cudaStream_t g_aux[64] = {};
+// per device: K1's side streams and their fork / join events (launch_k1)
+cudaStream_t g_k1s[64][3] = {};
+cudaEvent_t g_k1ev[64][4] = {};
 cudaEvent_t g_ev_lift[64] = {}, g_ev_plan[64] = {}, g_ev_fill[64] = {}, g_ev_k1[64] = {};
 struct PinRelease {
   cudaEvent_t ev;
@@ -1620,12 +1626,40 @@ cudaError_t launch_k1(int32_t n_segs, const int32_t *deg, const int32_t *coff, c
   k_deg_bounds<<<(n_segs + 1 + 255) / 256, 256, 0, st>>>(n_segs, d_degs, d_bnd);
   const int pg = std::min((n_segs + 127) / 128, 148 * PREP_SPLIT);
   const size_t sm = Sink::kStaged ? 128 * sizeof(typename Sink::Rec) : 0;
+#if K1_STREAMS
+  // the degree kernels run concurrently on side streams (forked from / joined
+  // back to `st`), so one kernel's last wave overlaps the next one's first
+  int dev = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!g_k1s[dev][0]) {
+    for (int i = 0; i < 3; ++i)
+      if ((e = cudaStreamCreateWithFlags(&g_k1s[dev][i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (int i = 0; i < 4; ++i)
+      if ((e = cudaEventCreateWithFlags(&g_k1ev[dev][i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  cudaStream_t *ss = g_k1s[dev];
+  if ((e = cudaEventRecord(g_k1ev[dev][3], st)) != cudaSuccess) return e;
+  for (int i = 0; i < 3; ++i)
+    if ((e = cudaStreamWaitEvent(ss[i], g_k1ev[dev][3], 0)) != cudaSuccess) return e;
+  k_prep_deg<5><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<4><<<pg, 128, sm, ss[0]>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<3><<<pg, 128, sm, ss[1]>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<2><<<pg, 128, sm, ss[2]>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_deg<1><<<pg, 128, sm, ss[2]>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
+  k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, sink, serr, d_order);
+  for (int i = 0; i < 3; ++i) {
+    if ((e = cudaEventRecord(g_k1ev[dev][i], ss[i])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, g_k1ev[dev][i], 0)) != cudaSuccess) return e;
+  }
+#else
   k_prep_deg<5><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_deg<4><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_deg<3><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_deg<2><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_deg<1><<<pg, 128, sm, st>>>(d_bnd, deg, coff, ctrl, w, sink, serr, d_order);
   k_prep_bad<<<std::min((n_segs + 255) / 256, 148), 256, 0, st>>>(d_bnd, sink, serr, d_order);
+#endif
   g_build_launches += 7;
   return cudaGetLastError();
 }
@@ -2257,6 +2291,7 @@ extern "C" wn_status_t wn_segment_prep(int32_t n_segs, const double *ctrl_uv, co
     return WN_ERR_ARG;
   }
   if (n_segs == 0) return WN_OK;
+  std::lock_guard<std::mutex> build_lock(g_build_mu);   // K1's side streams / events are shared with builds
   int dev = 0;
   WN_CUDA(cudaGetDevice(&dev));
   ensure_pool(dev);

@@ -1392,6 +1392,22 @@ __global__ void k_finish(int64_t n, const double *__restrict__ winding, uint8_t 
   }
 }
 
+// K3c over the hard-pair queue instead of the flag array: a query is PENDING
+// only if all its hard pairs are in the queue, so visiting the queue's entries
+// reaches every PENDING flag (1.8M entries instead of 82M flags on C5).  Several
+// entries of one query write the same final flag (idempotent).
+__global__ void k_finish_q(const HardEntry *__restrict__ hq, const int32_t *__restrict__ hq_count, int32_t hq_cap,
+                           const double *__restrict__ winding, uint8_t *__restrict__ flag, int rule) {
+  const int total = min(*hq_count, hq_cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int32_t q = hq[i].q;
+    if (flag[q] == FLAG_PENDING) {
+      const double w = winding[q];
+      flag[q] = isnan(w) ? (uint8_t)2 : classify(w, rule);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K4: bucketing by face (a3).  Histogram with warp-aggregated atomics and a
 // sortedness flag; scatter only when the batch is not grouped by face.
@@ -1540,6 +1556,13 @@ __global__ void k_grid_tiles(int32_t n_grid, int32_t tpg, int32_t qu, int64_t G,
 
 static thread_local int32_t g_launches = 0;
 
+// A/B switch (environment): WN_FINISH_Q=0 classifies by scanning the flag array
+static bool env_on(const char *name) {
+  const char *e = std::getenv(name);
+  return !(e && *e && atoi(e) == 0);
+}
+static bool finish_by_queue() { return env_on("WN_FINISH_Q"); }
+
 // K3 (phase 1, hard pairs, overflow, finish) on prepared tiles
 template <typename R>
 static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const int32_t *face_id, int max_tiles,
@@ -1570,13 +1593,14 @@ static wn_status_t launch_k3(wn_faces_t F, const QParams<R> &P, int64_t n, const
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, true><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters);
+    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, F->counters);   // (counts the on-boundary queries)
   } else {
     phase1(std::false_type{});
     if (em) WN_CUDA(cudaEventRecord(em, st));
     k_hard<R, false><<<hb, 256, 0, st>>>(P);
     k_overflow<R><<<148 * 4, 128, 0, st>>>(P, face_id, n);
-    k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr);
+    if (finish_by_queue()) k_finish_q<<<148 * 8, 256, 0, st>>>(P.hq, P.hq_count, P.hq_cap, P.winding, P.flag, P.rule);
+    else k_finish<<<148 * 8, 256, 0, st>>>(n, P.winding, P.flag, P.rule, nullptr);
   }
   launches += 4;
   if (F->timing_on) {

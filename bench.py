@@ -273,6 +273,20 @@ def run_reference(args, rank, world):
     return 0
 
 
+def _ncu_traffic():
+    """DRAM bytes per k_phase1 launch (dram__bytes_read.sum + dram__bytes_write.sum) from the committed
+    `ncu --set full` capture of the same workload (profiles/round2/k_phase1_traffic.json, written by
+    scripts/ncu_traffic.py); None if the file is absent.  Only `traffic` comes from it -- every other
+    roofline input is measured live."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "round2", "k_phase1_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return int(d["dram_read_bytes"] + d["dram_write_bytes"]), d.get("source", "profiles/round2/k_phase1_traffic.json")
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -531,8 +545,9 @@ def main():
     ach1 = w1 / (p1_avg / 1e3) / 1e9
     ach3 = (w1 + w2) / (k3_avg / 1e3) / 1e9
     lane_tests = cnt["pairs_tested"] + cnt["span_tests"]
+    traffic, traffic_src = _ncu_traffic()
     roofline = {"bound": "alu", "achieved": ach1, "peak": fp64_peak / 1e9, "unit": "G FP64-pipe lane-inst/s",
-                "frac": ach1 / (fp64_peak / 1e9), "traffic": None,
+                "frac": ach1 / (fp64_peak / 1e9), "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": "wn::k_phase1<double>", "kernel_ms": p1_avg, "kernel_share_of_step": p1_avg / ms_step,
                 "peak_source": "measured in this run: wn_measure_fp_peak (DFMA chains, lane inst/s) at %.0f MHz"
                                % fp64_mhz,

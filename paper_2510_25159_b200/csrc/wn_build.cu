@@ -511,7 +511,7 @@ __global__ void k_loop_face(int32_t n_faces, int32_t n_loops, const int32_t *__r
 // Homology class = round(closure / T).  Junctions that are not
 // bit-continuous after lifting are recorded as chain breaks.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_lift(int32_t n_loops, int32_t n_faces, int32_t n_segs,
+__global__ void __launch_bounds__(256, 4) k_lift(int32_t n_loops, int32_t n_faces, int32_t n_segs,
                                               const int32_t *__restrict__ loop_off,
                                               const int32_t *__restrict__ loop_face,
                                               const uint8_t *__restrict__ face_per, const double *__restrict__ face_dom,

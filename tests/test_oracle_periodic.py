@@ -104,6 +104,14 @@ def test_eq5_N_vs_2N_and_tile_periodicity(exact):
     ok = r1["comparable"] & r2["comparable"]
     assert ok.mean() > 0.9
     assert np.max(np.abs(r1["w"][ok] - r2["w"][ok])) < (1e-13 if exact else 1e-11)
+    # far truncations (N = 64 against 128) agree with the default N = 8:
+    # Eq. 5 does not depend on where the copies are cut off
+    r64 = oracle.query(wl, face_id=fid, uv=q, N5=64)
+    r128 = oracle.query(wl, face_id=fid, uv=q, N5=128)
+    okN = ok & r64["comparable"] & r128["comparable"]
+    assert okN.mean() > 0.9
+    assert np.max(np.abs(r64["w"][okN] - r128["w"][okN])) < (1e-12 if exact else 1e-10)
+    assert np.max(np.abs(r2["w"][okN] - r128["w"][okN])) < (1e-12 if exact else 1e-10)
     # tile periodicity: the unreduced point one period away gives the same value
     T = wl["face_domain"][fid, 1]
     r3 = oracle.query(wl, face_id=fid, uv=q + np.stack([T, 0 * T], 1), reduce=False)

@@ -401,7 +401,10 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
 constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classifies
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
 
-constexpr int HWB = 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
+#ifndef WN_P1_QPIPE
+#define WN_P1_QPIPE 1           // the next sub-tile's query points copied to shared memory (cp.async) during the sweep
+#endif
+constexpr int HWB = WN_P1_QPIPE ? 48 : 64;   // per-warp shared-memory buffer of hard pairs (flushed with one atomic)
 constexpr int HCHUNK = 32;   // hard pairs a k_hard warp reserves per atomic (one per lane: small queues stay spread)
 #ifndef WN_P1_PINF
 #define WN_P1_PINF 1            // the query's fp32 coordinates pinned in registers
@@ -467,12 +470,15 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
   constexpr bool F64 = sizeof(R) == 8;
   // records per staged chunk: 32 KB, or 28 KB when the chain-point parking
   // slots (4.2 KB) must fit the 48-KB static shared memory too
-  constexpr int RCH = (F64 ? 1024 : 2048) * (WN_P1_ZIDX ? 7 : 8) / 8;
+  constexpr int RCH = (F64 ? 1024 : 2048) * (WN_P1_ZIDX ? (WN_P1_QPIPE ? 27 : 28) : 32) / 32;
   __shared__ __align__(128) Hot<R> s_rec[RCH];
   __shared__ HardEntry s_hb[NWARP][HWB];
   __shared__ __align__(8) uint64_t s_bar;
 #if WN_P1_ZIDX
   __shared__ __align__(16) double2 s_park[NTH * QPL + NWARP];   // chain points parked across chunks
+#endif
+#if WN_P1_QPIPE
+  __shared__ __align__(16) double2 s_q[NTH * QPL];               // the thread's query points of the next sub-tile
 #endif
 
   if ((int)blockIdx.x >= *P.ntiles) return;               // uniform: no tile
@@ -744,6 +750,15 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     }
   }
 
+#if WN_P1_QPIPE
+  // Query pipeline (explicit batches whose position is the query index): while a
+  // sub-tile is swept, each thread's point of the next one travels to its
+  // shared-memory slot with an asynchronous 16-B copy, so the next prologue
+  // does not wait for global memory.
+  const bool qpipe = !GRID && !spatial && !unsorted && ((reinterpret_cast<uintptr_t>(P.uv) & 15) == 0);
+#else
+  constexpr bool qpipe = false;
+#endif
   // one unit = up to QU queries of face f, processed QTK at a time
   for (int sub = 0; sub < T.qcnt; sub += QTK) {
     bool valid[QPL];
@@ -766,12 +781,28 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           u = __dadd_rn(s_grid[0], __dmul_rn((double)iu + 0.5, s_grid[2]));   // = grid_coord(), bit for bit
           v = __dadd_rn(s_grid[1], __dmul_rn((double)iv + 0.5, s_grid[3]));
         } else {
-          u = P.uv[2 * (int64_t)qi[k]];
-          v = P.uv[2 * (int64_t)qi[k] + 1];
-          // the next sub-tile's point to L2 while this one is swept (given order
-          // or row tiles: the position is the query index)
-          if (!spatial && !unsorted && sub + QTK + lt[k] < T.qcnt)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(P.uv + 2 * (int64_t)(pos + QTK)));
+#if WN_P1_QPIPE
+          if (qpipe && sub > 0) {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(u), "=d"(v) : "r"(smem_u32(&s_q[t * QPL + k])) : "memory");
+          } else
+#endif
+          {
+            u = P.uv[2 * (int64_t)qi[k]];
+            v = P.uv[2 * (int64_t)qi[k] + 1];
+          }
+          // the next sub-tile's point: to this thread's shared slot (query
+          // pipeline; issued after (u, v) left the slot), else to L2
+          if (!spatial && !unsorted && sub + QTK + lt[k] < T.qcnt) {
+#if WN_P1_QPIPE
+            if (qpipe) {
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n\tcp.async.commit_group;" ::"r"(smem_u32(&s_q[t * QPL + k])),
+                           "l"(P.uv + 2 * (int64_t)(pos + QTK)), "d"(u), "d"(v)
+                           : "memory");
+            } else
+#endif
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(P.uv + 2 * (int64_t)(pos + QTK)));
+          }
         }
         if (!isfinite(u) || !isfinite(v)) {
           P.winding[qi[k]] = nan_d();

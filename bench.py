@@ -460,6 +460,25 @@ def main():
         e2e = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
 
+        # the same with the classification as the only result read back (h_winding = NULL)
+        def e2e_flags_step():
+            g = [t.to(dev, non_blocking=True) for t in h_geo]
+            fc = wn.Faces.build(*g, **kw)
+            fc.query_host(h_fid, h_uv, out=(None, h_f), sync=False, winding=False)
+            torch.cuda.current_stream(dev).synchronize()
+            fc.close()
+
+        e2e_flags_step()
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(ksteps):
+            e2e_flags_step()
+        b.record(st)
+        torch.cuda.synchronize()
+        et = max_over_ranks(a.elapsed_time(b), dist, dev)
+        e2e["flags_only"] = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                             "d2h_bytes_per_step": int(nq), "ms_per_step": et / ksteps}
+
     # ---- implicit-grid path (wn_query_grid, Sec. 5.4.3 tessellation): the same
     # C5 cell-centred 64x64 grids, generated in the kernel (0 B/query in) ----
     ng_ = len(wl["meta"]["grid_box"])
@@ -503,7 +522,7 @@ def main():
         cg = (ng_ + nch - 1) // nch
         gq = gn * gn
 
-        def grid_e2e_step():
+        def grid_e2e_step(copy_w=True):
             g = [t.to(dev, non_blocking=True) for t in h_geo]
             b = h_gb.to(dev, non_blocking=True)
             fc = wn.Faces.build(*g, **kw)
@@ -516,7 +535,8 @@ def main():
                 ev.record(st)
                 side.wait_event(ev)
                 with torch.cuda.stream(side):
-                    h_w[lo * gq:hi * gq].copy_(wnd[lo * gq:hi * gq], non_blocking=True)
+                    if copy_w:
+                        h_w[lo * gq:hi * gq].copy_(wnd[lo * gq:hi * gq], non_blocking=True)
                     h_f[lo * gq:hi * gq].copy_(flg[lo * gq:hi * gq], non_blocking=True)
             st.wait_stream(side)
             torch.cuda.current_stream(dev).synchronize()
@@ -535,6 +555,17 @@ def main():
         grid["e2e"] = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": int(sum(t.numel() * t.element_size() for t in h_geo) + h_gb.numel() * 8),
                        "d2h_bytes_per_step": int(d2h), "steps": ksteps, "ms_per_step": et / ksteps}
+        grid_e2e_step(False)
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(ksteps):
+            grid_e2e_step(False)
+        b.record(st)
+        torch.cuda.synchronize()
+        et = max_over_ranks(a.elapsed_time(b), dist, dev)
+        grid["e2e"]["flags_only"] = {"value": job_nq / (et / ksteps / 1e3), "unit": UNIT,
+                                     "h2d_bytes_per_step": grid["e2e"]["h2d_bytes_per_step"],
+                                     "d2h_bytes_per_step": int(nq), "ms_per_step": et / ksteps}
 
     # ---- roofline of the query kernel (algorithmic work / live time / measured peak) ----
     k3_avg = k3_ms / max(k3_n, 1)      # K3 (phase 1 + hard pairs + overflow + finish), CUDA events on the stream

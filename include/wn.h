@@ -158,7 +158,9 @@ wn_status_t wn_query(wn_faces_t faces, int64_t n, const int32_t *face_id, const 
  * host<->device transfers in both directions overlap the kernels.  Arguments
  * as for wn_query, but h_* are host pointers owned by the caller that must stay
  * valid until `stream` is synchronised; the results are in h_winding / h_flag
- * once it is.  Same per-query semantics as wn_query. */
+ * once it is.  Same per-query semantics as wn_query.  h_winding may be NULL:
+ * only the classification (the containment answer) is copied back,
+ * 1 B per query instead of 9. */
 wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t *h_face_id, const double *h_uv,
                           double *h_winding, uint8_t *h_flag, int64_t chunk, void *stream);
 

@@ -284,12 +284,13 @@ class Faces:
         self._keep_grid = (gf, gb)
         return QueryResult(wnd, flg)
 
-    def query_host(self, face_id, uv, out=None, chunk=0, stream=None, sync=True):
+    def query_host(self, face_id, uv, out=None, chunk=0, stream=None, sync=True, winding=True):
         """Streamed query of HOST arrays (wn_query_host): chunks are copied in,
         queried and copied back on overlapping streams.  face_id / uv: CPU
         tensors or numpy arrays (pinned CPU tensors give the overlap); returns
         (winding float64 [n], flag uint8 [n]) as CPU tensors, valid after the
-        stream is synchronised (sync=True waits)."""
+        stream is synchronised (sync=True waits).  winding=False: only the flags
+        come back (result.winding is None; out = (None, flag) or None)."""
         torch = _torch()
 
         def cpu(x, dt):
@@ -303,14 +304,17 @@ class Faces:
         n = fid.numel()
         if out is None:
             pin = fid.is_pinned()
-            wnd = torch.empty(n, dtype=torch.float64, pin_memory=pin)
+            wnd = torch.empty(n, dtype=torch.float64, pin_memory=pin) if winding else None
             flg = torch.empty(n, dtype=torch.uint8, pin_memory=pin)
         else:
             wnd, flg = out
+            if not winding:
+                wnd = None
         s = _stream(stream, self.device)
         with torch.cuda.device(self.device):
             rc = load().wn_query_host(self._h, n, C.c_void_p(fid.data_ptr()), C.c_void_p(q.data_ptr()),
-                                      C.c_void_p(wnd.data_ptr()), C.c_void_p(flg.data_ptr()), int(chunk), s)
+                                      C.c_void_p(wnd.data_ptr() if wnd is not None else None),
+                                      C.c_void_p(flg.data_ptr()), int(chunk), s)
         if rc != WN_OK:
             raise WNError(rc, last_error())
         if sync:

@@ -1920,7 +1920,7 @@ extern "C" wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t 
   if (!faces) { set_error("wn_query_host: NULL handle"); return WN_ERR_ARG; }
   if (n < 0) { set_error("wn_query_host: n < 0"); return WN_ERR_ARG; }
   if (n == 0) { g_launches = 0; return WN_OK; }
-  if (!h_face_id || !h_uv || !h_winding || !h_flag) { set_error("wn_query_host: NULL array"); return WN_ERR_ARG; }
+  if (!h_face_id || !h_uv || !h_flag) { set_error("wn_query_host: NULL array"); return WN_ERR_ARG; }
   const int dev = faces->device;
   WN_CUDA(cudaSetDevice(dev));
   ensure_pool(dev);
@@ -1971,7 +1971,8 @@ extern "C" wn_status_t wn_query_host(wn_faces_t faces, int64_t n, const int32_t 
     launches += g_launches;
     WN_CUDA(cudaEventRecord(ev_q[dev][k], st));
     WN_CUDA(cudaStreamWaitEvent(s_out[dev], ev_q[dev][k], 0));
-    WN_CUDA(cudaMemcpyAsync(h_winding + a, d_w[k], sizeof(double) * cn, cudaMemcpyDeviceToHost, s_out[dev]));
+    if (h_winding)   // (NULL: classification only -- the winding numbers stay on the device)
+      WN_CUDA(cudaMemcpyAsync(h_winding + a, d_w[k], sizeof(double) * cn, cudaMemcpyDeviceToHost, s_out[dev]));
     WN_CUDA(cudaMemcpyAsync(h_flag + a, d_fl[k], cn, cudaMemcpyDeviceToHost, s_out[dev]));
     WN_CUDA(cudaEventRecord(ev_out[dev][k], s_out[dev]));
   }

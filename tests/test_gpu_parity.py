@@ -308,6 +308,10 @@ def test_query_host_streamed_equals_device():
         r = faces.query_host(fid, uv, chunk=chunk)
         assert np.array_equal(r.flag.numpy(), rf), chunk
         assert np.array_equal(np.nan_to_num(r.winding.numpy(), nan=9.0), np.nan_to_num(rw, nan=9.0)), chunk
+    # classification only (h_winding = NULL): the same flags, no winding copy
+    r = faces.query_host(torch.from_numpy(wl["face_id"]).pin_memory(), torch.from_numpy(wl["uv"]).pin_memory(),
+                         chunk=7777, winding=False)
+    assert r.winding is None and np.array_equal(r.flag.numpy(), rf)
     faces.close()
 
 

@@ -37,7 +37,8 @@ def build(force=False, verbose=False, out=None, defines=()):
         print(r.stderr)
     if not out:
         with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-            fh.write(r.stderr)
+            # (without the compile times: the file then changes only when the code does)
+            fh.write("".join(l for l in r.stderr.splitlines(True) if "Compile time" not in l))
     os.replace(tmp, target)
     return target
 

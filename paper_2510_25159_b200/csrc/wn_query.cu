@@ -401,6 +401,9 @@ __device__ __forceinline__ float fdist_ftz(float dx, float dy) {
 constexpr uint8_t FLAG_PENDING = 0xFF;    // hard pairs queued: k_finish classifies
 constexpr uint8_t FLAG_OVERFLOW = 0xFE;   // a hard pair did not fit the queue: k_overflow recomputes
 
+#ifndef WN_P1_INTEPI
+#define WN_P1_INTEPI 1          // integer classification when the query met no line and no angle term
+#endif
 #ifndef WN_P1_QPIPE
 #define WN_P1_QPIPE 1           // the next sub-tile's query points copied to shared memory (cp.async) during the sweep
 #endif
@@ -847,7 +850,9 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
     int up[QPL];                   // side of the branch cut of the previous chain point (0/1)
     bool onb[QPL];
     int skip_end[QPL];             // query inactive (culled / pruned subtree) while gr < skip_end
-    int xs[QPL], halves[QPL];
+    // xs: crossings in the low 16 bits, line half-turns (+-1 per LINE / SLINE
+    // record) in the high 16 -- one register for both counts
+    int xs[QPL];
     double fr[QPL];
 #pragma unroll
     for (int k = 0; k < QPL; ++k) {
@@ -860,7 +865,7 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
       up[k] = 0;
       onb[k] = false;
       skip_end[k] = 0;
-      xs[k] = halves[k] = 0;
+      xs[k] = 0;
       fr[k] = 0.0;
       pend[k] = 0;
     }
@@ -1063,12 +1068,12 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           for (int k = 0; k < QPL; ++k) {
             const double q = (meta & F_AXISV) ? px[k] : py[k];
             const bool left = (meta & F_GE) ? (q >= h.x) : (q <= h.x);
-            if (act[k]) halves[k] += left ? 1 : -1;
+            if (act[k]) xs[k] += left ? (1 << 16) : -(1 << 16);
           }
         } else if (kind == K_SLINE) {
 #pragma unroll
           for (int k = 0; k < QPL; ++k)
-            if (act[k]) halves[k] += sline_left(meta, h.x, h.y, px[k], py[k], dom) ? 1 : -1;
+            if (act[k]) xs[k] += sline_left(meta, h.x, h.y, px[k], py[k], dom) ? (1 << 16) : -(1 << 16);
         } else if (kind == K_XCH || kind == K_NCH || kind == K_CLOSEG) {
 #pragma unroll
           for (int k = 0; k < QPL; ++k) {
@@ -1127,9 +1132,20 @@ __global__ void __launch_bounds__(NTH, WN_P1_MINB) k_phase1(QParams<R> P) {
           P.flag[qi[k]] = 2;
           if (COUNT) atomicAdd(P.counters + 7, 1ull);
         } else {
-          const double w = (double)xs[k] + 0.5 * (double)halves[k] + fr[k] * (1.0 / TWO_PI);
+          double w;
+          uint8_t fl;
+          const int xc = (int)(int16_t)(xs[k] & 0xFFFF), halves = (xs[k] - xc) >> 16;
+          if (WN_P1_INTEPI && halves == 0 && fr[k] == 0.0) {
+            // closed loops only: omega is the integer crossing count (the same
+            // bits as the general formula, without its double-precision rounding)
+            w = (double)xc;
+            fl = (P.rule == 0) ? (xc != 0) : (xc >= 1);
+          } else {
+            w = (double)xc + 0.5 * (double)halves + fr[k] * (1.0 / TWO_PI);
+            fl = classify(w, P.rule);
+          }
           P.winding[qi[k]] = w;
-          P.flag[qi[k]] = (pend[k] & 2) ? FLAG_OVERFLOW : (pend[k] & 1) ? FLAG_PENDING : classify(w, P.rule);
+          P.flag[qi[k]] = (pend[k] & 2) ? FLAG_OVERFLOW : (pend[k] & 1) ? FLAG_PENDING : fl;
         }
       }
     }
